@@ -1,0 +1,245 @@
+/* rhosolve-b200 C ABI.
+ *
+ * The drop-in boundary for the steady-state hot path of the reference
+ * `rhosolve` package (arXiv 1504.06768).  The reference's own native seam is
+ * its kernel module (pkg/src/rhosolve/kernels/__init__.py:19-36), four
+ * functions bound from Cython: csr_matvec, lower_solve, upper_solve and
+ * factorize (_ckernels.pyx:34,53,70,144).  This library exports device
+ * equivalents of those four plus the other stages of the path
+ * (liouville.py assembly/shift/modify, ordering.rcm, sparse.permute,
+ * factor.solve_lu, the krylov / steady drivers and _postprocess), each citing
+ * the reference interface it replaces.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers (cudaMalloc / torch tensors),
+ *     except where a parameter is documented as host.
+ *   - complex128 is rs_complex {double re, im;}: the numpy complex128 layout.
+ *   - Indices are int32 (every configuration has nnz < 2^31).
+ *   - Batches: `nsys` independent systems of equal order n are stored
+ *     block-diagonally.  row_ptr spans nsys*n rows with absolute positions,
+ *     column indices are local (0..n-1), vectors are nsys*n long.  A single
+ *     system is nsys = 1.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Every function returns 0 (RS_OK) or a negative RS_ERR_* code and never
+ *     throws; rs_last_error() describes the last failure of this thread.
+ *     Numerical outcomes the reference reports as values (zero pivot step,
+ *     Krylov breakdown, ...) are returned through output arguments, exactly
+ *     as the reference returns them (fail_col, IterResult flags).
+ *   - No function falls back to a CPU implementation.
+ */
+#ifndef RHOSOLVE_B200_H
+#define RHOSOLVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+#define RS_OK 0
+#define RS_ERR_ARG -1
+#define RS_ERR_CUDA -2
+#define RS_ERR_ALLOC -3
+#define RS_ERR_BREAKDOWN -4
+#define RS_ERR_NONFINITE -5
+#define RS_ERR_OVERFLOW -6
+#define RS_ERR_UNSUPPORTED -7
+
+typedef struct rs_complex {
+  double re;
+  double im;
+} rs_complex;
+
+int rs_abi_version(void);
+const char* rs_last_error(void);
+
+/* ---- kernel seam (kernels/__init__.py:19-36) ---------------------------- */
+
+/* y = A x.  Replaces csr_matvec (_ckernels.pyx:34-50): row-sequential sum,
+ * plain complex products, empty rows give 0 -- bit-identical. */
+int rs_csr_matvec(int32_t nsys, int32_t n, const int32_t* row_ptr,
+                  const int32_t* col_idx, const rs_complex* values,
+                  const rs_complex* x, rs_complex* y, void* stream);
+
+/* Left-looking LU / ILUTP.  Replaces factorize (_ckernels.pyx:144-385) as
+ * called by factor._factor (factor.py:70-112).
+ *   A is given column-major: Ap/Ai/Ax = CSR of A^T (sparse.transpose(a)),
+ *   q (nullable) = elimination column order, drop_tol, fill_cap (-1 = none),
+ *   row_norms (nullable unless drop_tol > 0) = max |re|+|im| per row.
+ * Outputs per system b (raw CSC exactly as the reference returns them):
+ *   Lp/Up [nsys*(n+1)], Li/Lx at b*capL, Ui/Ux at b*capU, pinv [nsys*n].
+ * state (device, int32 [3*nsys]) must be zeroed before the first call:
+ *   state[3b] = 1 done, 2 zero pivot (state[3b+1] = fail_col, the
+ *   reference's return value), 3 out of capacity (state[3b+1] = column to
+ *   resume from: grow the buffers, copy, call again with the same state).
+ * L row indices are remapped to pivotal order on completion, as in the
+ * reference. */
+int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
+                 const rs_complex* Ax, const int32_t* q, double drop_tol,
+                 int32_t fill_cap, const double* row_norms, int32_t* Lp,
+                 int32_t* Li, rs_complex* Lx, int64_t capL, int32_t* Up,
+                 int32_t* Ui, rs_complex* Ux, int64_t capU, int32_t* pinv,
+                 int32_t* state, void* stream);
+
+/* Row-oriented triangular factors for the solves.  From the raw CSC of
+ * rs_factorize, builds the strictly-lower L and strictly-upper U in CSR
+ * (ascending columns) plus rdiag = recipc(U_kk).  Call with L_ci == NULL to
+ * get only the row pointers and *L_nnz / *U_nnz (host) for allocation. */
+int rs_factor_rows(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li,
+                   const rs_complex* Lx, int64_t capL, const int32_t* Up,
+                   const int32_t* Ui, const rs_complex* Ux, int64_t capU,
+                   int32_t* L_rp, int32_t* L_ci, rs_complex* L_v, int64_t* L_nnz,
+                   int32_t* U_rp, int32_t* U_ci, rs_complex* U_v,
+                   rs_complex* rdiag, int64_t* U_nnz, void* stream);
+
+/* x = M^{-1} b through the factors: y[pinv] = b; lower_solve; upper_solve;
+ * x = y.  Replaces factor.solve_lu (factor.py:137-149) with
+ * lower_solve/upper_solve (_ckernels.pyx:53-85); bit-identical. */
+int rs_lu_solve(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t* L_rp,
+                const int32_t* L_ci, const rs_complex* L_v, const int32_t* U_rp,
+                const int32_t* U_ci, const rs_complex* U_v, const rs_complex* rdiag,
+                const rs_complex* b, rs_complex* x, void* stream);
+
+/* ---- superoperator (liouville.py) ---------------------------------------- */
+
+/* build_liouvillian (liouville.py:54-77), bit-identical structure and values.
+ * H and the K collapse operators are D x D CSR on the device; C_rp/C_ci/C_v/
+ * C_nnz are HOST arrays of K device pointers / sizes.  *herm_dev (host)
+ * receives max|H - H^dag| (the reference rejects H above 1e-12).
+ * Two passes: with out_ci == NULL fills out_rp and *nnz (host); then call
+ * again with out_ci/out_v allocated for *nnz entries. */
+int rs_liouvillian(int32_t D, const int32_t* H_rp, const int32_t* H_ci,
+                   const rs_complex* H_v, int64_t H_nnz, int32_t K,
+                   const int32_t* const* C_rp, const int32_t* const* C_ci,
+                   const rs_complex* const* C_v, const int64_t* C_nnz,
+                   double* herm_dev, int32_t* out_rp, int32_t* out_ci,
+                   rs_complex* out_v, int64_t* nnz, void* stream);
+
+/* shift (liouville.py:80-96): L - sigma I, every diagonal stored.  Two passes
+ * as above (out_ci == NULL: row pointers and *nnz only). */
+int rs_shift(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+             const rs_complex* v, double sigma, int32_t* out_rp, int32_t* out_ci,
+             rs_complex* out_v, int64_t* nnz, void* stream);
+
+/* default_weight (liouville.py:99-111), one weight per system into w (device).
+ * mode 0 = "abs", 1 = "signed". */
+int rs_default_weight(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+                      const rs_complex* v, int32_t mode, double* w, void* stream);
+
+/* build_modified (liouville.py:114-138): row 0 += w at columns k(D+1).
+ * w is a device array of nsys weights.  Two passes as above. */
+int rs_trace_modify(int32_t nsys, int32_t n, int32_t D, const int32_t* rp,
+                    const int32_t* ci, const rs_complex* v, const double* w,
+                    int32_t* out_rp, int32_t* out_ci, rs_complex* out_v,
+                    int64_t* nnz, void* stream);
+
+/* ---- ordering and permutation -------------------------------------------- */
+
+/* ordering.rcm (ordering.py:82-118), bit-identical: forward/inverse int32
+ * [nsys*n], local indices (Permutation.forward / .inverse). */
+int rs_rcm(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+           int32_t* forward, int32_t* inverse, void* stream);
+
+/* sparse.permute(a, p, p) (sparse.py:276-282): B[f[i], f[j]] = A[i, j]. */
+int rs_permute(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+               const rs_complex* v, const int32_t* forward, const int32_t* inverse,
+               int32_t* out_rp, int32_t* out_ci, rs_complex* out_v, void* stream);
+
+/* gather != 0: out[i] = x[forward[i]] (solution unpermute, steady.py:249-250);
+ * gather == 0: out[forward[i]] = x[i] (rhs permute, steady.py:89-94). */
+int rs_permute_vector(int32_t nsys, int32_t n, const rs_complex* x,
+                      const int32_t* forward, rs_complex* out, int32_t gather,
+                      void* stream);
+
+/* CSR transpose (sparse.transpose, sparse.py:216-219); values nullable. */
+int rs_transpose(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+                 const rs_complex* v, int32_t* out_rp, int32_t* out_ci,
+                 rs_complex* out_v, void* stream);
+
+/* factor.py:84-88: row_norms[r] = max |re|+|im| over row r. */
+int rs_row_norms(int32_t nsys, int32_t n, const int32_t* rp, const rs_complex* v,
+                 double* row_norms, void* stream);
+
+/* ---- steady-state drivers (steady.py / krylov.py) ------------------------- */
+
+enum rs_solve_mode {
+  RS_INV_DIRECT = 0,   /* inverse_power(inner="direct")          steady.py:203-208 */
+  RS_INV_BICGSTAB = 1, /* inverse_power(inner="iterative", "bicgstab") */
+  RS_INV_GMRES = 2,    /* inverse_power(inner="iterative", "gmres")    */
+  RS_LIN_DIRECT = 3,   /* solve_direct: one solve_lu                steady.py:116-134 */
+  RS_LIN_BICGSTAB = 4, /* solve_iterative(solver="bicgstab")       steady.py:137-168 */
+  RS_LIN_GMRES = 5     /* solve_iterative(solver="gmres")          */
+};
+
+/* status codes written to rs_solve_stats.status */
+enum rs_solve_status {
+  RS_SOLVE_OK = 0,
+  RS_SOLVE_INNER_BREAKDOWN = 1,   /* InnerSolverError, steady.py:509-512 */
+  RS_SOLVE_INNER_NONFINITE = 2,   /* InnerSolverError, steady.py:509-512 */
+  RS_SOLVE_INNER_NO_PROGRESS = 3, /* InnerSolverError, steady.py:513-514 */
+  RS_SOLVE_UNUSABLE_VECTOR = 4,   /* InnerSolverError, steady.py:525-526 */
+  RS_SOLVE_POWER_NOT_CONVERGED = 5 /* PowerIterationError, steady.py:537-539 */
+};
+
+typedef struct rs_solve_stats {
+  int32_t status;
+  int32_t outer;       /* inverse-power outer iterations */
+  int32_t inner_last;  /* Krylov iterations of the last inner solve */
+  int32_t inner_total;
+  int32_t converged;   /* IterResult.converged (linear modes) */
+  int32_t breakdown;   /* IterResult.breakdown (linear modes) */
+  double final_residual;
+  double condest;      /* factor.condest (factor.py:152-157) when requested */
+} rs_solve_stats;
+
+typedef struct rs_solver_args {
+  int32_t n;
+  int32_t nsys;
+  int32_t mode;    /* rs_solve_mode */
+  int32_t threads; /* CTA size, multiple of 32 (0 = default 512) */
+  /* solver-ready (shifted or modified), ordered system matrix */
+  const int32_t* A_rp;
+  const int32_t* A_ci;
+  const rs_complex* A_v;
+  /* plain ordered matrix, for the inverse-power residual test */
+  const int32_t* P_rp;
+  const int32_t* P_ci;
+  const rs_complex* P_v;
+  /* preconditioner from rs_factor_rows (all NULL: no preconditioner) */
+  const int32_t* L_rp;
+  const int32_t* L_ci;
+  const rs_complex* L_v;
+  const int32_t* U_rp;
+  const int32_t* U_ci;
+  const rs_complex* U_v;
+  const rs_complex* rdiag;
+  const int32_t* pinv;
+  const rs_complex* rhs; /* rhs (linear) or un-normalised start vector (inverse power) */
+  rs_complex* x;         /* solution in the ordered coordinates */
+  rs_solve_stats* stats; /* device, nsys entries */
+  double tol;
+  int32_t max_iter;
+  int32_t restart_m;
+  int32_t max_outer;
+  int32_t want_condest;
+} rs_solver_args;
+
+/* One launch runs the whole solve of every system on the device. */
+int rs_steady_solve(const rs_solver_args* args, void* stream);
+
+/* steady._postprocess (steady.py:62-71) with the optional unpermute:
+ * rho (D x D row-major per system), residual (device, nsys doubles),
+ * trace (device, nullable).  forward == NULL on the natural ordering. */
+int rs_postprocess(int32_t nsys, int32_t D, const rs_complex* x,
+                   const int32_t* forward, const int32_t* plain_rp,
+                   const int32_t* plain_ci, const rs_complex* plain_v,
+                   rs_complex* rho, double* residual, rs_complex* trace,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RHOSOLVE_B200_H */

@@ -1,0 +1,309 @@
+// extern "C" entry points declared in include/rhosolve_b200.h.  Thin
+// argument validation + dispatch to the launchers; no compute on the host and
+// no fallback path.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/rhosolve_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "solver.cuh"
+
+namespace rs {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+// defined in the other translation units
+int csr_permute(int B, int32_t n, const int32_t* rp, const int32_t* ci, const double2* v,
+                const int32_t* fwd, const int32_t* inv, int32_t* out_rp, int32_t* out_ci,
+                double2* out_v, cudaStream_t st);
+int csr_shift(int B, int32_t n, const int32_t* rp, const int32_t* ci, const double2* v,
+              double sigma, int32_t* out_rp, int32_t* out_ci, double2* out_v,
+              int64_t* nnz_out, cudaStream_t st);
+int csr_modify(int B, int32_t n, int32_t D, const int32_t* rp, const int32_t* ci,
+               const double2* v, const double* w, int32_t* out_rp, int32_t* out_ci,
+               double2* out_v, int64_t* nnz_out, cudaStream_t st);
+int csr_default_weight(int B, int32_t n, const int32_t* rp, const int32_t* ci,
+                       const double2* v, int signed_mode, double* w, cudaStream_t st);
+int csr_row_norms(int64_t nrows, const int32_t* rp, const double2* v, double* rn,
+                  cudaStream_t st);
+int factor_to_csr(int B, int32_t n, const int32_t* cp, const int32_t* ri, const double2* rv,
+                  int64_t cap, int lower, int32_t* out_rp, int32_t* out_ci, double2* out_v,
+                  double2* rU, int64_t* nnz_out, cudaStream_t st);
+int liouvillian_assemble(int32_t D, const int32_t* Hrp, const int32_t* Hci, const double2* Hv,
+                         int64_t Hnnz, int32_t K, const int32_t* const* Crp,
+                         const int32_t* const* Cci, const double2* const* Cv,
+                         const int64_t* Cnnz, double* herm_dev, int32_t* out_rp,
+                         int32_t* out_ci, double2* out_v, int64_t* nnz_out, cudaStream_t st);
+int rcm_order(int B, int32_t n, const int32_t* rp, const int32_t* ci, int32_t* fwd,
+              int32_t* inv, cudaStream_t st);
+int postprocess(int B, int32_t D, const double2* x, const int32_t* fwd, const int32_t* Lrp,
+                const int32_t* Lci, const double2* Lv, double2* rho, double* residual,
+                double2* trace_out, cudaStream_t st);
+int permute_vector(int B, int32_t n, const double2* x, const int32_t* fwd, double2* out,
+                   int gather, cudaStream_t st);
+
+}  // namespace rs
+
+using namespace rs;
+
+#define S(stream) reinterpret_cast<cudaStream_t>(stream)
+#define C2(p) reinterpret_cast<const double2*>(p)
+#define M2(p) reinterpret_cast<double2*>(p)
+
+extern "C" {
+
+int rs_abi_version(void) { return RS_ABI_VERSION; }
+const char* rs_last_error(void) { return g_err; }
+
+int rs_csr_matvec(int32_t nsys, int32_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                  const rs_complex* values, const rs_complex* x, rs_complex* y, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  if (!nsys || !n) return RS_OK;
+  RS_CHECK_ARG(row_ptr && x && y, "null pointer");
+  return launch_spmv((int64_t)nsys * n, n, row_ptr, col_idx, C2(values), C2(x), M2(y), S(stream));
+}
+
+int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
+                 const rs_complex* Ax, const int32_t* q, double drop_tol, int32_t fill_cap,
+                 const double* row_norms, int32_t* Lp, int32_t* Li, rs_complex* Lx,
+                 int64_t capL, int32_t* Up, int32_t* Ui, rs_complex* Ux, int64_t capU,
+                 int32_t* pinv, int32_t* state, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  RS_CHECK_ARG(drop_tol >= 0.0, "drop tolerance must be >= 0");
+  RS_CHECK_ARG(!(drop_tol > 0.0) || row_norms, "row_norms required when drop_tol > 0");
+  RS_CHECK_ARG(capL >= n && capU >= n, "factor capacity below n");
+  if (!nsys || !n) return RS_OK;
+  cudaStream_t st = S(stream);
+  const int64_t N = (int64_t)nsys * n;
+  FactorArgs a{};
+  a.n = n;
+  a.B = nsys;
+  a.Ap = Ap;
+  a.Ai = Ai;
+  a.Ax = C2(Ax);
+  a.q = q;
+  a.rn = row_norms;
+  a.drop_tol = drop_tol;
+  a.fill_cap = fill_cap;
+  a.Lp = Lp;
+  a.Li = Li;
+  a.Lx = M2(Lx);
+  a.capL = capL;
+  a.Up = Up;
+  a.Ui = Ui;
+  a.Ux = M2(Ux);
+  a.capU = capU;
+  a.pinv = pinv;
+  a.state = state;
+  a.smem_mode = ilutp_fits_smem(n) ? 1 : 0;
+  const int nwords = (n + 31) / 32;
+  // scratch: x, flag, prow, bits, pattern, urow, uval, lrow, ukeep, lkeep
+  size_t bytes = 0;
+  auto take = [&](size_t b) {
+    size_t o = bytes;
+    bytes += (b + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t o_x = a.smem_mode ? 0 : take(16 * N);
+  const size_t o_flag = a.smem_mode ? 0 : take(4 * N);
+  const size_t o_bits = a.smem_mode ? 0 : take(4 * (size_t)nwords * nsys);
+  const size_t o_prow = take(4 * N);
+  const size_t o_pat = take(4 * N);
+  const size_t o_urow = take(4 * N);
+  const size_t o_uval = take(16 * N);
+  const size_t o_lrow = take(4 * N);
+  const size_t o_uk = take(N);
+  const size_t o_lk = take(N);
+  unsigned char* ws = nullptr;
+  RS_CUDA_TRY(cudaMallocAsync(&ws, bytes, st));
+  if (!a.smem_mode) {
+    a.wx = reinterpret_cast<double2*>(ws + o_x);
+    a.wflag = reinterpret_cast<int32_t*>(ws + o_flag);
+    a.wbits = reinterpret_cast<uint32_t*>(ws + o_bits);
+  }
+  a.prow = reinterpret_cast<int32_t*>(ws + o_prow);
+  a.wpat = reinterpret_cast<int32_t*>(ws + o_pat);
+  a.wurow = reinterpret_cast<int32_t*>(ws + o_urow);
+  a.wuval = reinterpret_cast<double2*>(ws + o_uval);
+  a.wlrow = reinterpret_cast<int32_t*>(ws + o_lrow);
+  a.wukeep = ws + o_uk;
+  a.wlkeep = ws + o_lk;
+  // prow is scratch: a resumed launch rebuilds it as the inverse of pinv.
+  const int rc = launch_ilutp(a, st);
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
+int rs_factor_rows(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li,
+                   const rs_complex* Lx, int64_t capL, const int32_t* Up, const int32_t* Ui,
+                   const rs_complex* Ux, int64_t capU, int32_t* L_rp, int32_t* L_ci,
+                   rs_complex* L_v, int64_t* L_nnz, int32_t* U_rp, int32_t* U_ci,
+                   rs_complex* U_v, rs_complex* rdiag, int64_t* U_nnz, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  cudaStream_t st = S(stream);
+  RS_TRY(factor_to_csr(nsys, n, Lp, Li, C2(Lx), capL, 1, L_rp, L_ci, M2(L_v), nullptr, L_nnz,
+                       st));
+  RS_TRY(factor_to_csr(nsys, n, Up, Ui, C2(Ux), capU, 0, U_rp, U_ci, M2(U_v), M2(rdiag), U_nnz,
+                       st));
+  return RS_OK;
+}
+
+int rs_lu_solve(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t* L_rp,
+                const int32_t* L_ci, const rs_complex* L_v, const int32_t* U_rp,
+                const int32_t* U_ci, const rs_complex* U_v, const rs_complex* rdiag,
+                const rs_complex* b, rs_complex* x, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  SolverArgs a{};
+  a.n = n;
+  a.B = nsys;
+  a.Lrp = L_rp;
+  a.Lci = L_ci;
+  a.Lv = C2(L_v);
+  a.Urp = U_rp;
+  a.Uci = U_ci;
+  a.Uv = C2(U_v);
+  a.rU = C2(rdiag);
+  a.pinv = pinv;
+  a.rhs = C2(b);
+  a.xout = M2(x);
+  return launch_lu_solve(a, S(stream));
+}
+
+int rs_liouvillian(int32_t D, const int32_t* H_rp, const int32_t* H_ci, const rs_complex* H_v,
+                   int64_t H_nnz, int32_t K, const int32_t* const* C_rp,
+                   const int32_t* const* C_ci, const rs_complex* const* C_v,
+                   const int64_t* C_nnz, double* herm_dev, int32_t* out_rp, int32_t* out_ci,
+                   rs_complex* out_v, int64_t* nnz, void* stream) {
+  RS_CHECK_ARG(D >= 1, "hilbert dimension must be >= 1");
+  RS_CHECK_ARG(K >= 0, "negative collapse operator count");
+  RS_CHECK_ARG((int64_t)D * D < ((int64_t)1 << 31), "D*D exceeds int32 indexing");
+  return liouvillian_assemble(D, H_rp, H_ci, C2(H_v), H_nnz, K, C_rp, C_ci,
+                              reinterpret_cast<const double2* const*>(C_v), C_nnz, herm_dev,
+                              out_rp, out_ci, M2(out_v), nnz, S(stream));
+}
+
+int rs_shift(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, const rs_complex* v,
+             double sigma, int32_t* out_rp, int32_t* out_ci, rs_complex* out_v, int64_t* nnz,
+             void* stream) {
+  RS_CHECK_ARG(sigma != 0.0, "sigma must be nonzero");
+  return csr_shift(nsys, n, rp, ci, C2(v), sigma, out_rp, out_ci, M2(out_v), nnz, S(stream));
+}
+
+int rs_default_weight(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+                      const rs_complex* v, int32_t mode, double* w, void* stream) {
+  RS_CHECK_ARG(mode == 0 || mode == 1, "unknown weight mode");
+  return csr_default_weight(nsys, n, rp, ci, C2(v), mode, w, S(stream));
+}
+
+int rs_trace_modify(int32_t nsys, int32_t n, int32_t D, const int32_t* rp, const int32_t* ci,
+                    const rs_complex* v, const double* w, int32_t* out_rp, int32_t* out_ci,
+                    rs_complex* out_v, int64_t* nnz, void* stream) {
+  RS_CHECK_ARG((int64_t)D * D == n, "n must equal D*D");
+  return csr_modify(nsys, n, D, rp, ci, C2(v), w, out_rp, out_ci, M2(out_v), nnz, S(stream));
+}
+
+int rs_rcm(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, int32_t* forward,
+           int32_t* inverse, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  if (!nsys || !n) return RS_OK;
+  return rcm_order(nsys, n, rp, ci, forward, inverse, S(stream));
+}
+
+int rs_permute(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, const rs_complex* v,
+               const int32_t* forward, const int32_t* inverse, int32_t* out_rp, int32_t* out_ci,
+               rs_complex* out_v, void* stream) {
+  if (!nsys || !n) return RS_OK;
+  return csr_permute(nsys, n, rp, ci, C2(v), forward, inverse, out_rp, out_ci, M2(out_v),
+                     S(stream));
+}
+
+int rs_permute_vector(int32_t nsys, int32_t n, const rs_complex* x, const int32_t* forward,
+                      rs_complex* out, int32_t gather, void* stream) {
+  RS_CHECK_ARG(x != out, "permute_vector cannot run in place");
+  return permute_vector(nsys, n, C2(x), forward, M2(out), gather, S(stream));
+}
+
+int rs_transpose(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+                 const rs_complex* v, int32_t* out_rp, int32_t* out_ci, rs_complex* out_v,
+                 void* stream) {
+  if (!nsys || !n) return RS_OK;
+  return csr_transpose(nsys, n, rp, ci, C2(v), out_rp, out_ci, M2(out_v), S(stream));
+}
+
+int rs_row_norms(int32_t nsys, int32_t n, const int32_t* rp, const rs_complex* v,
+                 double* row_norms, void* stream) {
+  return csr_row_norms((int64_t)nsys * n, rp, C2(v), row_norms, S(stream));
+}
+
+int rs_steady_solve(const rs_solver_args* p, void* stream) {
+  RS_CHECK_ARG(p != nullptr, "null args");
+  RS_CHECK_ARG(p->n >= 0 && p->nsys >= 0, "negative size");
+  RS_CHECK_ARG(p->mode >= RS_INV_DIRECT && p->mode <= RS_LIN_GMRES, "unknown mode");
+  RS_CHECK_ARG(p->tol > 0.0, "tol must be > 0");
+  RS_CHECK_ARG(p->max_iter >= 1, "max_iter must be >= 1");
+  RS_CHECK_ARG(p->restart_m >= 1, "restart_m must be >= 1");
+  RS_CHECK_ARG(p->mode < RS_INV_DIRECT + 3 ? p->P_rp != nullptr : true,
+               "inverse power needs the plain matrix");
+  if (!p->nsys || !p->n) return RS_OK;
+  cudaStream_t st = S(stream);
+  SolverArgs a{};
+  a.n = p->n;
+  a.B = p->nsys;
+  a.mode = p->mode;
+  a.threads = p->threads > 0 ? p->threads : 512;
+  RS_CHECK_ARG(a.threads % 32 == 0 && a.threads <= 512, "threads must be a multiple of 32, <= 512");
+  a.Arp = p->A_rp;
+  a.Aci = p->A_ci;
+  a.Av = C2(p->A_v);
+  a.Prp = p->P_rp;
+  a.Pci = p->P_ci;
+  a.Pv = C2(p->P_v);
+  a.Lrp = p->L_rp;
+  a.Lci = p->L_ci;
+  a.Lv = C2(p->L_v);
+  a.Urp = p->U_rp;
+  a.Uci = p->U_ci;
+  a.Uv = C2(p->U_v);
+  a.rU = C2(p->rdiag);
+  a.pinv = p->pinv;
+  a.rhs = C2(p->rhs);
+  a.xout = M2(p->x);
+  a.stats = reinterpret_cast<SolveStats*>(p->stats);
+  a.tol = p->tol;
+  a.max_iter = p->max_iter;
+  a.restart_m = p->restart_m;
+  a.max_outer = p->max_outer > 0 ? p->max_outer : 50;
+  a.want_condest = p->want_condest;
+  int dev, max_smem;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t flag_bytes = ((size_t)a.n + 15) & ~(size_t)15;
+  a.y_in_smem = (flag_bytes + 16 * (size_t)a.n + 4096 <= (size_t)max_smem) ? 1 : 0;
+  a.work_stride = solver_work_stride(a.n, a.restart_m);
+  double2* work = nullptr;
+  RS_CUDA_TRY(cudaMallocAsync(&work, sizeof(double2) * a.work_stride * a.B, st));
+  a.work = work;
+  int rc = launch_steady_solver(a, st);
+  cudaFreeAsync(work, st);
+  return rc;
+}
+
+int rs_postprocess(int32_t nsys, int32_t D, const rs_complex* x, const int32_t* forward,
+                   const int32_t* plain_rp, const int32_t* plain_ci, const rs_complex* plain_v,
+                   rs_complex* rho, double* residual, rs_complex* trace, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && D >= 1, "bad size");
+  if (!nsys) return RS_OK;
+  return postprocess(nsys, D, C2(x), forward, plain_rp, plain_ci, C2(plain_v), M2(rho),
+                     residual, M2(trace), S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// Internal launcher declarations shared by the .cu translation units.
+#pragma once
+#include "common.cuh"
+
+namespace rs {
+
+// ---- spmv.cu -------------------------------------------------------------
+int launch_spmv(int64_t nrows, int32_t n, const int32_t* rp, const int32_t* ci,
+                const double2* v, const double2* x, double2* y, cudaStream_t st);
+
+// ---- csr.cu (structure utilities) -----------------------------------------
+// Exclusive scan of int32 counts into int32 offsets (n+1 outputs); returns
+// the total through *total_host when non-null (synchronises the stream).
+int scan_counts(const int32_t* counts, int32_t* offsets, int64_t n,
+                int64_t* total_host, cudaStream_t st);
+// Transpose of a block-diagonal batch of B n-by-n CSR matrices.  Output
+// rows hold their entries in ascending column order (counting sort that is
+// stable in the input row order), matching sparse.transpose / from_coo.
+int csr_transpose(int B, int32_t n, const int32_t* rp, const int32_t* ci,
+                  const double2* v, int32_t* out_rp, int32_t* out_ci,
+                  double2* out_v, cudaStream_t st);
+
+// ---- factorization (ilu.cu) -----------------------------------------------
+struct FactorArgs {
+  int32_t n;
+  int32_t B;
+  const int32_t* Ap;  // CSC column pointers, block-diagonal, [B*n+1]
+  const int32_t* Ai;  // local row indices (ascending within a column)
+  const double2* Ax;
+  const int32_t* q;   // optional elimination order (local), [B*n] or null
+  const double* rn;   // row norms [B*n] (required when drop_tol > 0)
+  double drop_tol;
+  int32_t fill_cap;   // -1: no cap
+  // outputs per system b; pointers are relative to b*cap
+  int32_t* Lp;  // [B*(n+1)]
+  int32_t* Li;
+  double2* Lx;
+  int64_t capL;
+  int32_t* Up;  // [B*(n+1)]
+  int32_t* Ui;
+  double2* Ux;
+  int64_t capU;
+  int32_t* pinv;  // [B*n]
+  int32_t* prow;  // [B*n]
+  int32_t* state;  // [B*3]: status, fail/next col, unused
+  // global scratch (per system slices of n)
+  double2* wx;
+  int32_t* wflag;
+  int32_t* wpinv_unused;
+  uint32_t* wbits;  // [B*nwords]
+  int32_t* wpat;
+  int32_t* wurow;
+  double2* wuval;
+  int32_t* wlrow;
+  uint8_t* wukeep;
+  uint8_t* wlkeep;
+  int smem_mode;  // 1: x/flag/pinv/bits live in shared memory
+};
+// state[3b+0] codes
+enum { FAC_RUNNING = 0, FAC_DONE = 1, FAC_ZERO_PIVOT = 2, FAC_OVERFLOW = 3 };
+int launch_ilutp(const FactorArgs& a, cudaStream_t st);
+__host__ __device__ size_t ilutp_smem_per_system(int32_t n);
+bool ilutp_fits_smem(int32_t n);
+
+}  // namespace rs

@@ -1,0 +1,651 @@
+// Device-resident steady-state solver: one CTA per system runs a whole
+//   * inverse_power (steady.py:177-260) with inner = direct LU apply,
+//     BiCGStab (krylov.py:181-291) or GMRES(m) (krylov.py:67-178), or
+//   * solve_iterative / solve_direct on the trace-modified system
+//     (steady.py:137-168, 116-134),
+// with the reference control flow reproduced branch for branch: monitor on the
+// preconditioned residual, true-residual confirmation, target *= 0.1
+// tightening, the 0.5*prev stall exit, breakdown tests, BiCGStab's half-step
+// restart, GMRES happy breakdown and zero-diagonal breakdown, the outer
+// phase-aligned difference and the infinity-norm plain residual test.
+//
+// Everything a step needs (matrix, factors, vectors) stays in L2 / shared
+// memory and no scalar crosses to the host until the solve ends, so a solve
+// costs one launch.  A batch of B independent systems (config-4 sweep) is a
+// grid of B CTAs.
+#include "common.cuh"
+#include "cta_ops.cuh"
+#include "solver.cuh"
+
+namespace rs {
+
+namespace {
+
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  // Smith's algorithm (scaled), as CPython/numpy complex division.
+  if (fabs(b.x) >= fabs(b.y)) {
+    if (b.x == 0.0 && b.y == 0.0) return make_double2(a.x / b.x, a.y / b.x);
+    const double r = b.y / b.x, d = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / d, (a.y - a.x * r) / d);
+  }
+  const double r = b.x / b.y, d = b.x * r + b.y;
+  return make_double2((a.x * r + a.y) / d, (a.y * r - a.x) / d);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double cabs(double2 a) { return hypot(a.x, a.y); }
+__device__ __forceinline__ bool finite2(double2 a) {
+  return isfinite(a.x) && isfinite(a.y);
+}
+
+struct Ctx {
+  int n;
+  // system matrix
+  const int32_t *Arp, *Aci;
+  const double2* Av;
+  // preconditioner
+  const int32_t *Lrp, *Lci, *Urp, *Uci, *pinv;
+  const double2 *Lv, *Uv, *rU;
+  bool have_M;
+  // scratch
+  double2* y;  // triangular-solve vector (smem or global)
+  volatile uint8_t* ready;
+  double* red;
+  double2* small;  // GMRES H/g/sn (global, per system)
+  double* cs;
+};
+
+// out = M^{-1} in  (factor.solve_lu, factor.py:137-149: y[pinv] = b; L; U;
+// x[q] = y with q = identity on the natural/RCM path).  out may alias in.
+__device__ void psolve(const Ctx& C, const double2* in, double2* out) {
+  const int n = C.n;
+  if (!C.have_M) {
+    if (in != out)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = in[i];
+    __syncthreads();
+    return;
+  }
+  double2* y = C.y;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    y[C.pinv[i]] = in[i];
+    C.ready[i] = 0;
+  }
+  __syncthreads();
+  cta::lower_solve(n, C.Lrp, C.Lci, C.Lv, y, C.ready);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) C.ready[i] = 0;
+  __syncthreads();
+  cta::upper_solve(n, C.Urp, C.Uci, C.Uv, C.rU, y, C.ready);
+  __syncthreads();
+  if (out != y)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = y[i];
+  __syncthreads();
+}
+
+// out = M^{-1} (A v)
+__device__ void apply_op(const Ctx& C, const double2* v, double2* tmp, double2* out) {
+  cta::spmv(C.n, C.Arp, C.Aci, C.Av, v, tmp);
+  __syncthreads();
+  psolve(C, tmp, out);
+}
+
+struct IterOut {
+  int iterations;
+  double final_residual;
+  bool converged, breakdown;
+};
+
+// Workspace vectors, each n complex128.
+struct Vecs {
+  double2 *x, *r, *rhat, *p, *v, *s, *t, *pb, *tmp;
+  double2* V;  // (m+1) x n for GMRES
+};
+
+__device__ void zero(int n, double2* a) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = make_double2(0.0, 0.0);
+}
+
+// krylov.bicgstab, krylov.py:181-291
+__device__ IterOut bicgstab(const Ctx& C, const double2* b, const Vecs& W, double tol,
+                            int max_iter) {
+  const int n = C.n;
+  IterOut out{0, 0.0, false, false};
+  const double bnorm = cta::nrm2(n, b, C.red);
+  if (bnorm == 0.0) {
+    zero(n, W.x);
+    __syncthreads();
+    out.converged = true;
+    return out;
+  }
+  psolve(C, b, W.pb);
+  const double pbnorm = cta::nrm2(n, W.pb, C.red);
+  if (pbnorm == 0.0 || !isfinite(pbnorm)) {
+    zero(n, W.x);
+    __syncthreads();
+    out.final_residual = bnorm;
+    out.breakdown = true;
+    return out;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    W.x[i] = make_double2(0.0, 0.0);
+    W.r[i] = W.pb[i];
+    W.rhat[i] = W.pb[i];
+    W.v[i] = make_double2(0.0, 0.0);
+    W.p[i] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double rhat_norm = cta::nrm2(n, W.rhat, C.red);
+  double2 rho_prev = make_double2(1.0, 0.0), alpha = make_double2(1.0, 0.0),
+          omega = make_double2(1.0, 0.0);
+  double target = tol * pbnorm;
+  double prev_true = INFINITY;
+  int it = 0;
+  while (it < max_iter) {
+    const double rnorm = cta::nrm2(n, W.r, C.red);
+    if (rnorm <= target) {
+      const double true_res = cta::resid_nrm2(n, C.Arp, C.Aci, C.Av, W.x, b, C.red);
+      if (true_res <= tol * bnorm) {
+        out.converged = true;
+        break;
+      }
+      if (true_res >= 0.5 * prev_true) break;
+      prev_true = true_res;
+      target *= 0.1;
+    }
+    const double2 rho = cta::vdot(n, W.rhat, W.r, C.red);
+    const double arho = cabs(rho);
+    if (arho < 1e-30 || arho < 1e-16 * rhat_norm * rnorm) {
+      out.breakdown = true;
+      break;
+    }
+    if (it == 0) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) W.p[i] = W.r[i];
+    } else {
+      const double2 beta = cmul(cdiv(rho, rho_prev), cdiv(alpha, omega));
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double2 d = csub(W.p[i], cmul(omega, W.v[i]));
+        W.p[i] = cadd(W.r[i], cmul(beta, d));
+      }
+    }
+    __syncthreads();
+    apply_op(C, W.p, W.tmp, W.v);
+    const double2 denom = cta::vdot(n, W.rhat, W.v, C.red);
+    if (denom.x == 0.0 && denom.y == 0.0) {
+      out.breakdown = true;
+      break;
+    }
+    alpha = cdiv(rho, denom);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      W.s[i] = csub(W.r[i], cmul(alpha, W.v[i]));
+    __syncthreads();
+    ++it;
+    const double snorm = cta::nrm2(n, W.s, C.red);
+    if (snorm <= target) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        W.x[i] = cadd(W.x[i], cmul(alpha, W.p[i]));
+      __syncthreads();
+      const double true_res = cta::resid_nrm2(n, C.Arp, C.Aci, C.Av, W.x, b, C.red);
+      if (true_res <= tol * bnorm) {
+        out.converged = true;
+        break;
+      }
+      if (true_res >= 0.5 * prev_true) break;
+      prev_true = true_res;
+      target *= 0.1;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        W.r[i] = W.s[i];
+        W.rhat[i] = W.s[i];
+        W.v[i] = make_double2(0.0, 0.0);
+        W.p[i] = make_double2(0.0, 0.0);
+      }
+      __syncthreads();
+      rhat_norm = cta::nrm2(n, W.rhat, C.red);
+      rho_prev = alpha = omega = make_double2(1.0, 0.0);
+      continue;
+    }
+    apply_op(C, W.s, W.tmp, W.t);
+    const double2 tt = cta::vdot(n, W.t, W.t, C.red);
+    if (tt.x == 0.0 && tt.y == 0.0) {
+      out.breakdown = true;
+      break;
+    }
+    omega = cdiv(cta::vdot(n, W.t, W.s, C.red), tt);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double2 xa = cadd(W.x[i], cmul(alpha, W.p[i]));
+      W.x[i] = cadd(xa, cmul(omega, W.s[i]));
+      W.r[i] = csub(W.s[i], cmul(omega, W.t[i]));
+    }
+    __syncthreads();
+    rho_prev = rho;
+    if (omega.x == 0.0 && omega.y == 0.0) {
+      out.breakdown = true;
+      break;
+    }
+  }
+  out.iterations = it;
+  out.final_residual = cta::resid_nrm2(n, C.Arp, C.Aci, C.Av, W.x, b, C.red);
+  return out;
+}
+
+// krylov.gmres, krylov.py:67-178.  H is (m+1) x m row-major in C.small,
+// followed by g (m+1) and sn (m); cs (m) in C.cs.  Scalar Givens work is done
+// by thread 0 and published through global memory + a barrier.
+__device__ IterOut gmres(const Ctx& C, const double2* b, const Vecs& W, double tol,
+                         int max_iter, int m) {
+  const int n = C.n;
+  IterOut out{0, 0.0, false, false};
+  double2* H = C.small;
+  double2* g = H + (m + 1) * m;
+  double2* sn = g + (m + 1);
+  double2* yv = sn + m;
+  double* cs = C.cs;
+  const double bnorm = cta::nrm2(n, b, C.red);
+  if (bnorm == 0.0) {
+    zero(n, W.x);
+    __syncthreads();
+    out.converged = true;
+    return out;
+  }
+  psolve(C, b, W.pb);
+  const double pbnorm = cta::nrm2(n, W.pb, C.red);
+  if (pbnorm == 0.0 || !isfinite(pbnorm)) {
+    zero(n, W.x);
+    __syncthreads();
+    out.final_residual = bnorm;
+    out.breakdown = true;
+    return out;
+  }
+  zero(n, W.x);
+  __syncthreads();
+  double target = tol * pbnorm;
+  int total = 0;
+  bool converged = false, breakdown = false, invariant = false;
+  double prev_true = INFINITY;
+  __shared__ double s_res;
+  __shared__ int s_flag;
+  while (total < max_iter && !converged && !invariant) {
+    double2* r = W.r;
+    if (total) {
+      apply_op(C, W.x, W.tmp, r);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) r[i] = csub(W.pb[i], r[i]);
+    } else {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) r[i] = W.pb[i];
+    }
+    __syncthreads();
+    const double beta = cta::nrm2(n, r, C.red);
+    bool monitor_hit = beta <= target;
+    double res = beta;
+    if (!monitor_hit) {
+      double2* V0 = W.V;
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        V0[i] = make_double2(r[i].x / beta, r[i].y / beta);
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < (m + 1) * m; ++i) H[i] = make_double2(0.0, 0.0);
+        for (int i = 0; i <= m; ++i) g[i] = make_double2(0.0, 0.0);
+        g[0] = make_double2(beta, 0.0);
+      }
+      __syncthreads();
+      int j = 0;
+      while (j < m && total < max_iter) {
+        double2* Vj = W.V + (size_t)j * n;
+        double2* w = W.r;  // reuse r as the Arnoldi vector
+        apply_op(C, Vj, W.tmp, w);
+        ++total;
+        for (int i = 0; i <= j; ++i) {
+          const double2* Vi = W.V + (size_t)i * n;
+          const double2 hij = cta::vdot(n, Vi, w, C.red);
+          for (int e = threadIdx.x; e < n; e += blockDim.x) w[e] = csub(w[e], cmul(hij, Vi[e]));
+          if (threadIdx.x == 0) H[i * m + j] = hij;
+          __syncthreads();
+        }
+        const double hnext = cta::nrm2(n, w, C.red);
+        if (hnext > 0.0) {
+          double2* Vn = W.V + (size_t)(j + 1) * n;
+          for (int e = threadIdx.x; e < n; e += blockDim.x)
+            Vn[e] = make_double2(w[e].x / hnext, w[e].y / hnext);
+        }
+        if (threadIdx.x == 0) {
+          for (int i = 0; i < j; ++i) {
+            const double2 hi = H[i * m + j], hi1 = H[(i + 1) * m + j];
+            const double2 t = cadd(make_double2(cs[i] * hi.x, cs[i] * hi.y), cmul(sn[i], hi1));
+            const double2 csn = make_double2(-sn[i].x, sn[i].y);  // -conj(sn)
+            H[(i + 1) * m + j] = cadd(cmul(csn, hi), make_double2(cs[i] * hi1.x, cs[i] * hi1.y));
+            H[i * m + j] = t;
+          }
+          const double2 al = H[j * m + j];
+          const double aal = cabs(al);
+          const double denom = hypot(aal, hnext);
+          if (denom == 0.0) {
+            cs[j] = 1.0;
+            sn[j] = make_double2(0.0, 0.0);
+          } else if (al.x == 0.0 && al.y == 0.0) {
+            cs[j] = 0.0;
+            sn[j] = make_double2(1.0, 0.0);
+          } else {
+            cs[j] = aal / denom;
+            const double2 ph = make_double2(al.x / aal, al.y / aal);
+            sn[j] = make_double2(ph.x * (hnext / denom), ph.y * (hnext / denom));
+          }
+          H[j * m + j] = cadd(make_double2(cs[j] * al.x, cs[j] * al.y),
+                              make_double2(sn[j].x * hnext, sn[j].y * hnext));
+          const double2 gj = g[j];
+          g[j + 1] = cmul(make_double2(-sn[j].x, sn[j].y), gj);
+          g[j] = make_double2(cs[j] * gj.x, cs[j] * gj.y);
+          s_res = cabs(g[j + 1]);
+        }
+        __syncthreads();
+        res = s_res;
+        ++j;
+        if (hnext == 0.0) {
+          invariant = true;
+          break;
+        }
+        if (res <= target) break;
+      }
+      // zero diagonal -> breakdown; else back-substitute and update x
+      if (threadIdx.x == 0) {
+        int bad = 0;
+        for (int i = 0; i < j; ++i) {
+          const double2 d = H[i * m + i];
+          if (d.x == 0.0 && d.y == 0.0) bad = 1;
+        }
+        if (!bad) {
+          for (int i = j - 1; i >= 0; --i) {
+            double2 acc = make_double2(0.0, 0.0);
+            for (int k = i + 1; k < j; ++k) acc = cadd(acc, cmul(H[i * m + k], yv[k]));
+            yv[i] = cdiv(csub(g[i], acc), H[i * m + i]);
+          }
+        }
+        s_flag = bad;
+      }
+      __syncthreads();
+      if (s_flag) {
+        breakdown = true;
+        break;
+      }
+      for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int k = 0; k < j; ++k) acc = cadd(acc, cmul(yv[k], W.V[(size_t)k * n + e]));
+        W.x[e] = cadd(W.x[e], acc);
+      }
+      __syncthreads();
+      monitor_hit = res <= target || invariant;
+    }
+    if (monitor_hit) {
+      const double true_res = cta::resid_nrm2(n, C.Arp, C.Aci, C.Av, W.x, b, C.red);
+      if (true_res <= tol * bnorm) {
+        converged = true;
+      } else if (invariant || true_res >= 0.5 * prev_true) {
+        break;
+      } else {
+        prev_true = true_res;
+        target *= 0.1;
+      }
+    }
+  }
+  out.iterations = total;
+  out.converged = converged;
+  out.breakdown = breakdown;
+  out.final_residual = cta::resid_nrm2(n, C.Arp, C.Aci, C.Av, W.x, b, C.red);
+  return out;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(512) steady_solver_kernel(SolverArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[32 * 4];
+  const int b = blockIdx.x;
+  const int n = a.n;
+  const int64_t bn = (int64_t)b * n;
+  SolveStats* st = a.stats + b;
+
+  Ctx C;
+  C.n = n;
+  C.Arp = a.Arp + bn;  // local-offset views: rows of system b
+  C.Aci = a.Aci;
+  C.Av = a.Av;
+  C.have_M = a.Lrp != nullptr;
+  C.Lrp = a.Lrp ? a.Lrp + bn : nullptr;
+  C.Lci = a.Lci;
+  C.Lv = a.Lv;
+  C.Urp = a.Urp ? a.Urp + bn : nullptr;
+  C.Uci = a.Uci;
+  C.Uv = a.Uv;
+  C.rU = a.rU ? a.rU + bn : nullptr;
+  C.pinv = a.pinv ? a.pinv + bn : nullptr;
+  C.red = red;
+  double2* ws = a.work + (int64_t)b * a.work_stride;
+  C.ready = reinterpret_cast<volatile uint8_t*>(smem);
+  const size_t flag_bytes = ((size_t)n + 15) & ~(size_t)15;
+  if (a.y_in_smem) C.y = reinterpret_cast<double2*>(smem + flag_bytes);
+  else C.y = ws;  // slot 0
+  const int m = a.restart_m;
+  C.small = ws + (int64_t)n;  // (m+1)*m + (m+1) + m + m complex
+  C.cs = reinterpret_cast<double*>(C.small + (m + 1) * m + (m + 1) + 2 * m);
+  const int64_t small_slots = ((m + 1) * m + (m + 1) + 3 * m + n - 1) / n + 1;
+  double2* vb = ws + (int64_t)n * (1 + small_slots);
+  Vecs W;
+  W.x = vb + 0 * (int64_t)n;
+  W.r = vb + 1 * (int64_t)n;
+  W.rhat = vb + 2 * (int64_t)n;
+  W.p = vb + 3 * (int64_t)n;
+  W.v = vb + 4 * (int64_t)n;
+  W.s = vb + 5 * (int64_t)n;
+  W.t = vb + 6 * (int64_t)n;
+  W.pb = vb + 7 * (int64_t)n;
+  W.tmp = vb + 8 * (int64_t)n;
+  W.V = vb + 9 * (int64_t)n;  // (m+1) vectors; BiCGStab does not use them
+  double2* xo = vb + (9 + (int64_t)m + 1) * n;      // outer iterate
+  double2* yo = vb + (10 + (int64_t)m + 1) * n;     // inner result / aligned
+  const double2* in = a.rhs + bn;
+  double2* out = a.xout + bn;
+
+  // local-index adjustment: CSR arrays are global block-diagonal; the row
+  // pointers above are offset by b*n, entries are absolute positions.
+  if (threadIdx.x == 0) {
+    st->status = 0;
+    st->outer = 0;
+    st->inner_last = 0;
+    st->inner_total = 0;
+    st->converged = 0;
+    st->breakdown = 0;
+    st->final_residual = 0.0;
+    st->condest = 0.0;
+  }
+
+  if (a.want_condest && C.have_M) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) W.tmp[i] = make_double2(1.0, 0.0);
+    __syncthreads();
+    psolve(C, W.tmp, W.pb);
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, cabs(W.pb[i]));
+    mx = cta::block_max(mx, red);
+    if (threadIdx.x == 0) st->condest = mx;
+  }
+
+  const int mode = a.mode;
+  if (mode == MODE_LIN_DIRECT || mode == MODE_LIN_BICGSTAB || mode == MODE_LIN_GMRES) {
+    IterOut io{0, 0.0, true, false};
+    if (mode == MODE_LIN_DIRECT) {
+      psolve(C, in, W.x);
+    } else if (mode == MODE_LIN_BICGSTAB) {
+      io = bicgstab(C, in, W, a.tol, a.max_iter);
+    } else {
+      io = gmres(C, in, W, a.tol, a.max_iter, m);
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = W.x[i];
+    if (threadIdx.x == 0) {
+      st->inner_last = io.iterations;
+      st->inner_total = io.iterations;
+      st->converged = io.converged;
+      st->breakdown = io.breakdown;
+      st->final_residual = io.final_residual;
+    }
+    return;
+  }
+
+  // ---- inverse power, steady.py:518-541 -----------------------------------
+  // start vector (drawn on the host, steady.py:171-174) normalised here
+  {
+    const double nx = cta::nrm2(n, in, red);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      xo[i] = make_double2(in[i].x / nx, in[i].y / nx);
+    __syncthreads();
+  }
+  const double tol = a.tol;
+  int outer = 0, inner_total = 0, inner_last = 0;
+  bool converged = false;
+  int status = 0;
+  while (outer < a.max_outer) {
+    double2* y = yo;
+    if (mode == MODE_INV_DIRECT) {
+      psolve(C, xo, y);
+    } else {
+      IterOut io = (mode == MODE_INV_BICGSTAB)
+                       ? bicgstab(C, xo, W, tol / 10.0, a.max_iter)
+                       : gmres(C, xo, W, tol / 10.0, a.max_iter, m);
+      inner_last = io.iterations;
+      inner_total += io.iterations;
+      int nonfin = 0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) nonfin |= !finite2(W.x[i]);
+      nonfin = __syncthreads_or(nonfin);
+      if (io.breakdown || nonfin) {
+        status = io.breakdown ? SOLVE_INNER_BREAKDOWN : SOLVE_INNER_NONFINITE;
+        break;
+      }
+      if (cta::nrm2(n, W.x, red) == 0.0) {
+        status = SOLVE_INNER_NO_PROGRESS;
+        break;
+      }
+      for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = W.x[i];
+      __syncthreads();
+    }
+    const double ny = cta::nrm2(n, y, red);
+    if (ny == 0.0 || !isfinite(ny)) {
+      status = SOLVE_UNUSABLE_VECTOR;
+      break;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      y[i] = make_double2(y[i].x / ny, y[i].y / ny);
+    __syncthreads();
+    ++outer;
+    const double2 ov = cta::vdot(n, y, xo, red);
+    double2 ph = make_double2(1.0, 0.0);
+    const bool ovnz = !(ov.x == 0.0 && ov.y == 0.0);
+    if (ovnz) {
+      const double aov = cabs(ov);
+      ph = make_double2(ov.x / aov, ov.y / aov);
+    }
+    double acc[1] = {0.0};
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double2 al = ovnz ? cmul(y[i], ph) : y[i];
+      const double2 d = csub(al, xo[i]);
+      acc[0] = __fma_rn(d.x, d.x, __fma_rn(d.y, d.y, acc[0]));
+    }
+    cta::block_sum<1>(acc, red);
+    const double diff = sqrt(acc[0]);
+    // resid_inf = max |L_plain,perm y|
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int p0 = a.Prp[bn + i], p1 = a.Prp[bn + i + 1];
+      double2 s = make_double2(0.0, 0.0);
+      if (p0 < p1) {
+        s = cmul_plain(a.Pv[p0], y[a.Pci[p0]]);
+        for (int p = p0 + 1; p < p1; ++p) s = cadd(s, cmul_plain(a.Pv[p], y[a.Pci[p]]));
+      }
+      mx = fmax(mx, cabs(s));
+    }
+    const double resid_inf = cta::block_max(mx, red);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) xo[i] = y[i];
+    __syncthreads();
+    if (diff <= tol || resid_inf <= tol) {
+      converged = true;
+      break;
+    }
+  }
+  if (status == 0 && !converged) status = SOLVE_POWER_NOT_CONVERGED;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = xo[i];
+  if (threadIdx.x == 0) {
+    st->status = status;
+    st->outer = outer;
+    st->inner_last = inner_last;
+    st->inner_total = inner_total;
+    st->converged = converged;
+  }
+}
+
+int64_t solver_work_stride(int32_t n, int restart_m) {
+  const int m = restart_m;
+  const int64_t small_slots = ((int64_t)(m + 1) * m + (m + 1) + 3 * m + n - 1) / n + 1;
+  return (int64_t)n * (1 + small_slots + 9 + (m + 1) + 2);
+}
+
+int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
+  if (a.B == 0) return RS_OK;
+  int dev, max_smem;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t flag_bytes = ((size_t)a.n + 15) & ~(size_t)15;
+  size_t smem = flag_bytes + (a.y_in_smem ? 16 * (size_t)a.n : 0);
+  if (smem + 2048 > (size_t)max_smem) {
+    set_error("steady solver: n=%d needs %zu B of shared memory", a.n, smem);
+    return RS_ERR_UNSUPPORTED;
+  }
+  RS_CUDA_TRY(cudaFuncSetAttribute(steady_solver_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  steady_solver_kernel<<<a.B, a.threads, smem, st>>>(a);
+  RS_CUDA_TRY(cudaGetLastError());
+  return RS_OK;
+}
+
+}  // namespace rs
+
+namespace rs {
+
+// Standalone preconditioner apply (factor.solve_lu), one CTA per system.
+__global__ void __launch_bounds__(512) lu_solve_kernel(SolverArgs a, int y_in_smem) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int b = blockIdx.x;
+  const int n = a.n;
+  const int64_t bn = (int64_t)b * n;
+  Ctx C;
+  C.n = n;
+  C.have_M = true;
+  C.Lrp = a.Lrp + bn;
+  C.Lci = a.Lci;
+  C.Lv = a.Lv;
+  C.Urp = a.Urp + bn;
+  C.Uci = a.Uci;
+  C.Uv = a.Uv;
+  C.rU = a.rU + bn;
+  C.pinv = a.pinv + bn;
+  C.ready = reinterpret_cast<volatile uint8_t*>(smem);
+  const size_t flag_bytes = ((size_t)n + 15) & ~(size_t)15;
+  C.y = y_in_smem ? reinterpret_cast<double2*>(smem + flag_bytes) : a.xout + bn;
+  psolve(C, a.rhs + bn, a.xout + bn);
+}
+
+int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
+  if (a.B == 0 || a.n == 0) return RS_OK;
+  int dev, max_smem;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t flag_bytes = ((size_t)a.n + 15) & ~(size_t)15;
+  int y_smem = flag_bytes + 16 * (size_t)a.n + 2048 <= (size_t)max_smem;
+  if (a.rhs == a.xout) y_smem = 1;  // in-place needs a separate y
+  size_t smem = flag_bytes + (y_smem ? 16 * (size_t)a.n : 0);
+  if (smem + 1024 > (size_t)max_smem) {
+    set_error("lu_solve: n=%d too large for an in-place apply", a.n);
+    return RS_ERR_UNSUPPORTED;
+  }
+  RS_CUDA_TRY(cudaFuncSetAttribute(lu_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+  lu_solve_kernel<<<a.B, 512, smem, st>>>(a, y_smem);
+  RS_CUDA_TRY(cudaGetLastError());
+  return RS_OK;
+}
+
+}  // namespace rs

@@ -1,0 +1,80 @@
+// Arguments of the device-resident steady-state solver (solver.cu).
+#pragma once
+#include "common.cuh"
+
+namespace rs {
+
+enum SolveMode {
+  MODE_INV_DIRECT = 0,
+  MODE_INV_BICGSTAB = 1,
+  MODE_INV_GMRES = 2,
+  MODE_LIN_DIRECT = 3,
+  MODE_LIN_BICGSTAB = 4,
+  MODE_LIN_GMRES = 5,
+};
+
+enum SolveStatus {
+  SOLVE_OK = 0,
+  SOLVE_INNER_BREAKDOWN = 1,    // steady.py:509-512
+  SOLVE_INNER_NONFINITE = 2,    // steady.py:509-512
+  SOLVE_INNER_NO_PROGRESS = 3,  // steady.py:513-514
+  SOLVE_UNUSABLE_VECTOR = 4,    // steady.py:525-526
+  SOLVE_POWER_NOT_CONVERGED = 5,  // steady.py:537-539
+};
+
+// Must match include/rhosolve_b200.h rs_solve_stats.
+struct SolveStats {
+  int32_t status;
+  int32_t outer;
+  int32_t inner_last;
+  int32_t inner_total;
+  int32_t converged;
+  int32_t breakdown;
+  double final_residual;
+  double condest;
+};
+
+struct SolverArgs {
+  int32_t n;
+  int32_t B;
+  int32_t mode;
+  int32_t threads;
+  // system matrix (shifted or modified, ordered), block-diagonal CSR
+  const int32_t* Arp;
+  const int32_t* Aci;
+  const double2* Av;
+  // plain ordered matrix (inverse power outer residual), block-diagonal CSR
+  const int32_t* Prp;
+  const int32_t* Pci;
+  const double2* Pv;
+  // preconditioner: strictly-lower L, strictly-upper U (block-diagonal CSR,
+  // pivotal coordinates), reciprocal pivots, row permutation pinv (local)
+  const int32_t* Lrp;
+  const int32_t* Lci;
+  const double2* Lv;
+  const int32_t* Urp;
+  const int32_t* Uci;
+  const double2* Uv;
+  const double2* rU;
+  const int32_t* pinv;
+  const double2* rhs;  // rhs (linear modes) or start vector (inverse power)
+  double2* xout;
+  SolveStats* stats;
+  double2* work;
+  int64_t work_stride;  // complex entries per system
+  double tol;
+  int32_t max_iter;
+  int32_t restart_m;
+  int32_t max_outer;
+  int32_t want_condest;
+  int32_t y_in_smem;
+};
+
+int64_t solver_work_stride(int32_t n, int restart_m);
+int launch_steady_solver(const SolverArgs& a, cudaStream_t st);
+
+}  // namespace rs
+
+namespace rs {
+int launch_lu_solve(const SolverArgs& a, cudaStream_t st);
+}

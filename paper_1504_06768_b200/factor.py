@@ -1,0 +1,232 @@
+"""Sparse LU / ILUTP on the GPU and the preconditioner apply.
+
+Drop-in for the reference factor module (pkg/src/rhosolve/factor.py):
+`lu`, `ilutp`, `solve_lu`, `condest`, `LUFactors`, `SingularMatrixError`,
+`PreconditionerBreakdownError`, same argument checks and messages.  The
+factorization itself is the warp-per-system kernel in csrc/ilu.cu, the apply
+the row-oriented triangular solves in csrc/cta_ops.cuh; both are
+bit-identical to the reference kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .sparse import DeviceCSR
+
+__all__ = ["LUFactors", "lu", "ilutp", "solve_lu", "condest", "SingularMatrixError",
+           "PreconditionerBreakdownError", "factor_batch"]
+
+
+class SingularMatrixError(ValueError):
+    """Complete factorization hit a zero pivot column."""
+
+
+class PreconditionerBreakdownError(ValueError):
+    """Incomplete factorization hit a zero pivot; retry with a smaller drop
+    tolerance."""
+
+
+class LUFactors:
+    """P_r A = L U (approximately when incomplete) for nsys systems.
+
+    raw:  per-system CSC exactly as the reference factorize returns it
+          (Lp, Li, Lx, Up, Ui, Ux with L rows in pivotal order), pinv.
+    rows: strictly-lower L and strictly-upper U in CSR + recipc(U_kk), the
+          form the device triangular solves consume.
+    fail: per-system zero-pivot step (-1 = ok)."""
+
+    __slots__ = ("n", "nsys", "raw", "capL", "capU", "pinv", "L_rp", "L_ci", "L_v", "U_rp",
+                 "U_ci", "U_v", "rdiag", "fill_factors", "complete", "drop_tol",
+                 "fill_limit", "fail", "lnnz", "unnz")
+
+    @property
+    def fill_factor(self):
+        return float(self.fill_factors[0])
+
+    def system_raw(self, b):
+        """Host copy of system b's raw CSC factors (reference layout, int64)."""
+        Lp, Li, Lx, Up, Ui, Ux = self.raw
+        n = self.n
+        lp = Lp[b * (n + 1):(b + 1) * (n + 1)].cpu().numpy().astype(np.int64)
+        up = Up[b * (n + 1):(b + 1) * (n + 1)].cpu().numpy().astype(np.int64)
+        li = Li[b * self.capL:b * self.capL + lp[-1]].cpu().numpy().astype(np.int64)
+        lx = Lx[b * self.capL:b * self.capL + lp[-1]].cpu().numpy()
+        ui = Ui[b * self.capU:b * self.capU + up[-1]].cpu().numpy().astype(np.int64)
+        ux = Ux[b * self.capU:b * self.capU + up[-1]].cpu().numpy()
+        pinv = self.pinv[b * n:(b + 1) * n].cpu().numpy().astype(np.int64)
+        return lp, li, lx, up, ui, ux, pinv
+
+    def __repr__(self):
+        kind = "complete" if self.complete else "incomplete"
+        return f"LUFactors(n={self.n}, nsys={self.nsys}, {kind}, fill={self.fill_factors})"
+
+
+def _transpose(M):
+    rp = torch.empty_like(M.row_ptr)
+    ci = torch.empty_like(M.col_idx)
+    v = torch.empty_like(M.values)
+    _lib.call("rs_transpose", M.nsys, M.n, _lib.ptr(M.row_ptr), _lib.ptr(M.col_idx),
+              _lib.ptr(M.values), _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(v), _lib.stream_ptr())
+    return rp, ci, v
+
+
+def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True):
+    """factor._factor (factor.py:70-112) for every system of a DeviceCSR."""
+    n, B = M.n, M.nsys
+    dev = M.values.device
+    if n == 0 or M.nnz == 0:
+        raise SingularMatrixError("zero pivot at elimination step 0")
+    incomplete = drop_tol > 0.0 or not math.isinf(fill_limit)
+    nnz_rows = M.row_ptr.diff().reshape(B, n).sum(1).cpu().numpy()
+    if math.isinf(fill_limit):
+        cap = -1
+    else:
+        # per-system cap (factor.py:92); systems of a batch share n and, in
+        # every configuration, nnz -- a differing nnz would change the cap.
+        caps = [int(math.ceil(fill_limit * int(z) / n)) for z in nnz_rows]
+        if len(set(caps)) != 1:
+            raise ValueError("batched ILUTP needs equal nnz across systems")
+        cap = caps[0]
+    Ap, Ai, Ax = _transpose(M)
+    rn = None
+    if drop_tol > 0.0:
+        rn = torch.empty(B * n, dtype=torch.float64, device=dev)
+        _lib.call("rs_row_norms", B, n, _lib.ptr(M.row_ptr), _lib.ptr(M.values), _lib.ptr(rn),
+                  _lib.stream_ptr())
+    maxnnz = int(nnz_rows.max())
+    per_col = max(cap - 1, 1) if cap >= 0 else None
+    guess = max(8 * maxnnz, 2 * n, 16)
+    capL = capU = min(n * per_col, guess) if per_col else guess
+    Lp = torch.zeros(B * (n + 1), dtype=torch.int32, device=dev)
+    Up = torch.zeros_like(Lp)
+    Li = torch.empty(B * capL, dtype=torch.int32, device=dev)
+    Lx = torch.empty(B * capL, dtype=torch.complex128, device=dev)
+    Ui = torch.empty(B * capU, dtype=torch.int32, device=dev)
+    Ux = torch.empty(B * capU, dtype=torch.complex128, device=dev)
+    pinv = torch.empty(B * n, dtype=torch.int32, device=dev)
+    state = torch.zeros(3 * B, dtype=torch.int32, device=dev)
+    st = _lib.stream_ptr()
+    while True:
+        _lib.call("rs_factorize", B, n, _lib.ptr(Ap), _lib.ptr(Ai), _lib.ptr(Ax), None,
+                  float(drop_tol), cap, _lib.ptr(rn), _lib.ptr(Lp), _lib.ptr(Li), _lib.ptr(Lx),
+                  capL, _lib.ptr(Up), _lib.ptr(Ui), _lib.ptr(Ux), capU, _lib.ptr(pinv),
+                  _lib.ptr(state), st)
+        sh = state.reshape(B, 3).cpu().numpy()
+        if not np.any(sh[:, 0] == 3):
+            break
+        # grow (x2) both factors of every system, preserving contents
+        ncapL, ncapU = 2 * capL, 2 * capU
+        Li, Lx = _regrow(Li, B, capL, ncapL), _regrow(Lx, B, capL, ncapL)
+        Ui, Ux = _regrow(Ui, B, capU, ncapU), _regrow(Ux, B, capU, ncapU)
+        capL, capU = ncapL, ncapU
+    fail = np.where(sh[:, 0] == 2, sh[:, 1], -1)
+    if raise_on_fail and np.any(fail >= 0):
+        k = int(fail[fail >= 0][0])
+        msg = f"zero pivot at elimination step {k}"
+        raise PreconditionerBreakdownError(msg) if incomplete else SingularMatrixError(msg)
+    f = LUFactors()
+    f.n, f.nsys = n, B
+    f.raw = (Lp, Li, Lx, Up, Ui, Ux)
+    f.capL, f.capU = capL, capU
+    f.pinv = pinv
+    lp = Lp.reshape(B, n + 1)[:, -1].cpu().numpy().astype(np.int64)
+    up = Up.reshape(B, n + 1)[:, -1].cpu().numpy().astype(np.int64)
+    f.lnnz, f.unnz = lp, up
+    f.fill_factors = (lp + up) / nnz_rows
+    f.complete = not incomplete
+    f.drop_tol = float(drop_tol) if incomplete else None
+    f.fill_limit = float(fill_limit) if incomplete else None
+    f.fail = fail
+    if np.all(fail < 0):
+        _build_rows(f, dev)
+    else:
+        f.L_rp = None
+    return f
+
+
+def _regrow(t, B, old, new):
+    out = torch.empty(B * new, dtype=t.dtype, device=t.device)
+    out.view(B, new)[:, :old].copy_(t.view(B, old))
+    return out
+
+
+def _build_rows(f, dev):
+    B, n = f.nsys, f.n
+    Lp, Li, Lx, Up, Ui, Ux = f.raw
+    f.L_rp = torch.empty(B * n + 1, dtype=torch.int32, device=dev)
+    f.U_rp = torch.empty_like(f.L_rp)
+    ln, un = ctypes.c_int64(0), ctypes.c_int64(0)
+    st = _lib.stream_ptr()
+    args = lambda lci, lv, uci, uv, rd: (  # noqa: E731
+        B, n, _lib.ptr(Lp), _lib.ptr(Li), _lib.ptr(Lx), f.capL, _lib.ptr(Up), _lib.ptr(Ui),
+        _lib.ptr(Ux), f.capU, _lib.ptr(f.L_rp), lci, lv, ctypes.byref(ln), _lib.ptr(f.U_rp),
+        uci, uv, rd, ctypes.byref(un), st)
+    _lib.call("rs_factor_rows", *args(None, None, None, None, None))
+    f.L_ci = torch.empty(max(ln.value, 1), dtype=torch.int32, device=dev)
+    f.L_v = torch.empty(max(ln.value, 1), dtype=torch.complex128, device=dev)
+    f.U_ci = torch.empty(max(un.value, 1), dtype=torch.int32, device=dev)
+    f.U_v = torch.empty(max(un.value, 1), dtype=torch.complex128, device=dev)
+    f.rdiag = torch.empty(B * n, dtype=torch.complex128, device=dev)
+    _lib.call("rs_factor_rows", *args(_lib.ptr(f.L_ci), _lib.ptr(f.L_v), _lib.ptr(f.U_ci),
+                                      _lib.ptr(f.U_v), _lib.ptr(f.rdiag)))
+
+
+def _mat(a):
+    return a.matrix if hasattr(a, "matrix") else a
+
+
+def _check_colperm(col_perm, n):
+    if col_perm is not None and not col_perm.is_identity():
+        raise NotImplementedError("column pre-orderings ('cmd') are outside the GPU path")
+
+
+def lu(a, col_perm=None):
+    """Complete sparse LU with partial pivoting (factor.py:115-118)."""
+    M = _mat(a)
+    _check_colperm(col_perm, M.n)
+    return factor_batch(M, 0.0, math.inf)
+
+
+def ilutp(a, d=1e-4, p=300.0, col_perm=None):
+    """ILUTP with drop tolerance d and fill budget p (factor.py:121-134)."""
+    if d < 0:
+        raise ValueError("drop tolerance d must be >= 0")
+    if not p >= 1:
+        raise ValueError("fill limit p must be >= 1")
+    M = _mat(a)
+    _check_colperm(col_perm, M.n)
+    return factor_batch(M, float(d), float(p))
+
+
+def solve_lu_device(f, b):
+    """x = M^{-1} b on the device for every system (b: nsys*n complex128)."""
+    x = torch.empty_like(b)
+    _lib.call("rs_lu_solve", f.nsys, f.n, _lib.ptr(f.pinv), _lib.ptr(f.L_rp), _lib.ptr(f.L_ci),
+              _lib.ptr(f.L_v), _lib.ptr(f.U_rp), _lib.ptr(f.U_ci), _lib.ptr(f.U_v),
+              _lib.ptr(f.rdiag), _lib.ptr(b), _lib.ptr(x), _lib.stream_ptr())
+    return x
+
+
+def solve_lu(f, b):
+    """factor.solve_lu (factor.py:137-149).  numpy in -> numpy out; a CUDA
+    tensor in -> CUDA tensor out."""
+    if isinstance(b, torch.Tensor):
+        return solve_lu_device(f, b.to(torch.complex128).contiguous())
+    b = np.asarray(b, dtype=np.complex128)
+    if b.shape != (f.n * f.nsys,):
+        raise ValueError(f"rhs length {b.shape} does not match n={f.n}")
+    dev = f.pinv.device
+    return solve_lu_device(f, torch.from_numpy(b).to(dev)).cpu().numpy()
+
+
+def condest(f):
+    """||M^{-1} 1||_inf (factor.py:152-157); one value per system."""
+    e = torch.ones(f.nsys * f.n, dtype=torch.complex128, device=f.pinv.device)
+    x = solve_lu_device(f, e).reshape(f.nsys, f.n).abs().amax(1).cpu().numpy()
+    return float(x[0]) if f.nsys == 1 else x

@@ -1,0 +1,337 @@
+"""Steady-state drivers: the drop-in surface of the reference steady module
+(pkg/src/rhosolve/steady.py:116-260).
+
+Same signatures, defaults, result fields and exceptions as the reference:
+`solve_direct`, `solve_iterative`, `inverse_power`, `SteadyStateResult`,
+`InnerSolverError`, `PowerIterationError`, `DEFAULT_SEED`, `MAX_OUTER`.
+Every stage runs on the GPU through the C ABI: shift / trace modification,
+RCM, permutation, LU / ILUTP, then ONE solver launch that runs the whole
+inverse-power (or Krylov) iteration on the device, then the unpermute and
+post-processing kernels.  Only the seeded start vector (numpy PCG64, as the
+reference draws it) and the final rho cross the PCIe bus.
+
+`inverse_power_batch` / `solve_batch` run many independent systems (the
+config-4 parameter sweep) as one block-diagonal batch: one CTA per system.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, factor, liouville, ordering
+from .liouville import DEFAULT_SIGMA
+
+__all__ = ["SteadyStateResult", "solve_direct", "solve_iterative", "inverse_power",
+           "inverse_power_batch", "solve_batch", "InnerSolverError", "PowerIterationError",
+           "DEFAULT_SEED", "MAX_OUTER", "start_vector"]
+
+DEFAULT_SEED = 12345
+MAX_OUTER = 50
+
+
+class InnerSolverError(RuntimeError):
+    """The inner linear solve of the inverse-power iteration produced no
+    usable iterate (breakdown or non-finite values)."""
+
+
+class PowerIterationError(RuntimeError):
+    """Inverse-power iteration exceeded the outer iteration budget."""
+
+
+@dataclass
+class SteadyStateResult:
+    """Steady-state density matrix plus diagnostics (steady.py:39-59).
+    residual = ||L vec(rho)||_2 against the plain Liouvillian."""
+
+    rho: np.ndarray
+    method: str
+    ordering: str
+    residual: float
+    iterations: int
+    fill_factor: float
+    condest: float | None
+    build_time: float
+    factor_time: float
+    solve_time: float
+    converged: bool = True
+    breakdown: bool = False
+    seed: int | None = None
+    inner_iterations: int | None = None
+    error: str | None = None
+    extra: dict = field(default_factory=dict)
+
+
+_STATS_DT = np.dtype([("status", np.int32), ("outer", np.int32), ("inner_last", np.int32),
+                      ("inner_total", np.int32), ("converged", np.int32),
+                      ("breakdown", np.int32), ("final_residual", np.float64),
+                      ("condest", np.float64)])
+assert _STATS_DT.itemsize == _lib.STATS_BYTES
+
+
+def _sync():
+    torch.cuda.synchronize()
+    return time.perf_counter()
+
+
+def start_vector(n, seed):
+    """steady.py:171-174 (host PCG64 draw, normalised on the device later)."""
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal(n) + 1j * rng.standard_normal(n)
+
+
+def _require_plain(L):
+    if L.variant != "plain":
+        raise ValueError(f"expected the plain variant, got {L.variant!r}")
+
+
+def _prepare(system, ordering_name, plain=None):
+    """steady._prepare for "natural" / "rcm" (steady.py:74-94) on the device.
+    Returns (matrix, rhs, plain_ordered, forward, label)."""
+    m = system.matrix
+    if ordering_name == "natural":
+        return m, system.rhs, plain, None, "natural"
+    if ordering_name == "rcm":
+        fwd, inv = ordering.rcm_device(m)
+        pm = ordering.permute(m, fwd, inv)
+        prhs = None
+        if system.rhs is not None:
+            prhs = ordering.permute_vector(system.rhs, fwd, m.nsys, m.n, gather=False)
+        pp = ordering.permute(plain, fwd, inv) if plain is not None else None
+        return pm, prhs, pp, fwd, "rcm"
+    if ordering_name == "cmd":
+        raise NotImplementedError("the 'cmd' ordering (MBM + column minimum degree) is "
+                                  "outside the GPU hot path")
+    raise ValueError(f"unknown ordering {ordering_name!r}")
+
+
+def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0):
+    dev = A.values.device
+    B, n = A.nsys, A.n
+    x = torch.empty(B * n, dtype=torch.complex128, device=dev)
+    stats = torch.zeros(B * _STATS_DT.itemsize, dtype=torch.uint8, device=dev)
+    a = _lib.SolverArgs()
+    a.n, a.nsys, a.mode, a.threads = n, B, mode, threads
+    a.A_rp, a.A_ci, a.A_v = A.row_ptr.data_ptr(), A.col_idx.data_ptr(), A.values.data_ptr()
+    if P is not None:
+        a.P_rp, a.P_ci, a.P_v = P.row_ptr.data_ptr(), P.col_idx.data_ptr(), P.values.data_ptr()
+    if f is not None:
+        a.L_rp, a.L_ci, a.L_v = f.L_rp.data_ptr(), f.L_ci.data_ptr(), f.L_v.data_ptr()
+        a.U_rp, a.U_ci, a.U_v = f.U_rp.data_ptr(), f.U_ci.data_ptr(), f.U_v.data_ptr()
+        a.rdiag, a.pinv = f.rdiag.data_ptr(), f.pinv.data_ptr()
+    a.rhs, a.x, a.stats = rhs.data_ptr(), x.data_ptr(), stats.data_ptr()
+    a.tol, a.max_iter, a.restart_m = float(tol), int(max_iter), int(restart_m)
+    a.max_outer, a.want_condest = MAX_OUTER, 1 if want_condest else 0
+    import ctypes
+    _lib.call("rs_steady_solve", ctypes.byref(a), _lib.stream_ptr())
+    st = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=_STATS_DT)
+    return x, st
+
+
+def _postprocess(x, fwd, L):
+    M = L.matrix
+    D = L.hilbert_dim
+    dev = M.values.device
+    rho = torch.empty(M.nsys * D * D, dtype=torch.complex128, device=dev)
+    res = torch.empty(M.nsys, dtype=torch.float64, device=dev)
+    _lib.call("rs_postprocess", M.nsys, D, _lib.ptr(x), _lib.ptr(fwd), _lib.ptr(M.row_ptr),
+              _lib.ptr(M.col_idx), _lib.ptr(M.values), _lib.ptr(rho), _lib.ptr(res), None,
+              _lib.stream_ptr())
+    return rho.reshape(M.nsys, D, D).cpu().numpy(), res.cpu().numpy()
+
+
+def _check_ops(tol=None, max_iter=None, restart_m=None):
+    if tol is not None and not tol > 0:
+        raise ValueError("tol must be > 0")
+    if max_iter is not None and max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    if restart_m is not None and restart_m < 1:
+        raise ValueError("restart_m must be >= 1")
+
+
+# ------------------------------------------------------------------ API ----
+def solve_direct(L, ordering_name="natural", w=None):
+    """Steady state by one complete-LU solve of the trace-modified system
+    (steady.py:116-134)."""
+    _require_plain(L)
+    t0 = _sync()
+    modified = liouville.build_modified(L, w)
+    mat, rhs, _, fwd, label = _prepare(modified, ordering_name)
+    t1 = _sync()
+    f = factor.lu(mat)
+    t2 = _sync()
+    x, _ = _solve(_lib.LIN_DIRECT, mat, None, f, rhs, 1.0, 1, 1, False)
+    rho, res = _postprocess(x, fwd, L)
+    t3 = _sync()
+    return SteadyStateResult(rho=rho[0], method="direct", ordering=label, residual=float(res[0]),
+                             iterations=0, fill_factor=f.fill_factor, condest=None,
+                             build_time=t1 - t0, factor_time=t2 - t1, solve_time=t3 - t2)
+
+
+def solve_iterative(L, ordering_name="natural", solver="gmres", d=1e-4, p=300.0, tol=1e-14,
+                    restart_m=20, max_iter=1000, w=None):
+    """Preconditioned Krylov on the trace-modified system (steady.py:137-168).
+    Non-convergence and solver breakdown are reported, not raised."""
+    _require_plain(L)
+    if solver not in ("gmres", "bicgstab"):
+        raise ValueError(f"unknown solver {solver!r}")
+    _check_ops(tol, max_iter, restart_m)
+    t0 = _sync()
+    modified = liouville.build_modified(L, w)
+    mat, rhs, _, fwd, label = _prepare(modified, ordering_name)
+    t1 = _sync()
+    f = factor.ilutp(mat, d=d, p=p)
+    t2 = _sync()
+    mode = _lib.LIN_GMRES if solver == "gmres" else _lib.LIN_BICGSTAB
+    x, st = _solve(mode, mat, None, f, rhs, tol, max_iter, restart_m, True)
+    rho, res = _postprocess(x, fwd, L)
+    t3 = _sync()
+    s = st[0]
+    return SteadyStateResult(rho=rho[0], method=f"iterative-{solver}", ordering=label,
+                             residual=float(res[0]), iterations=int(s["inner_last"]),
+                             fill_factor=f.fill_factor, condest=float(s["condest"]),
+                             build_time=t1 - t0, factor_time=t2 - t1, solve_time=t3 - t2,
+                             converged=bool(s["converged"]), breakdown=bool(s["breakdown"]),
+                             extra={"final_residual": float(s["final_residual"])})
+
+
+_STATUS_MSG = {
+    _lib.SOLVE_INNER_BREAKDOWN: (InnerSolverError, "inner Krylov solve broke down; try a "
+                                 "smaller drop tolerance or a larger fill budget"),
+    _lib.SOLVE_INNER_NONFINITE: (InnerSolverError, "inner Krylov solve broke down; try a "
+                                 "smaller drop tolerance or a larger fill budget"),
+    _lib.SOLVE_INNER_NO_PROGRESS: (InnerSolverError, "inner Krylov solve made no progress"),
+    _lib.SOLVE_UNUSABLE_VECTOR: (InnerSolverError, "inner solve returned an unusable vector"),
+    _lib.SOLVE_POWER_NOT_CONVERGED: (PowerIterationError,
+                                     f"no convergence within {MAX_OUTER} outer iterations"),
+}
+
+
+def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, max_iter, seeds,
+                raise_errors, threads=0):
+    _require_plain(L)
+    if inner not in ("direct", "iterative"):
+        raise ValueError(f"unknown inner solve {inner!r}")
+    if not tol > 0:
+        raise ValueError("tol must be > 0")
+    if inner == "iterative" and solver not in ("gmres", "bicgstab"):
+        raise ValueError(f"unknown solver {solver!r}")
+    _check_ops(None, max_iter, restart_m)
+    t0 = _sync()
+    shifted = liouville.shift(L, sigma)
+    mat, _, plain, fwd, label = _prepare(shifted, ordering_name, plain=L.matrix)
+    if plain is None:
+        plain = L.matrix
+    t1 = _sync()
+    if inner == "direct":
+        f = factor.factor_batch(mat, 0.0, float("inf"), raise_on_fail=raise_errors)
+        mode = _lib.INV_DIRECT
+    else:
+        if d < 0:
+            raise ValueError("drop tolerance d must be >= 0")
+        if not p >= 1:
+            raise ValueError("fill limit p must be >= 1")
+        f = factor.factor_batch(mat, float(d), float(p), raise_on_fail=raise_errors)
+        mode = _lib.INV_GMRES if solver == "gmres" else _lib.INV_BICGSTAB
+    t2 = _sync()
+    n, B = mat.n, mat.nsys
+    x0 = np.concatenate([start_vector(n, s) for s in seeds])
+    x0 = torch.from_numpy(x0).to(mat.values.device)
+    if f.L_rp is None:  # some system of the batch failed to factor
+        return None, f, None, None, label, (t0, t1, t2, _sync())
+    x, st = _solve(mode, mat, plain, f, x0, tol, max_iter, restart_m, inner == "iterative",
+                   threads)
+    rho, res = _postprocess(x, fwd, L)
+    t3 = _sync()
+    return (rho, res), f, st, x, label, (t0, t1, t2, t3)
+
+
+def inverse_power(L, sigma=DEFAULT_SIGMA, tol=1e-14, inner="direct", ordering_name="natural",
+                  solver="gmres", d=1e-4, p=300.0, restart_m=20, max_iter=1000,
+                  seed=DEFAULT_SEED):
+    """Null eigenvector of the shifted Liouvillian by inverse-power iteration
+    (steady.py:177-260); inner="iterative" is the paper's doubly-iterative
+    method (ILUTP-preconditioned BiCGStab/GMRES to tol/10 each outer step)."""
+    if L.nsys != 1:
+        raise ValueError("inverse_power takes one system; use inverse_power_batch")
+    out, f, st, _, label, (t0, t1, t2, t3) = _power_core(
+        L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, max_iter, [seed], True)
+    s = st[0]
+    if s["status"] != _lib.SOLVE_OK:
+        exc, msg = _STATUS_MSG[int(s["status"])]
+        raise exc(msg)
+    rho, res = out
+    return SteadyStateResult(
+        rho=rho[0], method="power-direct" if inner == "direct" else "power-doubly-iterative",
+        ordering=label, residual=float(res[0]), iterations=int(s["outer"]),
+        fill_factor=f.fill_factor, condest=float(s["condest"]) if inner == "iterative" else None,
+        build_time=t1 - t0, factor_time=t2 - t1, solve_time=t3 - t2, seed=seed,
+        inner_iterations=int(s["inner_total"]) if inner == "iterative" else None)
+
+
+def inverse_power_batch(L, seeds, sigma=DEFAULT_SIGMA, tol=1e-14, inner="direct",
+                        ordering_name="natural", solver="gmres", d=1e-4, p=300.0,
+                        restart_m=20, max_iter=1000, threads=0):
+    """inverse_power over every system of a block-diagonal batch in one pass
+    (one CTA per system).  Per-system failures are reported on the result's
+    `error` field instead of raising."""
+    seeds = list(seeds)
+    if len(seeds) != L.nsys:
+        raise ValueError("one seed per system required")
+    out, f, st, _, label, (t0, t1, t2, t3) = _power_core(
+        L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, max_iter, seeds, False,
+        threads)
+    results = []
+    method = "power-direct" if inner == "direct" else "power-doubly-iterative"
+    for b in range(L.nsys):
+        if out is None:
+            err = (f"zero pivot at elimination step {int(f.fail[b])}" if f.fail[b] >= 0
+                   else None)
+            results.append(SteadyStateResult(
+                rho=None, method=method, ordering=label, residual=float("nan"), iterations=0,
+                fill_factor=float(f.fill_factors[b]), condest=None, build_time=t1 - t0,
+                factor_time=t2 - t1, solve_time=0.0, seed=seeds[b], error=err))
+            continue
+        s = st[b]
+        err = None if s["status"] == _lib.SOLVE_OK else _STATUS_MSG[int(s["status"])][1]
+        results.append(SteadyStateResult(
+            rho=out[0][b], method=method, ordering=label, residual=float(out[1][b]),
+            iterations=int(s["outer"]), fill_factor=float(f.fill_factors[b]),
+            condest=float(s["condest"]) if inner == "iterative" else None,
+            build_time=t1 - t0, factor_time=t2 - t1, solve_time=t3 - t2, seed=seeds[b],
+            inner_iterations=int(s["inner_total"]) if inner == "iterative" else None,
+            error=err))
+    return results
+
+
+def solve_batch(L, method="bicgstab", ordering_name="natural", d=1e-4, p=300.0, tol=1e-14,
+                restart_m=20, max_iter=1000, w=None, threads=0):
+    """solve_iterative / solve_direct (method="direct") over a batch."""
+    _require_plain(L)
+    t0 = _sync()
+    modified = liouville.build_modified(L, w)
+    mat, rhs, _, fwd, label = _prepare(modified, ordering_name)
+    t1 = _sync()
+    if method == "direct":
+        f = factor.factor_batch(mat, 0.0, float("inf"))
+        mode = _lib.LIN_DIRECT
+    else:
+        f = factor.factor_batch(mat, float(d), float(p))
+        mode = _lib.LIN_GMRES if method == "gmres" else _lib.LIN_BICGSTAB
+    t2 = _sync()
+    x, st = _solve(mode, mat, None, f, rhs, tol, max_iter, restart_m, method != "direct",
+                   threads)
+    rho, res = _postprocess(x, fwd, L)
+    t3 = _sync()
+    name = "direct" if method == "direct" else f"iterative-{method}"
+    return [SteadyStateResult(rho=rho[b], method=name, ordering=label, residual=float(res[b]),
+                              iterations=int(st[b]["inner_last"]),
+                              fill_factor=float(f.fill_factors[b]),
+                              condest=None if method == "direct" else float(st[b]["condest"]),
+                              build_time=t1 - t0, factor_time=t2 - t1, solve_time=t3 - t2,
+                              converged=bool(st[b]["converged"]),
+                              breakdown=bool(st[b]["breakdown"]))
+            for b in range(L.nsys)]

@@ -1,0 +1,95 @@
+"""GPU kernel parity against the CPU oracle (bit-exact for every kernel that
+the reference computes deterministically)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1504_06768_b200 import factor, liouville, ordering
+from paper_1504_06768_b200 import _lib
+from paper_1504_06768_b200.sparse import from_host, CSRMatrix
+from tests.helpers import bits_equal, csr_equal, model, oracle_L
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [("c1", {}), ("c4", {"i": 0}), ("c4", {"i": 300}), ("c2", {})]
+
+
+def _host(o):
+    return CSRMatrix(o.n, o.m, o.rp, o.ci, o.v)
+
+
+@pytest.mark.parametrize("name,kw", SMALL)
+def test_assembly_bit_exact(cuda, name, kw):
+    H, c = model(name, **kw)
+    L = liouville.build_liouvillian(H, c)
+    assert csr_equal(L.matrix, oracle_L(H, c))
+
+
+@pytest.mark.parametrize("name,kw", SMALL)
+def test_shift_modify_bit_exact(cuda, name, kw):
+    H, c = model(name, **kw)
+    L = liouville.build_liouvillian(H, c)
+    Lo = oracle_L(H, c)
+    assert csr_equal(liouville.shift(L).matrix, O.shift(Lo))
+    w = O.default_weight(Lo)
+    mo, _, _ = O.build_modified(Lo, H.matrix.nrows, w)
+    assert csr_equal(liouville.build_modified(L, w=w).matrix, mo)
+    assert abs(liouville.default_weight(L) - w) <= 1e-12 * w
+
+
+@pytest.mark.parametrize("name,kw", SMALL)
+def test_rcm_bit_exact(cuda, name, kw):
+    H, c = model(name, **kw)
+    Lo = oracle_L(H, c)
+    for m in (O.shift(Lo), O.build_modified(Lo, H.matrix.nrows)[0]):
+        fwd, inv = O.rcm(m)
+        p = ordering.rcm(from_host(_host(m)))
+        assert bits_equal(p.forward, fwd) and bits_equal(p.inverse, inv)
+
+
+@pytest.mark.parametrize("name,kw", SMALL)
+def test_spmv_bit_exact(cuda, name, kw):
+    H, c = model(name, **kw)
+    Lo = oracle_L(H, c)
+    x = np.random.default_rng(5).standard_normal(Lo.n) + 1j * np.random.default_rng(6).standard_normal(Lo.n)
+    A = from_host(_host(Lo))
+    y = torch.empty(Lo.n, dtype=torch.complex128, device="cuda")
+    xd = torch.from_numpy(x).cuda()
+    _lib.call("rs_csr_matvec", 1, A.n, _lib.ptr(A.row_ptr), _lib.ptr(A.col_idx),
+              _lib.ptr(A.values), _lib.ptr(xd), _lib.ptr(y), _lib.stream_ptr())
+    assert bits_equal(y.cpu().numpy(), O.csr_matvec(Lo, x))
+
+
+FACTOR_CASES = [("c1", {}, 1e-5, 10.0), ("c1", {}, 0.0, math.inf), ("c1", {}, 1e-4, 300.0),
+                ("c4", {"i": 0}, 0.0, math.inf), ("c2", {}, 1e-4, 300.0)]
+
+
+@pytest.mark.parametrize("name,kw,d,p", FACTOR_CASES)
+def test_factorize_bit_exact(cuda, name, kw, d, p):
+    H, c = model(name, **kw)
+    Lo = O.shift(oracle_L(H, c))
+    fwd, _ = O.rcm(Lo)
+    m = O.permute(Lo, fwd)
+    fo = O.factorize_raw(m, d, p)
+    f = factor.factor_batch(from_host(_host(m)), d, p)
+    lp, li, lx, up, ui, ux, pinv = f.system_raw(0)
+    assert bits_equal(lp, fo.Lp) and bits_equal(up, fo.Up) and bits_equal(pinv, fo.pinv)
+    assert bits_equal(li, fo.Li) and bits_equal(ui, fo.Ui)
+    assert bits_equal(lx, fo.Lx) and bits_equal(ux, fo.Ux)
+    b = np.random.default_rng(9).standard_normal(m.n) + 0.5j
+    assert bits_equal(factor.solve_lu(f, b), fo.solve(b))
+
+
+def test_factorize_breakdown_step(cuda):
+    """Reference breaks down at step n-1 on the shifted JC sweep (1e-5, 10)."""
+    H, c = model("c4", i=0)
+    Lo = O.shift(oracle_L(H, c))
+    fwd, _ = O.rcm(Lo)
+    m = O.permute(Lo, fwd)
+    with pytest.raises(O.Breakdown) as e:
+        O.factorize_raw(m, 1e-5, 10.0)
+    with pytest.raises(factor.PreconditionerBreakdownError, match=f"step {e.value.step}$"):
+        factor.ilutp(from_host(_host(m)), d=1e-5, p=10.0)

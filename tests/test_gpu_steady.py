@@ -1,0 +1,79 @@
+"""End-to-end steady-state parity on the GPU against the oracle (reference
+algorithm on CPU): trace distance <= 1e-6 and ||L vec rho||_2 <= 1e-10."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1504_06768_b200 import liouville, steady
+from tests.helpers import model, oracle_L
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(res, ref, resid=1e-10):
+    assert res.residual <= resid
+    assert O.trace_distance(res.rho, ref["rho"]) <= 1e-6
+
+
+def test_c1_inverse_power_direct(cuda):
+    H, c = model("c1")
+    L = liouville.build_liouvillian(H, c)
+    ref = O.inverse_power(oracle_L(H, c), 20, tol=1e-12, inner="direct", seed=0)
+    res = steady.inverse_power(L, tol=1e-12, inner="direct", ordering_name="rcm", seed=0)
+    _check(res, ref)
+    assert res.iterations == ref["outer"]
+
+
+def test_c1_inverse_power_bicgstab(cuda):
+    H, c = model("c1")
+    L = liouville.build_liouvillian(H, c)
+    ref = O.inverse_power(oracle_L(H, c), 20, tol=1e-12, inner="iterative", solver="bicgstab",
+                          d=1e-5, p=10, seed=0)
+    res = steady.inverse_power(L, tol=1e-12, inner="iterative", ordering_name="rcm",
+                               solver="bicgstab", d=1e-5, p=10, seed=0)
+    _check(res, ref)
+
+
+def test_c1_inverse_power_gmres(cuda):
+    H, c = model("c1")
+    L = liouville.build_liouvillian(H, c)
+    ref = O.inverse_power(oracle_L(H, c), 20, tol=1e-12, inner="iterative", solver="gmres",
+                          d=1e-5, p=10, seed=0)
+    res = steady.inverse_power(L, tol=1e-12, inner="iterative", ordering_name="rcm",
+                               solver="gmres", d=1e-5, p=10, seed=0)
+    _check(res, ref)
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "gmres", "direct"])
+def test_c1_linear(cuda, method):
+    H, c = model("c1")
+    L = liouville.build_liouvillian(H, c)
+    ref = O.solve_linear(oracle_L(H, c), 20, method=method, d=1e-5, p=10, tol=1e-12)
+    if method == "direct":
+        res = steady.solve_direct(L, "rcm")
+    else:
+        res = steady.solve_iterative(L, "rcm", method, d=1e-5, p=10, tol=1e-12)
+        assert res.converged == ref["converged"]
+    _check(res, ref)
+
+
+def test_c2_inverse_power_bicgstab_defaults(cuda):
+    H, c = model("c2")
+    L = liouville.build_liouvillian(H, c)
+    ref = O.inverse_power(oracle_L(H, c), 80, tol=1e-12, inner="iterative", solver="bicgstab",
+                          d=1e-4, p=300, seed=1)
+    res = steady.inverse_power(L, tol=1e-12, inner="iterative", ordering_name="rcm",
+                               solver="bicgstab", d=1e-4, p=300, seed=1)
+    _check(res, ref)
+
+
+def test_c4_batch_power_direct(cuda):
+    idx = [0, 100, 255, 511]
+    models = [model("c4", i=i) for i in idx]
+    L = liouville.build_liouvillian_batch(models)
+    res = steady.inverse_power_batch(L, [2 + i for i in idx], tol=1e-12, inner="direct",
+                                     ordering_name="rcm")
+    for (H, c), i, r in zip(models, idx, res):
+        ref = O.inverse_power(oracle_L(H, c), 40, tol=1e-12, inner="direct", seed=2 + i)
+        assert r.error is None
+        _check(r, ref)
