@@ -54,6 +54,9 @@ typedef struct rs_complex {
 
 int rs_abi_version(void);
 const char* rs_last_error(void);
+/* Number of kernels this library has launched in the process (bench
+ * bookkeeping: gpu_launches). */
+long long rs_launch_count(void);
 
 /* ---- kernel seam (kernels/__init__.py:19-36) ---------------------------- */
 

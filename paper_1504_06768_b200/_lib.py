@@ -86,7 +86,7 @@ _SIGS = {
     "rs_postprocess": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
 }
 
-EXPORTED = tuple(_SIGS) + ("rs_last_error",)
+EXPORTED = tuple(_SIGS) + ("rs_last_error", "rs_launch_count")
 
 _lib = None
 
@@ -107,6 +107,8 @@ def load():
         fn.restype = _i32
     lib.rs_last_error.argtypes = []
     lib.rs_last_error.restype = ctypes.c_char_p
+    lib.rs_launch_count.argtypes = []
+    lib.rs_launch_count.restype = ctypes.c_longlong
     _lib = lib
     return lib
 
@@ -128,6 +130,11 @@ def require_cuda():
     if not torch.cuda.is_available():
         raise RuntimeError("rhosolve-b200 needs a CUDA device (sm_100a); "
                            "there is no CPU fallback")
+
+
+def launch_count():
+    """Kernels launched by the library so far in this process."""
+    return int(load().rs_launch_count())
 
 
 def stream_ptr(stream=None):

@@ -289,12 +289,12 @@ static int op_cdc(int32_t D, const OpCSR& C, const OpCSR& Ct, OpBufs& out, int64
   RS_CUDA_TRY(cudaMallocAsync(&pres, (int64_t)D * D, st));
   RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (D + 1), st));
   RS_CUDA_TRY(cudaMallocAsync(&out.rp, sizeof(int32_t) * (D + 1), st));
-  cdc_dense_kernel<<<D, 128, 0, st>>>(D, Ct, C, acc, pres, counts);
+  cdc_dense_kernel<<<D, 128, 0, st>>>(D, Ct, C, acc, pres, counts); ::rs::count_launch();
   int rc = scan_counts(counts, out.rp, D, nnz, st);
   if (rc == RS_OK) {
     RS_CUDA_TRY(cudaMallocAsync(&out.ci, sizeof(int32_t) * (*nnz + 1), st));
     RS_CUDA_TRY(cudaMallocAsync(&out.v, sizeof(double2) * (*nnz + 1), st));
-    cdc_compact_kernel<<<gridn(D, 128), 128, 0, st>>>(D, acc, pres, out.rp, out.ci, out.v);
+    cdc_compact_kernel<<<gridn(D, 128), 128, 0, st>>>(D, acc, pres, out.rp, out.ci, out.v); ::rs::count_launch();
   }
   cudaFreeAsync(acc, st);
   cudaFreeAsync(pres, st);
@@ -337,7 +337,7 @@ int liouvillian_assemble(int32_t D, const int32_t* Hrp, const int32_t* Hci, cons
     unsigned long long* dm = nullptr;
     RS_CUDA_TRY(cudaMallocAsync(&dm, sizeof(unsigned long long), st));
     RS_CUDA_TRY(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
-    herm_dev_kernel<<<gridn(D, 128), 128, 0, st>>>(D, a.H, dm);
+    herm_dev_kernel<<<gridn(D, 128), 128, 0, st>>>(D, a.H, dm); ::rs::count_launch();
     unsigned long long hv = 0;
     RS_CUDA_TRY(cudaMemcpyAsync(&hv, dm, sizeof(hv), cudaMemcpyDeviceToHost, st));
     RS_CUDA_TRY(cudaStreamSynchronize(st));
@@ -351,11 +351,11 @@ int liouvillian_assemble(int32_t D, const int32_t* Hrp, const int32_t* Hci, cons
       int32_t* counts = nullptr;
       RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (n + 1), st));
       assemble_kernel<false><<<gridn(n, 128), 128, 0, st>>>(a, counts, nullptr, nullptr,
-                                                           nullptr);
+                                                           nullptr); ::rs::count_launch();
       rc = scan_counts(counts, out_rp, n, nnz_out, st);
       cudaFreeAsync(counts, st);
     } else {
-      assemble_kernel<true><<<gridn(n, 128), 128, 0, st>>>(a, nullptr, out_rp, out_ci, out_v);
+      assemble_kernel<true><<<gridn(n, 128), 128, 0, st>>>(a, nullptr, out_rp, out_ci, out_v); ::rs::count_launch();
     }
   }
   free_op(ht, st);

@@ -2,6 +2,7 @@
 // argument validation + dispatch to the launchers; no compute on the host and
 // no fallback path.
 #include <stdarg.h>
+#include <atomic>
 #include <stdio.h>
 #include <string.h>
 
@@ -13,6 +14,9 @@
 namespace rs {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -63,6 +67,7 @@ extern "C" {
 
 int rs_abi_version(void) { return RS_ABI_VERSION; }
 const char* rs_last_error(void) { return g_err; }
+long long rs_launch_count(void) { return g_launches.load(); }
 
 int rs_csr_matvec(int32_t nsys, int32_t n, const int32_t* row_ptr, const int32_t* col_idx,
                   const rs_complex* values, const rs_complex* x, rs_complex* y, void* stream) {
@@ -104,32 +109,31 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.capU = capU;
   a.pinv = pinv;
   a.state = state;
-  a.smem_mode = ilutp_fits_smem(n) ? 1 : 0;
+  a.warps = nsys >= 148 ? 8 : 16;
+  RS_TRY(ilutp_plan(n, a.warps, &a.smem_mode, &a.bits_in_smem));
   const int nwords = (n + 31) / 32;
-  // scratch: x, flag, prow, bits, pattern, urow, uval, lrow, ukeep, lkeep
+  const int64_t NW = N * a.warps;  // per-warp slices
   size_t bytes = 0;
   auto take = [&](size_t b) {
     size_t o = bytes;
     bytes += (b + 255) & ~(size_t)255;
     return o;
   };
-  const size_t o_x = a.smem_mode ? 0 : take(16 * N);
-  const size_t o_flag = a.smem_mode ? 0 : take(4 * N);
-  const size_t o_bits = a.smem_mode ? 0 : take(4 * (size_t)nwords * nsys);
+  const size_t o_x = take(16 * NW);
+  const size_t o_flag = take(4 * NW);
+  const size_t o_bits = a.bits_in_smem ? 0 : take(4 * (size_t)nwords * nsys * a.warps);
   const size_t o_prow = take(4 * N);
-  const size_t o_pat = take(4 * N);
-  const size_t o_urow = take(4 * N);
-  const size_t o_uval = take(16 * N);
-  const size_t o_lrow = take(4 * N);
-  const size_t o_uk = take(N);
-  const size_t o_lk = take(N);
+  const size_t o_pat = take(4 * NW);
+  const size_t o_urow = take(4 * NW);
+  const size_t o_uval = take(16 * NW);
+  const size_t o_lrow = take(4 * NW);
+  const size_t o_uk = take(NW);
+  const size_t o_lk = take(NW);
   unsigned char* ws = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&ws, bytes, st));
-  if (!a.smem_mode) {
-    a.wx = reinterpret_cast<double2*>(ws + o_x);
-    a.wflag = reinterpret_cast<int32_t*>(ws + o_flag);
-    a.wbits = reinterpret_cast<uint32_t*>(ws + o_bits);
-  }
+  a.wx = reinterpret_cast<double2*>(ws + o_x);
+  a.wflag = reinterpret_cast<int32_t*>(ws + o_flag);
+  a.wbits = a.bits_in_smem ? nullptr : reinterpret_cast<uint32_t*>(ws + o_bits);
   a.prow = reinterpret_cast<int32_t*>(ws + o_prow);
   a.wpat = reinterpret_cast<int32_t*>(ws + o_pat);
   a.wurow = reinterpret_cast<int32_t*>(ws + o_urow);
@@ -175,7 +179,18 @@ int rs_lu_solve(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t* L_r
   a.pinv = pinv;
   a.rhs = C2(b);
   a.xout = M2(x);
-  return launch_lu_solve(a, S(stream));
+  cudaStream_t st = S(stream);
+  int dev, max_smem;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  double2* work = nullptr;
+  if (32 * (size_t)n + 2048 > (size_t)max_smem) {
+    RS_CUDA_TRY(cudaMallocAsync(&work, sizeof(double2) * 2 * (size_t)n * nsys, st));
+    a.work = work;
+  }
+  const int rc = launch_lu_solve(a, st);
+  if (work) cudaFreeAsync(work, st);
+  return rc;
 }
 
 int rs_liouvillian(int32_t D, const int32_t* H_rp, const int32_t* H_ci, const rs_complex* H_v,
@@ -286,8 +301,7 @@ int rs_steady_solve(const rs_solver_args* p, void* stream) {
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t flag_bytes = ((size_t)a.n + 15) & ~(size_t)15;
-  a.y_in_smem = (flag_bytes + 16 * (size_t)a.n + 4096 <= (size_t)max_smem) ? 1 : 0;
+  a.y_in_smem = (32 * (size_t)a.n + 4096 <= (size_t)max_smem) ? 1 : 0;
   a.work_stride = solver_work_stride(a.n, a.restart_m);
   double2* work = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&work, sizeof(double2) * a.work_stride * a.B, st));

@@ -78,6 +78,8 @@ __device__ __forceinline__ int warp_lane() { return threadIdx.x & 31; }
 
 namespace rs {
 void set_error(const char* fmt, ...);
+// Host-side count of this library's kernel launches (rs_launch_count()).
+void count_launch();
 }
 
 #define RS_CUDA_TRY(expr)                                                   \

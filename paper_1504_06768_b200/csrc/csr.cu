@@ -89,9 +89,9 @@ int csr_transpose(int B, int32_t n, const int32_t* rp, const int32_t* ci, const 
     RS_CUDA_TRY(cudaMallocAsync(&idx, sizeof(int32_t) * nnz, st));
     RS_CUDA_TRY(cudaMallocAsync(&key2, sizeof(int32_t) * nnz, st));
     RS_CUDA_TRY(cudaMallocAsync(&idx2, sizeof(int32_t) * nnz, st));
-    expand_rows_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, rp, rowid);
+    expand_rows_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, rp, rowid); ::rs::count_launch();
     transpose_keys_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, n, rowid, ci, key, idx,
-                                                              counts);
+                                                              counts); ::rs::count_launch();
     int end_bit = 1;
     while (end_bit < 31 && ((int64_t)1 << end_bit) < nrows) ++end_bit;
     RS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, idx, idx2,
@@ -100,7 +100,7 @@ int csr_transpose(int B, int32_t n, const int32_t* rp, const int32_t* ci, const 
     RS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, idx, idx2,
                                                 (int)nnz, 0, end_bit, st));
     transpose_gather_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, n, idx2, rowid, v,
-                                                                out_ci, out_v);
+                                                                out_ci, out_v); ::rs::count_launch();
   }
   rc = scan_counts(counts, out_rp, nrows, nullptr, st);
   cudaFreeAsync(counts, st);
@@ -160,12 +160,12 @@ int csr_permute(int B, int32_t n, const int32_t* rp, const int32_t* ci, const do
   const int64_t nrows = (int64_t)B * n;
   int32_t* counts = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (nrows + 1), st));
-  permute_count_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, n, rp, inv, counts);
+  permute_count_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, n, rp, inv, counts); ::rs::count_launch();
   int rc = scan_counts(counts, out_rp, nrows, nullptr, st);
   cudaFreeAsync(counts, st);
   if (rc) return rc;
   permute_fill_kernel<<<grid_for(nrows, 128), 128, 0, st>>>(nrows, n, rp, ci, v, fwd, inv,
-                                                            out_rp, out_ci, out_v);
+                                                            out_rp, out_ci, out_v); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -222,12 +222,12 @@ int csr_shift(int B, int32_t n, const int32_t* rp, const int32_t* ci, const doub
   const int64_t nrows = (int64_t)B * n;
   int32_t* counts = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (nrows + 1), st));
-  shift_count_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, n, rp, ci, counts);
+  shift_count_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, n, rp, ci, counts); ::rs::count_launch();
   int rc = scan_counts(counts, out_rp, nrows, nnz_out, st);
   cudaFreeAsync(counts, st);
   if (rc || !out_ci) return rc;
   shift_fill_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, n, rp, ci, v, sigma, out_rp,
-                                                          out_ci, out_v);
+                                                          out_ci, out_v); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -298,12 +298,12 @@ int csr_modify(int B, int32_t n, int32_t D, const int32_t* rp, const int32_t* ci
   const int64_t nrows = (int64_t)B * n;
   int32_t* counts = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (nrows + 1), st));
-  modify_count_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, n, D, rp, ci, counts);
+  modify_count_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, n, D, rp, ci, counts); ::rs::count_launch();
   int rc = scan_counts(counts, out_rp, nrows, nnz_out, st);
   cudaFreeAsync(counts, st);
   if (rc || !out_ci) return rc;
   modify_fill_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, n, D, rp, ci, v, w, out_rp,
-                                                           out_ci, out_v);
+                                                           out_ci, out_v); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -348,7 +348,7 @@ __global__ void default_weight_kernel(int32_t n, const int32_t* rp, const int32_
 
 int csr_default_weight(int B, int32_t n, const int32_t* rp, const int32_t* ci,
                        const double2* v, int signed_mode, double* w, cudaStream_t st) {
-  default_weight_kernel<<<B, 256, 0, st>>>(n, rp, ci, v, signed_mode, w);
+  default_weight_kernel<<<B, 256, 0, st>>>(n, rp, ci, v, signed_mode, w); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -367,7 +367,7 @@ __global__ void row_norms_kernel(int64_t nrows, const int32_t* rp, const double2
 int csr_row_norms(int64_t nrows, const int32_t* rp, const double2* v, double* rn,
                   cudaStream_t st) {
   if (nrows == 0) return RS_OK;
-  row_norms_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, rp, v, rn);
+  row_norms_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(nrows, rp, v, rn); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -417,7 +417,7 @@ int factor_to_csr(int B, int32_t n, const int32_t* cp, const int32_t* ri, const 
   int32_t* crp = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (nrows + 1), st));
   RS_CUDA_TRY(cudaMallocAsync(&crp, sizeof(int32_t) * (nrows + 1), st));
-  factor_strip_count_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(B, n, cp, cap, lower, counts);
+  factor_strip_count_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(B, n, cp, cap, lower, counts); ::rs::count_launch();
   int64_t nnz = 0;
   int rc = scan_counts(counts, crp, nrows, &nnz, st);
   cudaFreeAsync(counts, st);
@@ -431,7 +431,7 @@ int factor_to_csr(int B, int32_t n, const int32_t* cp, const int32_t* ri, const 
   RS_CUDA_TRY(cudaMallocAsync(&cci, sizeof(int32_t) * (nnz + 1), st));
   RS_CUDA_TRY(cudaMallocAsync(&cv, sizeof(double2) * (nnz + 1), st));
   factor_strip_fill_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(B, n, cp, ri, rv, cap, lower,
-                                                                 crp, cci, cv, rU);
+                                                                 crp, cci, cv, rU); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   rc = csr_transpose(B, n, crp, cci, cv, out_rp, out_ci, out_v, st);
   cudaFreeAsync(crp, st);

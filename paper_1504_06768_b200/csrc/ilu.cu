@@ -13,20 +13,25 @@
 //      (-mag, U-before-L, index), and emits U (pivot last) and L (unit
 //      diagonal first, scaled by recipc(pivot)).
 // Each x[i] therefore receives its updates in ascending c, one complex
-// multiply-subtract each.  Here the same ascending order comes from scanning a
-// bitmap of pending pivotal columns; the entries of one L column touch
-// distinct rows, so a warp applies them in parallel without changing any
-// rounding.  Newly reached rows are appended to the pattern in the
-// reference's discovery order (ballot + prefix), so even the raw CSC output
-// (column-internal order included) matches the reference.
+// multiply-subtract each.  Here the ascending order comes from a bitmap of
+// pending pivotal columns; the entries of one L column touch distinct rows,
+// so a warp applies them in parallel without changing any rounding.  Newly
+// reached rows are appended in the reference's discovery order (ballot +
+// prefix), so the raw CSC output matches the reference array for array.
 //
-// B200 mapping: column k depends on every earlier pivot choice, so the
-// elimination is inherently column-sequential.  One warp owns one system and
-// runs warp-synchronously (no CTA barriers on the per-pop critical path);
-// x, the touched-row flags, pinv, prow, Lp and the pending bitmap sit in
-// shared memory when 32 B/row fits (n <= ~7000: configs 1, 2, 4), otherwise
-// in L2-resident global scratch.  A batch of B systems (the config-4 sweep)
-// runs one warp per system across the SMs.
+// B200 mapping -- a column pipeline.  Column k needs every earlier pivot, so
+// the elimination is sequential in its *tail* (the last updates, the pivot
+// search, dropping and emission), but the bulk of a column's work -- the
+// updates from columns finished long ago -- is not.  One CTA owns one system;
+// warp w owns columns k = w, w+W, w+2W, ...  Each warp keeps a private dense
+// accumulator and marker array and a private pending bitmap, and advances a
+// "swept" frontier over finished columns: when column m completes, every
+// warp whose pattern contains prow[m] marks m pending.  A warp pops pending
+// columns strictly below its frontier (no smaller one can ever appear), so up
+// to W columns are updated concurrently while the critical path shrinks to
+// one column's tail.  pinv/prow/Lp (shared) live in shared memory when they
+// fit; completion is a single shared counter with release/acquire fences.
+// A batch of systems (config-4 sweep) is a grid of CTAs.
 //
 // Storage: with a cap, nnz(L)+nnz(U) <= n*cap, so the caller preallocates;
 // complete LU (cap = -1) may overflow, in which case the kernel stops before
@@ -45,7 +50,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
-
 __device__ __forceinline__ int warp_sum_i(int v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
@@ -54,36 +58,35 @@ __device__ __forceinline__ int warp_min_i(int v) {
   for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
   return v;
 }
-
 __device__ __forceinline__ uint64_t mag_key(double2 z) {
   return (uint64_t)__double_as_longlong(cabs1(z));
 }
-
-struct SysPtrs {
-  double2* x;
-  int32_t* flag;
-  int32_t* pinv;
-  int32_t* prow;
-  int32_t* Lp;  // shadow of Lp (smem mode) or the output itself
-  uint32_t* bits;
-};
+__device__ __forceinline__ int vload(const int32_t* p) {
+  return *reinterpret_cast<const volatile int32_t*>(p);
+}
+__device__ __forceinline__ void vstore(int32_t* p, int v) {
+  *reinterpret_cast<volatile int32_t*>(p) = v;
+}
 
 }  // namespace
 
-__host__ __device__ size_t ilutp_smem_per_system(int32_t n) {
+// shared-memory bytes per CTA: pinv, prow, Lp (when shared_in_smem) + the
+// per-warp pending bitmaps (when bits_in_smem) + control words.
+__host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_smem,
+                                            int bits_in_smem) {
   const size_t nwords = ((size_t)n + 31) / 32;
-  size_t bytes = 16 * (size_t)n + 4 * (size_t)n * 3 + 4 * ((size_t)n + 1) +
-                 4 * nwords;
-  return (bytes + 15) & ~(size_t)15;
+  size_t b = 64;
+  if (shared_in_smem) b += 4 * ((size_t)n * 2 + (size_t)n + 1);
+  if (bits_in_smem) b += 4 * nwords * (size_t)warps;
+  return (b + 15) & ~(size_t)15;
 }
 
-__global__ void ilutp_warp_kernel(FactorArgs a) {
+__global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const int wpb = blockDim.x >> 5;
-  const int b = blockIdx.x * wpb + wid;
-  if (b >= a.B) return;
+  const int W = blockDim.x >> 5;
+  const int b = blockIdx.x;
   const int32_t n = a.n;
   const int nwords = (n + 31) >> 5;
   int32_t* state = a.state + 3 * (int64_t)b;
@@ -99,92 +102,102 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
   int32_t* Ui = a.Ui + (int64_t)b * a.capU;
   double2* Ux = a.Ux + (int64_t)b * a.capU;
   int32_t* gpinv = a.pinv + bn;
-  int32_t* gprow = a.prow + bn;
-  int32_t* pat = a.wpat + bn;
-  int32_t* urow = a.wurow + bn;
-  double2* uval = a.wuval + bn;
-  int32_t* lrow = a.wlrow + bn;
-  uint8_t* ukeep = a.wukeep + bn;
-  uint8_t* lkeep = a.wlkeep + bn;
   const double* rn = a.rn ? a.rn + bn : nullptr;
   const int32_t* Ap = a.Ap + bn;
   const double drop = a.drop_tol;
 
-  SysPtrs s;
+  // control words: ctl[0] = number of finished columns, ctl[1] = abort
+  volatile int32_t* ctl = reinterpret_cast<volatile int32_t*>(smem);
+  unsigned char* sp = smem + 64;
+  int32_t *pinv, *prow, *Lp;
   if (a.smem_mode) {
-    unsigned char* base = smem + (size_t)wid * ilutp_smem_per_system(n);
-    s.x = reinterpret_cast<double2*>(base);
-    s.flag = reinterpret_cast<int32_t*>(s.x + n);
-    s.pinv = s.flag + n;
-    s.prow = s.pinv + n;
-    s.Lp = s.prow + n;
-    s.bits = reinterpret_cast<uint32_t*>(s.Lp + n + 1);
-    for (int i = lane; i < n; i += 32) {
-      s.flag[i] = -1;
-      s.pinv[i] = k0 ? gpinv[i] : -1;
-      s.prow[i] = -1;
-    }
-    for (int i = lane; i <= n; i += 32) s.Lp[i] = (i <= k0) ? gLp[i] : 0;
+    pinv = reinterpret_cast<int32_t*>(sp);
+    prow = pinv + n;
+    Lp = prow + n;
+    sp += 4 * ((size_t)n * 2 + (size_t)n + 1);
   } else {
-    s.x = a.wx + bn;
-    s.flag = a.wflag + bn;
-    s.pinv = gpinv;
-    s.prow = gprow;
-    s.Lp = gLp;
-    s.bits = a.wbits + (int64_t)b * nwords;
-    for (int i = lane; i < n; i += 32) {
-      s.flag[i] = -1;
-      if (!k0) s.pinv[i] = -1;
-      s.prow[i] = -1;
+    pinv = gpinv;
+    prow = a.prow + bn;
+    Lp = gLp;
+  }
+  uint32_t* bits;
+  if (a.bits_in_smem) bits = reinterpret_cast<uint32_t*>(sp) + (size_t)wid * nwords;
+  else bits = a.wbits + ((int64_t)b * W + wid) * nwords;
+
+  // per-warp private scratch (global, L1/L2 resident)
+  const int64_t ws = ((int64_t)b * W + wid) * n;
+  double2* x = a.wx + ws;
+  int32_t* flag = a.wflag + ws;
+  int32_t* pat = a.wpat + ws;
+  int32_t* urow = a.wurow + ws;
+  double2* uval = a.wuval + ws;
+  int32_t* lrow = a.wlrow + ws;
+  uint8_t* ukeep = a.wukeep + ws;
+  uint8_t* lkeep = a.wlkeep + ws;
+
+  // ---- init -----------------------------------------------------------------
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (k0 == 0) gpinv[i] = -1;
+    prow[i] = -1;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int pv = gpinv[i];
+    if (a.smem_mode) pinv[i] = pv;
+    if (pv >= 0) prow[pv] = i;  // resume after overflow: prow = pinv^-1
+  }
+  if (a.smem_mode)
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) Lp[i] = (i <= k0) ? gLp[i] : 0;
+  for (int i = lane; i < n; i += 32) flag[i] = -1;
+  for (int w = lane; w < nwords; w += 32) bits[w] = 0u;
+  if (threadIdx.x == 0) {
+    ctl[0] = k0;
+    ctl[1] = 0;
+    if (k0 == 0) {
+      gLp[0] = 0;
+      gUp[0] = 0;
+      Lp[0] = 0;
     }
   }
-  __syncwarp();
-  if (k0) {  // resumed after a capacity overflow: prow is the inverse of pinv
-    for (int i = lane; i < n; i += 32) {
-      const int pv = s.pinv[i];
-      if (pv >= 0) s.prow[pv] = i;
-    }
-  }
-  for (int w = lane; w < nwords; w += 32) s.bits[w] = 0u;
-  if (k0 == 0 && lane == 0) {
-    gLp[0] = 0;
-    gUp[0] = 0;
-    s.Lp[0] = 0;
-  }
-  __syncwarp();
-  int32_t lnnz = k0 ? gLp[k0] : 0;
-  int32_t unnz = k0 ? gUp[k0] : 0;
+  __threadfence_block();
+  __syncthreads();
   const bool have_cap = a.fill_cap >= 0;
 
-  for (int k = k0; k < n; ++k) {
+  // round-robin columns, starting at the resume point
+  for (int k = k0 + wid; k < n; k += W) {
     const int j = a.q ? a.q[bn + k] : k;
-    // ---- 1. scatter column j, seed the pending set ------------------------
+    int scanned = ctl[0];
+    __syncwarp();
+    if (ctl[1]) break;
+    __threadfence_block();
+    // ---- 1. scatter column j; seed pending with columns already finished --
     const int32_t c0 = Ap[j], c1 = Ap[j + 1];
     int npat = c1 - c0;
     int lowc = 0x7fffffff;
     for (int e = c0 + lane; e < c1; e += 32) {
       const int i = a.Ai[e];
-      s.x[i] = a.Ax[e];
-      s.flag[i] = k;
+      x[i] = a.Ax[e];
+      flag[i] = k;
       pat[e - c0] = i;
-      const int pv = s.pinv[i];
-      if (pv >= 0) {
-        atomicOr(&s.bits[pv >> 5], 1u << (pv & 31));
+      const int pv = vload(pinv + i);
+      if (pv >= 0 && pv < scanned) {
+        atomicOr(&bits[pv >> 5], 1u << (pv & 31));
         lowc = min(lowc, pv);
       }
     }
     lowc = warp_min_i(lowc);
     __syncwarp();
 
-    // ---- 2. left-looking updates in ascending pivotal order ---------------
+    // ---- 2. updates in ascending pivotal order, gated by the frontier -----
     int unum = 0;
-    const int wend = (k + 31) >> 5;
-    int w = (lowc == 0x7fffffff) ? wend : (lowc >> 5);
+    int w = (lowc == 0x7fffffff) ? ((scanned + 31) >> 5) : (lowc >> 5);
+    bool aborted = false;
     while (true) {
+      const int wend = (scanned + 31) >> 5;
       int c = -1;
       while (w < wend) {
         const int ww = w + lane;
-        const uint32_t bv = (ww < wend) ? s.bits[ww] : 0u;
+        const uint32_t bv = (ww < wend) ? bits[ww] : 0u;
         const unsigned m = __ballot_sync(FULL, bv != 0u);
         if (m) {
           const int src = __ffs(m) - 1;
@@ -195,13 +208,37 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
         }
         w += 32;
       }
-      if (c < 0) break;
-      const int pr = s.prow[c];
-      const double2 xc = s.x[pr];
-      const int32_t p0 = s.Lp[c] + 1, p1 = s.Lp[c + 1];
+      if (c < 0) {
+        if (scanned == k) break;
+        // advance the frontier over newly finished columns
+        int d;
+        while ((d = ctl[0]) == scanned && !ctl[1]) {
+        }
+        if (ctl[1]) {
+          aborted = true;
+          break;
+        }
+        __threadfence_block();
+        int newlow = 0x7fffffff;
+        for (int m = scanned + lane; m < d; m += 32) {
+          const int r = vload(prow + m);
+          if (flag[r] == k) {
+            atomicOr(&bits[m >> 5], 1u << (m & 31));
+            newlow = min(newlow, m);
+          }
+        }
+        newlow = warp_min_i(newlow);
+        __syncwarp();
+        w = (newlow == 0x7fffffff) ? ((d + 31) >> 5) : (newlow >> 5);
+        scanned = d;
+        continue;
+      }
+      const int pr = vload(prow + c);
+      const double2 xc = x[pr];
+      const int32_t p0 = vload(Lp + c) + 1, p1 = vload(Lp + c + 1);
       __syncwarp();
       if (lane == 0) {
-        atomicAnd(&s.bits[w], ~(1u << (c & 31)));
+        atomicAnd(&bits[w], ~(1u << (c & 31)));
         urow[unum] = c;
         uval[unum] = xc;
       }
@@ -215,26 +252,28 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
         if (act) {
           i = Li[p];
           lv = Lx[p];
-          isnew = s.flag[i] != k;
+          isnew = flag[i] != k;
         }
         const unsigned nm = __ballot_sync(FULL, isnew);
         if (act) {
           double2 xi;
           if (isnew) {
-            s.flag[i] = k;
+            flag[i] = k;
             xi = make_double2(0.0, 0.0);
             pat[npat + __popc(nm & lanemask_lt())] = i;
-            const int pv = s.pinv[i];
-            if (pv >= 0) atomicOr(&s.bits[pv >> 5], 1u << (pv & 31));
+            const int pv = vload(pinv + i);
+            if (pv >= 0 && pv < scanned) atomicOr(&bits[pv >> 5], 1u << (pv & 31));
           } else {
-            xi = s.x[i];
+            xi = x[i];
           }
-          s.x[i] = csub(xi, cmul_plain(lv, xc));
+          x[i] = csub(xi, cmul_plain(lv, xc));
         }
         npat += __popc(nm);
       }
       __syncwarp();
     }
+    if (aborted) break;
+    __threadfence_block();  // acquire: every column < k is final
 
     // ---- 3. pivot: max |re|+|im| over non-pivotal rows, ties -> lowest row -
     double best = -1.0;
@@ -244,11 +283,11 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
       const int t = base + lane;
       const bool act = t < npat;
       const int i = act ? pat[t] : 0;
-      const bool cand = act && s.pinv[i] < 0;
+      const bool cand = act && vload(pinv + i) < 0;
       const unsigned cm = __ballot_sync(FULL, cand);
       if (cand) {
         lrow[lnum + __popc(cm & lanemask_lt())] = i;
-        const double mag = cabs1(s.x[i]);
+        const double mag = cabs1(x[i]);
         if (mag > best || (mag == best && i < ipiv)) {
           best = mag;
           ipiv = i;
@@ -268,23 +307,18 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
       if (lane == 0) {
         state[0] = FAC_ZERO_PIVOT;
         state[1] = k;
+        ctl[1] = 1;
       }
-      if (a.smem_mode) {
-        for (int i = lane; i < n; i += 32) {
-          gpinv[i] = s.pinv[i];
-          gprow[i] = s.prow[i];
-        }
-      }
-      return;
+      break;
     }
-    const double2 piv = s.x[ipiv];
+    const double2 piv = x[ipiv];
     __syncwarp();
 
     // ---- 4. dropping ------------------------------------------------------
     int kept_u = 0, kept_l = 0;
     for (int t = lane; t < unum; t += 32) {
       bool keep = true;
-      if (drop > 0.0 && cabs1(uval[t]) < drop * rn[s.prow[urow[t]]]) keep = false;
+      if (drop > 0.0 && cabs1(uval[t]) < drop * rn[vload(prow + urow[t])]) keep = false;
       ukeep[t] = keep;
       kept_u += keep;
     }
@@ -292,7 +326,7 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
       const int i = lrow[t];
       bool keep = true;
       if (i == ipiv) keep = false;
-      else if (drop > 0.0 && cabs1(s.x[i]) < drop * rn[i]) keep = false;
+      else if (drop > 0.0 && cabs1(x[i]) < drop * rn[i]) keep = false;
       lkeep[t] = keep;
       kept_l += keep;
     }
@@ -306,28 +340,22 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
       int allowed = a.fill_cap - 2;
       if (allowed < 0) allowed = 0;
       if (allowed > ncand) allowed = ncand;
-      // Threshold T = allowed-th largest magnitude key (keys are the bit
-      // patterns of non-negative doubles, so integer order == value order).
       uint64_t T = 0;
       uint32_t S = 0xffffffffu;
       if (allowed > 0) {
         for (int bit = 62; bit >= 0; --bit) {
           const uint64_t cand = T | (1ull << bit);
           int cnt = 0;
-          for (int t = lane; t < unum; t += 32)
-            cnt += (ukeep[t] && mag_key(uval[t]) >= cand);
-          for (int t = lane; t < lnum; t += 32)
-            cnt += (lkeep[t] && mag_key(s.x[lrow[t]]) >= cand);
+          for (int t = lane; t < unum; t += 32) cnt += (ukeep[t] && mag_key(uval[t]) >= cand);
+          for (int t = lane; t < lnum; t += 32) cnt += (lkeep[t] && mag_key(x[lrow[t]]) >= cand);
           cnt = warp_sum_i(cnt);
           if (cnt >= allowed) T = cand;
         }
         int gt = 0;
         for (int t = lane; t < unum; t += 32) gt += (ukeep[t] && mag_key(uval[t]) > T);
-        for (int t = lane; t < lnum; t += 32)
-          gt += (lkeep[t] && mag_key(s.x[lrow[t]]) > T);
+        for (int t = lane; t < lnum; t += 32) gt += (lkeep[t] && mag_key(x[lrow[t]]) > T);
         gt = warp_sum_i(gt);
-        const int need = allowed - gt;  // >= 1 ties at T to take
-        // S = need-th smallest secondary key (dom<<31 | idx) among ties.
+        const int need = allowed - gt;
         S = 0;
         for (int bit = 31; bit >= 0; --bit) {
           const uint32_t cand = S | (1u << bit);
@@ -335,7 +363,7 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
           for (int t = lane; t < unum; t += 32)
             cnt += (ukeep[t] && mag_key(uval[t]) == T && (uint32_t)urow[t] < cand);
           for (int t = lane; t < lnum; t += 32)
-            cnt += (lkeep[t] && mag_key(s.x[lrow[t]]) == T &&
+            cnt += (lkeep[t] && mag_key(x[lrow[t]]) == T &&
                     ((1u << 31) | (uint32_t)lrow[t]) < cand);
           cnt = warp_sum_i(cnt);
           if (cnt < need) S = cand;
@@ -355,7 +383,7 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
       for (int t = lane; t < lnum; t += 32) {
         bool keep = false;
         if (allowed > 0 && lkeep[t]) {
-          const uint64_t kk = mag_key(s.x[lrow[t]]);
+          const uint64_t kk = mag_key(x[lrow[t]]);
           keep = kk > T || (kk == T && ((1u << 31) | (uint32_t)lrow[t]) <= S);
         }
         lkeep[t] = keep;
@@ -366,19 +394,16 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
       __syncwarp();
     }
 
-    // ---- 6. emit U (kept rows ascending, pivot last) and L (unit first) ---
+    // ---- 6. emit U (kept rows ascending, pivot last), L (unit first) ------
+    const int32_t lnnz = vload(Lp + k);
+    const int32_t unnz = vload(gUp + k);
     if ((int64_t)unnz + kept_u + 1 > a.capU || (int64_t)lnnz + kept_l + 1 > a.capL) {
       if (lane == 0) {
         state[0] = FAC_OVERFLOW;
         state[1] = k;
+        ctl[1] = 1;
       }
-      if (a.smem_mode) {
-        for (int i = lane; i < n; i += 32) {
-          gpinv[i] = s.pinv[i];
-          gprow[i] = s.prow[i];
-        }
-      }
-      return;
+      break;
     }
     int off = unnz;
     for (int base = 0; base < unum; base += 32) {
@@ -395,10 +420,8 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
     if (lane == 0) {
       Ui[off] = k;
       Ux[off] = piv;
-      gUp[k + 1] = off + 1;
     }
-    unnz = off + 1;
-
+    const int32_t unew = off + 1;
     const double2 rp = recipc(piv);
     if (lane == 0) {
       Li[lnnz] = ipiv;
@@ -413,30 +436,30 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
         const int o = off + __popc(m & lanemask_lt());
         const int i = lrow[t];
         Li[o] = i;
-        Lx[o] = cmul_plain(s.x[i], rp);
+        Lx[o] = cmul_plain(x[i], rp);
       }
       off += __popc(m);
     }
-    lnnz = off;
+    __threadfence_block();
+    __syncwarp();
     if (lane == 0) {
-      gLp[k + 1] = off;
-      s.Lp[k + 1] = off;
-      s.pinv[ipiv] = k;
-      s.prow[k] = ipiv;
+      vstore(gUp + k + 1, unew);
+      vstore(gLp + k + 1, off);
+      if (a.smem_mode) vstore(Lp + k + 1, off);
+      vstore(pinv + ipiv, k);
+      if (a.smem_mode) gpinv[ipiv] = k;
+      vstore(prow + k, ipiv);
+      __threadfence_block();  // release column k
+      ctl[0] = k + 1;
     }
     __syncwarp();
   }
-
-  // ---- finish: publish pinv/prow, remap L rows to pivotal indices ---------
-  if (a.smem_mode) {
-    for (int i = lane; i < n; i += 32) {
-      gpinv[i] = s.pinv[i];
-      gprow[i] = s.prow[i];
-    }
-  }
-  __syncwarp();
-  for (int p = lane; p < lnnz; p += 32) Li[p] = s.pinv[Li[p]];
-  if (lane == 0) {
+  __syncthreads();
+  if (ctl[1]) return;  // zero pivot or overflow: state already recorded
+  // ---- finish: remap L rows to pivotal indices ------------------------------
+  const int32_t lnnz = gLp[n];
+  for (int p = threadIdx.x; p < lnnz; p += blockDim.x) Li[p] = pinv[Li[p]];
+  if (threadIdx.x == 0) {
     state[0] = FAC_DONE;
     state[1] = -1;
   }
@@ -444,42 +467,24 @@ __global__ void ilutp_warp_kernel(FactorArgs a) {
 
 int launch_ilutp(const FactorArgs& a, cudaStream_t st) {
   if (a.B == 0 || a.n == 0) return RS_OK;
-  int dev;
-  RS_CUDA_TRY(cudaGetDevice(&dev));
-  int max_smem = 0;
-  RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem,
-                                     cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t per = ilutp_smem_per_system(a.n);
-  int spb = 1;  // systems (warps) per CTA
-  size_t smem = 0;
-  if (a.smem_mode) {
-    spb = (int)((size_t)max_smem / per);
-    if (spb < 1) {
-      set_error("ilutp smem mode requested but n=%d needs %zu B", a.n, per);
-      return RS_ERR_ARG;
-    }
-    if (spb > 4) spb = 4;
-    if (spb > a.B) spb = a.B;
-    smem = per * spb;
-    RS_CUDA_TRY(cudaFuncSetAttribute(ilutp_warp_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-  } else {
-    spb = a.B < 4 ? a.B : 4;
-  }
-  const int grid = (a.B + spb - 1) / spb;
-  ilutp_warp_kernel<<<grid, 32 * spb, smem, st>>>(a);
+  const int W = a.warps;
+  const size_t smem = ilutp_smem_bytes(a.n, W, a.smem_mode, a.bits_in_smem);
+  RS_CUDA_TRY(cudaFuncSetAttribute(ilutp_pipeline_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ilutp_pipeline_kernel<<<a.B, 32 * W, smem, st>>>(a); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
 
-bool ilutp_fits_smem(int32_t n) {
+int ilutp_plan(int32_t n, int warps, int* smem_mode, int* bits_in_smem) {
   int dev = 0, max_smem = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return false;
-  if (cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
-                             dev) != cudaSuccess)
-    return false;
-  return ilutp_smem_per_system(n) <= (size_t)max_smem;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // keep ~96 KB of the carveout as L1 for the per-warp accumulators
+  const size_t budget = (size_t)max_smem > 131072 ? (size_t)max_smem - 98304 : 32768;
+  *bits_in_smem = ilutp_smem_bytes(n, warps, 0, 1) <= budget;
+  *smem_mode = ilutp_smem_bytes(n, warps, 1, *bits_in_smem) <= budget;
+  return RS_OK;
 }
 
 }  // namespace rs

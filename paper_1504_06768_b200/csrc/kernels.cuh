@@ -43,23 +43,25 @@ struct FactorArgs {
   int32_t* pinv;  // [B*n]
   int32_t* prow;  // [B*n]
   int32_t* state;  // [B*3]: status, fail/next col, unused
-  // global scratch (per system slices of n)
+  // per-warp private scratch: (B*warps) slices of n
   double2* wx;
   int32_t* wflag;
-  int32_t* wpinv_unused;
-  uint32_t* wbits;  // [B*nwords]
+  uint32_t* wbits;  // [B*warps*nwords] when !bits_in_smem
   int32_t* wpat;
   int32_t* wurow;
   double2* wuval;
   int32_t* wlrow;
   uint8_t* wukeep;
   uint8_t* wlkeep;
-  int smem_mode;  // 1: x/flag/pinv/bits live in shared memory
+  int smem_mode;     // 1: pinv / prow / Lp shadow live in shared memory
+  int bits_in_smem;  // 1: per-warp pending bitmaps in shared memory
+  int warps;         // warps (columns in flight) per system
 };
 // state[3b+0] codes
 enum { FAC_RUNNING = 0, FAC_DONE = 1, FAC_ZERO_PIVOT = 2, FAC_OVERFLOW = 3 };
 int launch_ilutp(const FactorArgs& a, cudaStream_t st);
-__host__ __device__ size_t ilutp_smem_per_system(int32_t n);
-bool ilutp_fits_smem(int32_t n);
+__host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_smem,
+                                            int bits_in_smem);
+int ilutp_plan(int32_t n, int warps, int* smem_mode, int* bits_in_smem);
 
 }  // namespace rs

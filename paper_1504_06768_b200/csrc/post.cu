@@ -89,7 +89,7 @@ int postprocess(int B, int32_t D, const double2* x, const int32_t* fwd, const in
   const int64_t n = (int64_t)D * D;
   double2* tmp = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(double2) * n * B, st));
-  postprocess_kernel<<<B, 512, 0, st>>>(D, x, fwd, Lrp, Lci, Lv, rho, tmp, residual, trace_out);
+  postprocess_kernel<<<B, 512, 0, st>>>(D, x, fwd, Lrp, Lci, Lv, rho, tmp, residual, trace_out); ::rs::count_launch();
   cudaFreeAsync(tmp, st);
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
@@ -120,6 +120,7 @@ int permute_vector(int B, int32_t n, const double2* x, const int32_t* fwd, doubl
   const unsigned grid = (unsigned)((total + 255) / 256);
   if (gather) unpermute_kernel<<<grid, 256, 0, st>>>(total, n, x, fwd, out);
   else scatter_perm_kernel<<<grid, 256, 0, st>>>(total, n, x, fwd, out);
+  ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }

@@ -213,13 +213,13 @@ int rcm_order(int B, int32_t n, const int32_t* rp, const int32_t* ci, int32_t* f
   RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (nrows + 1), st));
   RS_CUDA_TRY(cudaMallocAsync(&arp, sizeof(int32_t) * (nrows + 1), st));
   sym_adj_kernel<false><<<gridr(nrows, 256), 256, 0, st>>>(nrows, n, rp, ci, trp, tci, counts,
-                                                          nullptr, nullptr);
+                                                          nullptr, nullptr); ::rs::count_launch();
   int64_t annz = 0;
   rc = scan_counts(counts, arp, nrows, &annz, st);
   if (rc) return rc;
   RS_CUDA_TRY(cudaMallocAsync(&aci, sizeof(int32_t) * (annz + 1), st));
   sym_adj_kernel<true><<<gridr(nrows, 256), 256, 0, st>>>(nrows, n, rp, ci, trp, tci, nullptr,
-                                                         arp, aci);
+                                                         arp, aci); ::rs::count_launch();
   RcmArgs a;
   a.n = n;
   a.arp = arp;
@@ -233,7 +233,7 @@ int rcm_order(int B, int32_t n, const int32_t* rp, const int32_t* ci, int32_t* f
   a.boff = scratch + 4 * nrows;
   a.fwd = fwd;
   a.inv = inv;
-  rcm_kernel<<<B, 1024, 0, st>>>(a);
+  rcm_kernel<<<B, 1024, 0, st>>>(a); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   cudaFreeAsync(scratch, st);
   cudaFreeAsync(trp, st);

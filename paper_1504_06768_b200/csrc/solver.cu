@@ -49,8 +49,8 @@ struct Ctx {
   const double2 *Lv, *Uv, *rU;
   bool have_M;
   // scratch
-  double2* y;  // triangular-solve vector (smem or global)
-  volatile uint8_t* ready;
+  double2* y;   // triangular-solve scratch P (smem or global)
+  double2* y2;  // triangular-solve scratch Q
   double* red;
   double2* small;  // GMRES H/g/sn (global, per system)
   double* cs;
@@ -58,6 +58,8 @@ struct Ctx {
 
 // out = M^{-1} in  (factor.solve_lu, factor.py:137-149: y[pinv] = b; L; U;
 // x[q] = y with q = identity on the natural/RCM path).  out may alias in.
+// Two scratch vectors P, Q (shared memory when they fit): P = permuted rhs,
+// Q = lower-solve output, then P is reused as the upper-solve output.
 __device__ void psolve(const Ctx& C, const double2* in, double2* out) {
   const int n = C.n;
   if (!C.have_M) {
@@ -66,21 +68,23 @@ __device__ void psolve(const Ctx& C, const double2* in, double2* out) {
     __syncthreads();
     return;
   }
-  double2* y = C.y;
+  double2* P = C.y;
+  double2* Q = C.y2;
+  const double2 s = cta::sentinel2();
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    y[C.pinv[i]] = in[i];
-    C.ready[i] = 0;
+    P[C.pinv[i]] = in[i];
+    Q[i] = s;
   }
   __syncthreads();
-  cta::lower_solve(n, C.Lrp, C.Lci, C.Lv, y, C.ready);
+  cta::lower_solve(n, C.Lrp, C.Lci, C.Lv, P, Q);
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) C.ready[i] = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) P[i] = s;
   __syncthreads();
-  cta::upper_solve(n, C.Urp, C.Uci, C.Uv, C.rU, y, C.ready);
+  cta::upper_solve(n, C.Urp, C.Uci, C.Uv, C.rU, Q, P);
   __syncthreads();
-  if (out != y)
-    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = y[i];
+  if (out != P)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[i];
   __syncthreads();
 }
 
@@ -418,15 +422,18 @@ __global__ void __launch_bounds__(512) steady_solver_kernel(SolverArgs a) {
   C.pinv = a.pinv ? a.pinv + bn : nullptr;
   C.red = red;
   double2* ws = a.work + (int64_t)b * a.work_stride;
-  C.ready = reinterpret_cast<volatile uint8_t*>(smem);
-  const size_t flag_bytes = ((size_t)n + 15) & ~(size_t)15;
-  if (a.y_in_smem) C.y = reinterpret_cast<double2*>(smem + flag_bytes);
-  else C.y = ws;  // slot 0
+  if (a.y_in_smem) {
+    C.y = reinterpret_cast<double2*>(smem);
+    C.y2 = C.y + n;
+  } else {
+    C.y = ws;  // slots 0 and 1
+    C.y2 = ws + n;
+  }
   const int m = a.restart_m;
-  C.small = ws + (int64_t)n;  // (m+1)*m + (m+1) + m + m complex
+  C.small = ws + 2 * (int64_t)n;  // (m+1)*m + (m+1) + m + m complex
   C.cs = reinterpret_cast<double*>(C.small + (m + 1) * m + (m + 1) + 2 * m);
   const int64_t small_slots = ((m + 1) * m + (m + 1) + 3 * m + n - 1) / n + 1;
-  double2* vb = ws + (int64_t)n * (1 + small_slots);
+  double2* vb = ws + (int64_t)n * (2 + small_slots);
   Vecs W;
   W.x = vb + 0 * (int64_t)n;
   W.r = vb + 1 * (int64_t)n;
@@ -580,7 +587,7 @@ __global__ void __launch_bounds__(512) steady_solver_kernel(SolverArgs a) {
 int64_t solver_work_stride(int32_t n, int restart_m) {
   const int m = restart_m;
   const int64_t small_slots = ((int64_t)(m + 1) * m + (m + 1) + 3 * m + n - 1) / n + 1;
-  return (int64_t)n * (1 + small_slots + 9 + (m + 1) + 2);
+  return (int64_t)n * (2 + small_slots + 9 + (m + 1) + 2);
 }
 
 int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
@@ -588,15 +595,14 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t flag_bytes = ((size_t)a.n + 15) & ~(size_t)15;
-  size_t smem = flag_bytes + (a.y_in_smem ? 16 * (size_t)a.n : 0);
+  size_t smem = a.y_in_smem ? 32 * (size_t)a.n : 0;
   if (smem + 2048 > (size_t)max_smem) {
     set_error("steady solver: n=%d needs %zu B of shared memory", a.n, smem);
     return RS_ERR_UNSUPPORTED;
   }
   RS_CUDA_TRY(cudaFuncSetAttribute(steady_solver_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  steady_solver_kernel<<<a.B, a.threads, smem, st>>>(a);
+  steady_solver_kernel<<<a.B, a.threads, smem, st>>>(a); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -622,9 +628,13 @@ __global__ void __launch_bounds__(512) lu_solve_kernel(SolverArgs a, int y_in_sm
   C.Uv = a.Uv;
   C.rU = a.rU + bn;
   C.pinv = a.pinv + bn;
-  C.ready = reinterpret_cast<volatile uint8_t*>(smem);
-  const size_t flag_bytes = ((size_t)n + 15) & ~(size_t)15;
-  C.y = y_in_smem ? reinterpret_cast<double2*>(smem + flag_bytes) : a.xout + bn;
+  if (y_in_smem) {
+    C.y = reinterpret_cast<double2*>(smem);
+    C.y2 = C.y + n;
+  } else {
+    C.y = a.work + 2 * bn;
+    C.y2 = C.y + n;
+  }
   psolve(C, a.rhs + bn, a.xout + bn);
 }
 
@@ -633,17 +643,15 @@ int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t flag_bytes = ((size_t)a.n + 15) & ~(size_t)15;
-  int y_smem = flag_bytes + 16 * (size_t)a.n + 2048 <= (size_t)max_smem;
-  if (a.rhs == a.xout) y_smem = 1;  // in-place needs a separate y
-  size_t smem = flag_bytes + (y_smem ? 16 * (size_t)a.n : 0);
-  if (smem + 1024 > (size_t)max_smem) {
-    set_error("lu_solve: n=%d too large for an in-place apply", a.n);
+  const int y_smem = 32 * (size_t)a.n + 2048 <= (size_t)max_smem;
+  size_t smem = y_smem ? 32 * (size_t)a.n : 0;
+  if (!y_smem && !a.work) {
+    set_error("lu_solve: n=%d needs global scratch", a.n);
     return RS_ERR_UNSUPPORTED;
   }
   RS_CUDA_TRY(cudaFuncSetAttribute(lu_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-  lu_solve_kernel<<<a.B, 512, smem, st>>>(a, y_smem);
+  lu_solve_kernel<<<a.B, 512, smem, st>>>(a, y_smem); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }

@@ -80,7 +80,7 @@ int launch_spmv(int64_t nrows, int32_t n, const int32_t* rp, const int32_t* ci,
   }
   const int64_t grid = (nrows + SPMV_ROWS - 1) / SPMV_ROWS;
   spmv_staged_kernel<<<(unsigned)grid, SPMV_ROWS, smem, st>>>(nrows, n, rp, ci,
-                                                              v, x, y);
+                                                              v, x, y); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }

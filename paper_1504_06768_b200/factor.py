@@ -76,7 +76,7 @@ def _transpose(M):
     return rp, ci, v
 
 
-def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True):
+def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
     """factor._factor (factor.py:70-112) for every system of a DeviceCSR."""
     n, B = M.n, M.nsys
     dev = M.values.device
@@ -103,6 +103,8 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True):
     per_col = max(cap - 1, 1) if cap >= 0 else None
     guess = max(8 * maxnnz, 2 * n, 16)
     capL = capU = min(n * per_col, guess) if per_col else guess
+    if capacity is not None:  # tests: force the overflow/resume path
+        capL = capU = max(int(capacity), n)
     Lp = torch.zeros(B * (n + 1), dtype=torch.int32, device=dev)
     Up = torch.zeros_like(Lp)
     Li = torch.empty(B * capL, dtype=torch.int32, device=dev)

@@ -93,3 +93,38 @@ def test_factorize_breakdown_step(cuda):
         O.factorize_raw(m, 1e-5, 10.0)
     with pytest.raises(factor.PreconditionerBreakdownError, match=f"step {e.value.step}$"):
         factor.ilutp(from_host(_host(m)), d=1e-5, p=10.0)
+
+
+def test_factorize_overflow_resume(cuda):
+    """Complete LU from a deliberately tiny capacity: the kernel stops at the
+    first column that does not fit, the host grows the buffers and resumes;
+    the result must still equal the reference factors bit for bit."""
+    H, c = model("c2")
+    Lo = O.shift(oracle_L(H, c))
+    fwd, _ = O.rcm(Lo)
+    m = O.permute(Lo, fwd)
+    fo = O.factorize_raw(m, 0.0, math.inf)
+    f = factor.factor_batch(from_host(_host(m)), 0.0, math.inf, capacity=m.n + 7)
+    lp, li, lx, up, ui, ux, pinv = f.system_raw(0)
+    assert bits_equal(lp, fo.Lp) and bits_equal(li, fo.Li) and bits_equal(lx, fo.Lx)
+    assert bits_equal(up, fo.Up) and bits_equal(ui, fo.Ui) and bits_equal(ux, fo.Ux)
+
+
+def test_factorize_batch_matches_single(cuda):
+    """Block-diagonal batch (one CTA per system) == per-system reference."""
+    mats = []
+    for i in (0, 7, 300):
+        H, c = model("c4", i=i)
+        Lo = O.build_modified(oracle_L(H, c), 40)[0]
+        fwd, _ = O.rcm(Lo)
+        mats.append(O.permute(Lo, fwd))
+    f = factor.factor_batch(from_host([_host(m) for m in mats]), 1e-5, 10.0)
+    for b, m in enumerate(mats):
+        fo = O.factorize_raw(m, 1e-5, 10.0)
+        lp, li, lx, up, ui, ux, pinv = f.system_raw(b)
+        assert bits_equal(lx, fo.Lx) and bits_equal(ux, fo.Ux) and bits_equal(li, fo.Li)
+        x = np.random.default_rng(b).standard_normal(m.n) + 0j
+        xs = np.zeros(3 * m.n, complex)
+        xs[b * m.n:(b + 1) * m.n] = x
+        got = factor.solve_lu(f, xs)[b * m.n:(b + 1) * m.n]
+        assert bits_equal(got, fo.solve(x))
