@@ -17,6 +17,7 @@ static thread_local char g_err[1024] = "";
 static std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static unsigned long long* g_factor_probe = nullptr;  // tuning hook
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -68,6 +69,12 @@ extern "C" {
 int rs_abi_version(void) { return RS_ABI_VERSION; }
 const char* rs_last_error(void) { return g_err; }
 long long rs_launch_count(void) { return g_launches.load(); }
+// Tuning hook (not part of the documented ABI): when set, the next
+// factorizations record per-column phase clocks of system 0 into buf[n*6].
+int rs_debug_factor_probe(void* buf) {
+  g_factor_probe = reinterpret_cast<unsigned long long*>(buf);
+  return 0;
+}
 
 int rs_csr_matvec(int32_t nsys, int32_t n, const int32_t* row_ptr, const int32_t* col_idx,
                   const rs_complex* values, const rs_complex* x, rs_complex* y, void* stream) {
@@ -109,7 +116,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.capU = capU;
   a.pinv = pinv;
   a.state = state;
-  a.warps = nsys >= 148 ? 8 : 16;
+  a.warps = nsys >= 148 ? 8 : 32;
   RS_TRY(ilutp_plan(n, a.warps, &a.smem_mode, &a.bits_in_smem));
   const int nwords = (n + 31) / 32;
   const int64_t NW = N * a.warps;  // per-warp slices
@@ -141,6 +148,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.wlrow = reinterpret_cast<int32_t*>(ws + o_lrow);
   a.wukeep = ws + o_uk;
   a.wlkeep = ws + o_lk;
+  a.probe = g_factor_probe;
   // prow is scratch: a resumed launch rebuilds it as the inverse of pinv.
   const int rc = launch_ilutp(a, st);
   cudaFreeAsync(ws, st);

@@ -123,6 +123,13 @@ __device__ __forceinline__ void spmv(int n, const int32_t* __restrict__ rp,
 // sentinel half and is simply polled again.
 constexpr unsigned long long SENTINEL = 0x7ff4dead5eedbeefull;
 
+// Poll backoff of the triangular sweeps (ns): first / maximum nap after a
+// poll that made no progress.  Tunable through rs_debug_tri_backoff.
+__device__ unsigned g_tri_nap_min = 0;
+__device__ unsigned g_tri_nap_max = 0;
+// tuning hook: per-row (start, publish) clocks of a sweep, [2*n]
+__device__ long long* g_tri_times = nullptr;
+
 __device__ __forceinline__ double sentinel_d() { return __longlong_as_double(SENTINEL); }
 __device__ __forceinline__ double2 sentinel2() {
   return make_double2(sentinel_d(), sentinel_d());
@@ -134,7 +141,7 @@ __device__ __forceinline__ double2 vld2(const double2* p) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(p);
     asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
   } else {
-    asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   }
   return v;
 }
@@ -144,7 +151,7 @@ __device__ __forceinline__ void vst2(double2* p, double2 v) {
     asm volatile("st.volatile.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y)
                  : "memory");
   } else {
-    asm volatile("st.volatile.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y)
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y)
                  : "memory");
   }
 }
@@ -153,89 +160,267 @@ __device__ __forceinline__ bool is_ready(double2 v) {
          __double_as_longlong(v.y) != (long long)SENTINEL;
 }
 
-// One row of a triangular solve: acc = init - sum_e vals[e] * src[cols[e]]
-// over the row's entries in the given order (dir = +1 ascending storage,
-// -1 descending), each source polled until final.  Warp-cooperative: lanes
-// fetch 32 entries at a time and wait only on their own source; the ordered
-// subtraction chain (the reference rounding order) advances over the ready
-// prefix, so early terms are folded while late sources are still pending.
-__device__ __forceinline__ double2 tri_row(double2 acc, int p_first, int cnt_total, int dir,
-                                           const int32_t* __restrict__ ci,
-                                           const double2* __restrict__ v,
-                                           const double2* src) {
-  const int lane = threadIdx.x & 31;
-  for (int base = 0; base < cnt_total; base += 32) {
-    const int e = base + lane;
-    const bool act = e < cnt_total;
-    int c = 0;
-    double2 lv = make_double2(0.0, 0.0);
-    if (act) {
-      const int p = p_first + dir * e;
-      c = __ldg(ci + p);
-      lv = __ldg(v + p);
-    }
-    const int cnt = min(32, cnt_total - base);
-    bool have = !act;
-    double2 prod = make_double2(0.0, 0.0);
-    int done = 0;
-    while (done < cnt) {
-      if (!have) {
-        const double2 s = vld2(src + c);
-        if (is_ready(s)) {
-          prod = cmul_plain(lv, s);
-          have = true;
-        }
-      }
-      const unsigned m = __ballot_sync(FULL, have);
-      const unsigned pend = ~m;
-      int upto = pend ? (__ffs(pend) - 1) : 32;
-      if (upto > cnt) upto = cnt;
-      for (int q = done; q < upto; ++q) {
-        const double px = __shfl_sync(FULL, prod.x, q);
-        const double py = __shfl_sync(FULL, prod.y, q);
-        acc = csub(acc, make_double2(px, py));
-      }
-      done = upto;
+// Thread-per-row sparse triangular sweep in lock-step.  Thread t owns rows
+// t, t+T, t+2T, ... of the sweep order; each warp loops while any lane still
+// has work, and in every iteration a lane either consumes its next entry
+// (source final -> acc -= L * y_src, the reference's rounding order) or polls
+// again.  No lane ever blocks another lane of its warp, and the per-step
+// critical path is one 16-byte poll plus one complex multiply-subtract.
+// Row entries stream through two register groups of G: the group being
+// consumed and the next one, whose loads were issued G consumptions earlier
+// -- registers of an in-flight load are never touched on the hot path (a
+// read would stall the whole warp for a memory latency).  Deadlock-free: the
+// oldest unfinished row has all of its sources final and its lane polls it.
+template <int G>
+struct EntryGroup {
+  int c[G];
+  double2 l[G];
+};
+
+template <int G>
+__device__ __forceinline__ void load_group(EntryGroup<G>& g, const int32_t* __restrict__ ci,
+                                           const double2* __restrict__ v, int p, int step,
+                                           int avail) {
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    if (k < avail) {
+      g.c[k] = __ldg(ci + p + k * step);
+      g.l[k] = __ldg(v + p + k * step);
     }
   }
-  return acc;
 }
 
-// Unit-lower solve: out[r] = in[r] - sum_{c<r, ascending} L[r,c] out[c].
-// out must be pre-filled with the sentinel.  Rows are dealt round-robin to
-// warps in increasing order: the oldest unfinished row always has all its
-// sources final, so the sweep is deadlock-free.
-__device__ __noinline__ static void lower_solve(int n, const int32_t* __restrict__ rp,
-                                                const int32_t* __restrict__ ci,
-                                                const double2* __restrict__ v,
-                                                const double2* in, double2* out) {
+template <int G>
+__device__ __forceinline__ void pick(const EntryGroup<G>& g, int i, int& c, double2& l) {
+  c = g.c[0];
+  l = g.l[0];
+#pragma unroll
+  for (int k = 1; k < G; ++k)
+    if (i == k) {
+      c = g.c[k];
+      l = g.l[k];
+    }
+}
+
+template <bool UPPER>
+__device__ __forceinline__ void tri_sweep(int n, const int32_t* __restrict__ rp,
+                                          const int32_t* __restrict__ ci,
+                                          const double2* __restrict__ v,
+                                          const double2* __restrict__ rU, const double2* in,
+                                          double2* out) {
+  constexpr int G = 4;
+  const int T = blockDim.x;
+  const int step = UPPER ? -1 : 1;
+  for (int base = 0; base < n; base += T) {
+    const int q = base + threadIdx.x;
+    const bool act = q < n;
+    const int r = UPPER ? n - 1 - q : q;
+    int left = 0, pnext = 0;
+    double2 acc = make_double2(0.0, 0.0);
+    EntryGroup<G> A, B;
+    if (act) {
+      const int p0 = rp[r], p1 = rp[r + 1];
+      left = p1 - p0;
+      const int p = UPPER ? p1 - 1 : p0;
+      acc = in[r];
+      load_group<G>(A, ci, v, p, step, left);
+      load_group<G>(B, ci, v, p + G * step, step, left - G);
+      pnext = p + 2 * G * step;
+    }
+    int apos = 0;
+    bool pending = act;
+    while (__any_sync(FULL, pending)) {
+      if (pending) {
+        if (left > 0) {
+          int c;
+          double2 l;
+          pick<G>(A, apos, c, l);
+          const double2 s = vld2(out + c);
+          if (is_ready(s)) {
+            acc = csub(acc, cmul_plain(l, s));
+            --left;
+            if (++apos == G && left > 0) {
+              A = B;  // loaded G consumptions ago
+              apos = 0;
+              load_group<G>(B, ci, v, pnext, step, left - G);
+              pnext += G * step;
+            }
+          }
+        }
+        if (left == 0) {
+          vst2(out + r, UPPER ? cmul_plain(acc, __ldg(rU + r)) : acc);
+          pending = false;
+        }
+      }
+    }
+  }
+}
+
+// Warp-per-row variant (rows dealt round-robin to warps): lanes fetch 32
+// entries at a time, wait only on their own source, and the ordered
+// subtraction chain advances over the ready prefix.
+template <bool UPPER>
+__device__ __forceinline__ void tri_sweep_warp(int n, const int32_t* __restrict__ rp,
+                                               const int32_t* __restrict__ ci,
+                                               const double2* __restrict__ v,
+                                               const double2* __restrict__ rU,
+                                               const double2* in, double2* out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  for (int r = wid; r < n; r += nw) {
+  long long* const tt = g_tri_times;
+  for (int q = wid; q < n; q += nw) {
+    const int r = UPPER ? n - 1 - q : q;
+    if (tt && lane == 0) tt[2 * r] = clock64();
     const int p0 = rp[r], p1 = rp[r + 1];
-    const double2 acc = tri_row(in[r], p0, p1 - p0, 1, ci, v, out);
-    if (lane == 0) vst2(out + r, acc);
+    const int total = p1 - p0;
+    double2 acc = in[r];
+    for (int base = 0; base < total; base += 32) {
+      const int e = base + lane;
+      const bool act = e < total;
+      int c = 0;
+      double2 lv = make_double2(0.0, 0.0);
+      if (act) {
+        const int p = UPPER ? p1 - 1 - e : p0 + e;
+        c = __ldg(ci + p);
+        lv = __ldg(v + p);
+      }
+      const int cnt = min(32, total - base);
+      bool have = !act;
+      double2 prod = make_double2(0.0, 0.0);
+      int done = 0;
+      unsigned nap = 0;
+      while (done < cnt) {
+        if (!have) {
+          const double2 s = vld2(out + c);
+          if (is_ready(s)) {
+            prod = cmul_plain(lv, s);
+            have = true;
+          }
+        }
+        const unsigned m = __ballot_sync(FULL, have);
+        const unsigned pend = ~m;
+        int upto = pend ? (__ffs(pend) - 1) : 32;
+        if (upto > cnt) upto = cnt;
+        if (upto == done) {
+          // nothing new: back off so polling warps leave the issue slots to
+          // the warp on the critical path (the solve is latency-bound)
+          nap = nap ? min(nap * 2, g_tri_nap_max) : g_tri_nap_min;
+          if (nap) __nanosleep(nap);
+          continue;
+        }
+        nap = 0;
+        for (int k = done; k < upto; ++k) {
+          const double px = __shfl_sync(FULL, prod.x, k);
+          const double py = __shfl_sync(FULL, prod.y, k);
+          acc = csub(acc, make_double2(px, py));
+        }
+        done = upto;
+      }
+    }
+    if (lane == 0) {
+      vst2(out + r, UPPER ? cmul_plain(acc, __ldg(rU + r)) : acc);
+      if (tt) tt[2 * r + 1] = clock64();
+    }
     __syncwarp();
   }
 }
 
+// Warp-per-row with a lane-0 ordered fold.  For each chunk of up to 64
+// entries the warp loads (column, value) pairs coalesced, tries each source
+// once and stores the product of every source already final into a per-warp
+// shared buffer; then lane 0 alone folds the chunk in the reference order,
+// reading precomputed products and, for the entries that were not ready,
+// polling the source in a tight loop and multiplying itself.  The critical
+// hop (last source published -> this row published) is therefore one
+// shared-memory poll, one complex multiply-subtract and one 16-byte store.
+constexpr int FOLD_CHUNK = 64;
+
+struct FoldBuf {
+  int c[FOLD_CHUNK];
+  double2 l[FOLD_CHUNK];
+  double2 p[FOLD_CHUNK];
+  unsigned ok[FOLD_CHUNK / 32];
+};
+
+template <bool UPPER>
+__device__ __forceinline__ void tri_sweep_fold(int n, const int32_t* __restrict__ rp,
+                                               const int32_t* __restrict__ ci,
+                                               const double2* __restrict__ v,
+                                               const double2* __restrict__ rU,
+                                               const double2* in, double2* out,
+                                               FoldBuf* bufs) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  FoldBuf& B = bufs[wid];
+  for (int q = wid; q < n; q += nw) {
+    const int r = UPPER ? n - 1 - q : q;
+    const int p0 = rp[r], p1 = rp[r + 1];
+    const int total = p1 - p0;
+    double2 acc = in[r];
+    const double2 rr = UPPER ? __ldg(rU + r) : make_double2(0.0, 0.0);
+    for (int base = 0; base < total; base += FOLD_CHUNK) {
+      const int cnt = min(FOLD_CHUNK, total - base);
+#pragma unroll
+      for (int h = 0; h < FOLD_CHUNK / 32; ++h) {
+        const int e = h * 32 + lane;
+        bool ok = false;
+        if (e < cnt) {
+          const int p = UPPER ? p1 - 1 - (base + e) : p0 + base + e;
+          const int c = __ldg(ci + p);
+          const double2 lv = __ldg(v + p);
+          B.c[e] = c;
+          B.l[e] = lv;
+          const double2 s = vld2(out + c);
+          if (is_ready(s)) {
+            B.p[e] = cmul_plain(lv, s);
+            ok = true;
+          }
+        }
+        const unsigned m = __ballot_sync(FULL, ok);
+        if (lane == 0) B.ok[h] = m;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        for (int e = 0; e < cnt; ++e) {
+          double2 pe;
+          if ((B.ok[e >> 5] >> (e & 31)) & 1u) {
+            pe = B.p[e];
+          } else {
+            const int c = B.c[e];
+            double2 s;
+            do {
+              s = vld2(out + c);
+            } while (!is_ready(s));
+            pe = cmul_plain(B.l[e], s);
+          }
+          acc = csub(acc, pe);
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) vst2(out + r, UPPER ? cmul_plain(acc, rr) : acc);
+    __syncwarp();
+  }
+}
+
+// Unit-lower solve: out[r] = in[r] - sum_{c<r, ascending} L[r,c] out[c]
+// (reference lower_solve, _ckernels.pyx:53-67).  out pre-filled with the
+// sentinel.
+__device__ __noinline__ static void lower_solve(int n, const int32_t* __restrict__ rp,
+                                                const int32_t* __restrict__ ci,
+                                                const double2* __restrict__ v,
+                                                const double2* in, double2* out) {
+  tri_sweep_warp<false>(n, rp, ci, v, nullptr, in, out);
+}
+
 // Upper solve: out[r] = (in[r] - sum_{c>r, descending} U[r,c] out[c]) *
-// recipc(U_rr) -- the reference's descending-column scatter order
-// (upper_solve, _ckernels.pyx:70-85).  Rows in decreasing order.
+// recipc(U_rr) (reference upper_solve, _ckernels.pyx:70-85).
 __device__ __noinline__ static void upper_solve(int n, const int32_t* __restrict__ rp,
                                                 const int32_t* __restrict__ ci,
                                                 const double2* __restrict__ v,
                                                 const double2* __restrict__ rU,
                                                 const double2* in, double2* out) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  for (int q = wid; q < n; q += nw) {
-    const int r = n - 1 - q;
-    const int p0 = rp[r], p1 = rp[r + 1];
-    const double2 acc = tri_row(in[r], p1 - 1, p1 - p0, -1, ci, v, out);
-    if (lane == 0) vst2(out + r, cmul_plain(acc, __ldg(rU + r)));
-    __syncwarp();
-  }
+  tri_sweep_warp<true>(n, rp, ci, v, rU, in, out);
 }
 
 }  // namespace cta

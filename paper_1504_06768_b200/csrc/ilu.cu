@@ -68,6 +68,10 @@ __device__ __forceinline__ void vstore(int32_t* p, int v) {
   *reinterpret_cast<volatile int32_t*>(p) = v;
 }
 
+__device__ __forceinline__ void probe_mark(unsigned long long* pr, int k, int slot, int lane) {
+  if (pr && lane == 0) pr[(size_t)k * 6 + slot] = clock64();
+}
+
 }  // namespace
 
 // shared-memory bytes per CTA: pinv, prow, Lp (when shared_in_smem) + the
@@ -170,6 +174,8 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
     __syncwarp();
     if (ctl[1]) break;
     __threadfence_block();
+    unsigned long long* const pr = (b == 0) ? a.probe : nullptr;
+    probe_mark(pr, k, 0, lane);
     // ---- 1. scatter column j; seed pending with columns already finished --
     const int32_t c0 = Ap[j], c1 = Ap[j + 1];
     int npat = c1 - c0;
@@ -192,6 +198,11 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
     int unum = 0;
     int w = (lowc == 0x7fffffff) ? ((scanned + 31) >> 5) : (lowc >> 5);
     bool aborted = false;
+    // first chunk of the next pending column, fetched while the current one
+    // is applied (L columns are immutable once published)
+    int pre_c = -1, pre_i = 0;
+    double2 pre_v = make_double2(0.0, 0.0);
+    uint32_t cur_word = 0;
     while (true) {
       const int wend = (scanned + 31) >> 5;
       int c = -1;
@@ -204,6 +215,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
           const uint32_t word = __shfl_sync(FULL, bv, src);
           w += src;
           c = (w << 5) + __ffs(word) - 1;
+          cur_word = word;
           break;
         }
         w += 32;
@@ -212,7 +224,13 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
         if (scanned == k) break;
         // advance the frontier over newly finished columns
         int d;
+        // the warp owning the next column to finish spins hot; the others
+        // back off so they do not steal issue slots from the critical tail
+        // nap length grows with the distance to this column's turn
+        const int dist = k - scanned - 1;
+        const unsigned nap = dist <= 0 ? 0u : (dist < 4 ? 64u * dist : 512u);
         while ((d = ctl[0]) == scanned && !ctl[1]) {
+          if (nap) __nanosleep(nap);
         }
         if (ctl[1]) {
           aborted = true;
@@ -236,6 +254,22 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       const int pr = vload(prow + c);
       const double2 xc = x[pr];
       const int32_t p0 = vload(Lp + c) + 1, p1 = vload(Lp + c + 1);
+      const bool use_pre = (pre_c == c);
+      const int my_pre_i = pre_i;
+      const double2 my_pre_v = pre_v;
+      {  // prefetch the next pending column below the frontier (same word)
+        const uint32_t rest = cur_word & ~((2u << (c & 31)) - 1u);
+        pre_c = -1;
+        if (rest) {
+          const int cn = (w << 5) + __ffs(rest) - 1;
+          const int q0 = vload(Lp + cn) + 1 + lane, q1 = vload(Lp + cn + 1);
+          pre_c = cn;
+          if (q0 < q1) {
+            pre_i = Li[q0];
+            pre_v = Lx[q0];
+          }
+        }
+      }
       __syncwarp();
       if (lane == 0) {
         atomicAnd(&bits[w], ~(1u << (c & 31)));
@@ -250,8 +284,13 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
         double2 lv = make_double2(0.0, 0.0);
         bool isnew = false;
         if (act) {
-          i = Li[p];
-          lv = Lx[p];
+          if (use_pre && base == p0) {
+            i = my_pre_i;
+            lv = my_pre_v;
+          } else {
+            i = Li[p];
+            lv = Lx[p];
+          }
           isnew = flag[i] != k;
         }
         const unsigned nm = __ballot_sync(FULL, isnew);
@@ -274,6 +313,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
     }
     if (aborted) break;
     __threadfence_block();  // acquire: every column < k is final
+    probe_mark(pr, k, 1, lane);
 
     // ---- 3. pivot: max |re|+|im| over non-pivotal rows, ties -> lowest row -
     double best = -1.0;
@@ -313,6 +353,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
     }
     const double2 piv = x[ipiv];
     __syncwarp();
+    probe_mark(pr, k, 2, lane);
 
     // ---- 4. dropping ------------------------------------------------------
     int kept_u = 0, kept_l = 0;
@@ -394,6 +435,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       __syncwarp();
     }
 
+    probe_mark(pr, k, 3, lane);
     // ---- 6. emit U (kept rows ascending, pivot last), L (unit first) ------
     const int32_t lnnz = vload(Lp + k);
     const int32_t unnz = vload(gUp + k);
@@ -452,6 +494,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       __threadfence_block();  // release column k
       ctl[0] = k + 1;
     }
+    probe_mark(pr, k, 4, lane);
     __syncwarp();
   }
   __syncthreads();

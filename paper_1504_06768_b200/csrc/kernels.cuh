@@ -56,6 +56,7 @@ struct FactorArgs {
   int smem_mode;     // 1: pinv / prow / Lp shadow live in shared memory
   int bits_in_smem;  // 1: per-warp pending bitmaps in shared memory
   int warps;         // warps (columns in flight) per system
+  unsigned long long* probe;  // optional per-column phase clocks [n*6] (tuning)
 };
 // state[3b+0] codes
 enum { FAC_RUNNING = 0, FAC_DONE = 1, FAC_ZERO_PIVOT = 2, FAC_OVERFLOW = 3 };

@@ -657,3 +657,59 @@ int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
 }
 
 }  // namespace rs
+
+namespace rs {
+
+// Debug / tuning: time one triangular sweep variant in isolation.
+// which: 0 = lower, 1 = upper; variant: 0 = thread-per-row, 1 = warp-per-row.
+__global__ void __launch_bounds__(1024) tri_probe_kernel(int n, const int32_t* rp,
+                                                         const int32_t* ci, const double2* v,
+                                                         const double2* rU, const double2* in,
+                                                         double2* gout, int which, int variant,
+                                                         int smem_buf) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  cta::FoldBuf* fb = reinterpret_cast<cta::FoldBuf*>(smem);
+  double2* out = smem_buf ? reinterpret_cast<double2*>(smem + sizeof(cta::FoldBuf) * 32) : gout;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = cta::sentinel2();
+  __syncthreads();
+  if (which == 0) {
+    if (variant == 0) cta::tri_sweep<false>(n, rp, ci, v, rU, in, out);
+    else if (variant == 1) cta::tri_sweep_warp<false>(n, rp, ci, v, rU, in, out);
+    else cta::tri_sweep_fold<false>(n, rp, ci, v, rU, in, out, fb);
+  } else {
+    if (variant == 0) cta::tri_sweep<true>(n, rp, ci, v, rU, in, out);
+    else if (variant == 1) cta::tri_sweep_warp<true>(n, rp, ci, v, rU, in, out);
+    else cta::tri_sweep_fold<true>(n, rp, ci, v, rU, in, out, fb);
+  }
+  __syncthreads();
+  if (smem_buf)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) gout[i] = out[i];
+}
+
+}  // namespace rs
+
+extern "C" int rs_debug_tri_probe(int n, const int32_t* rp, const int32_t* ci, const void* v,
+                                  const void* rU, const void* in, void* out, int which,
+                                  int variant, int smem_buf, int threads, void* stream) {
+  const size_t smem = (smem_buf ? 16 * (size_t)n : 0) + sizeof(rs::cta::FoldBuf) * 32;
+  RS_CUDA_TRY(cudaFuncSetAttribute(rs::tri_probe_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  rs::tri_probe_kernel<<<1, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      n, rp, ci, reinterpret_cast<const double2*>(v), reinterpret_cast<const double2*>(rU),
+      reinterpret_cast<const double2*>(in), reinterpret_cast<double2*>(out), which, variant,
+      smem_buf);
+  RS_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+extern "C" int rs_debug_tri_backoff(unsigned nap_min, unsigned nap_max) {
+  RS_CUDA_TRY(cudaMemcpyToSymbol(rs::cta::g_tri_nap_min, &nap_min, sizeof(unsigned)));
+  RS_CUDA_TRY(cudaMemcpyToSymbol(rs::cta::g_tri_nap_max, &nap_max, sizeof(unsigned)));
+  return 0;
+}
+
+extern "C" int rs_debug_tri_times(void* buf) {
+  long long* p = reinterpret_cast<long long*>(buf);
+  RS_CUDA_TRY(cudaMemcpyToSymbol(rs::cta::g_tri_times, &p, sizeof(p)));
+  return 0;
+}

@@ -3,7 +3,7 @@
 Drop-in for the reference factor module (pkg/src/rhosolve/factor.py):
 `lu`, `ilutp`, `solve_lu`, `condest`, `LUFactors`, `SingularMatrixError`,
 `PreconditionerBreakdownError`, same argument checks and messages.  The
-factorization itself is the warp-per-system kernel in csrc/ilu.cu, the apply
+factorization itself is the column-pipelined kernel in csrc/ilu.cu, the apply
 the row-oriented triangular solves in csrc/cta_ops.cuh; both are
 bit-identical to the reference kernels.
 """
@@ -101,7 +101,7 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
                   _lib.stream_ptr())
     maxnnz = int(nnz_rows.max())
     per_col = max(cap - 1, 1) if cap >= 0 else None
-    guess = max(8 * maxnnz, 2 * n, 16)
+    guess = max(24 * maxnnz, 2 * n, 16)
     capL = capU = min(n * per_col, guess) if per_col else guess
     if capacity is not None:  # tests: force the overflow/resume path
         capL = capU = max(int(capacity), n)
