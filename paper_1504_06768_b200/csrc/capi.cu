@@ -67,6 +67,22 @@ using namespace rs;
 extern "C" {
 
 int rs_abi_version(void) { return RS_ABI_VERSION; }
+
+// Keep freed stream-ordered allocations in the device pool instead of
+// returning them to the OS at every synchronisation: the solve path
+// allocates and frees its scratch every call.
+static int keep_pool_memory() {
+  static int done = 0;
+  if (done) return RS_OK;
+  int dev;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  RS_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+  unsigned long long thr = ~0ull;
+  RS_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done = 1;
+  return RS_OK;
+}
 const char* rs_last_error(void) { return g_err; }
 long long rs_launch_count(void) { return g_launches.load(); }
 // Tuning hook (not part of the documented ABI): when set, the next
@@ -89,6 +105,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
                  const double* row_norms, int32_t* Lp, int32_t* Li, rs_complex* Lx,
                  int64_t capL, int32_t* Up, int32_t* Ui, rs_complex* Ux, int64_t capU,
                  int32_t* pinv, int32_t* state, void* stream) {
+  RS_TRY(keep_pool_memory());
   RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
   RS_CHECK_ARG(drop_tol >= 0.0, "drop tolerance must be >= 0");
   RS_CHECK_ARG(!(drop_tol > 0.0) || row_norms, "row_norms required when drop_tol > 0");
@@ -160,6 +177,7 @@ int rs_factor_rows(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li
                    const rs_complex* Ux, int64_t capU, int32_t* L_rp, int32_t* L_ci,
                    rs_complex* L_v, int64_t* L_nnz, int32_t* U_rp, int32_t* U_ci,
                    rs_complex* U_v, rs_complex* rdiag, int64_t* U_nnz, void* stream) {
+  RS_TRY(keep_pool_memory());
   RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
   cudaStream_t st = S(stream);
   RS_TRY(factor_to_csr(nsys, n, Lp, Li, C2(Lx), capL, 1, L_rp, L_ci, M2(L_v), nullptr, L_nnz,
@@ -206,6 +224,7 @@ int rs_liouvillian(int32_t D, const int32_t* H_rp, const int32_t* H_ci, const rs
                    const int32_t* const* C_ci, const rs_complex* const* C_v,
                    const int64_t* C_nnz, double* herm_dev, int32_t* out_rp, int32_t* out_ci,
                    rs_complex* out_v, int64_t* nnz, void* stream) {
+  RS_TRY(keep_pool_memory());
   RS_CHECK_ARG(D >= 1, "hilbert dimension must be >= 1");
   RS_CHECK_ARG(K >= 0, "negative collapse operator count");
   RS_CHECK_ARG((int64_t)D * D < ((int64_t)1 << 31), "D*D exceeds int32 indexing");
@@ -236,6 +255,7 @@ int rs_trace_modify(int32_t nsys, int32_t n, int32_t D, const int32_t* rp, const
 
 int rs_rcm(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, int32_t* forward,
            int32_t* inverse, void* stream) {
+  RS_TRY(keep_pool_memory());
   RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
   if (!nsys || !n) return RS_OK;
   return rcm_order(nsys, n, rp, ci, forward, inverse, S(stream));
@@ -268,6 +288,7 @@ int rs_row_norms(int32_t nsys, int32_t n, const int32_t* rp, const rs_complex* v
 }
 
 int rs_steady_solve(const rs_solver_args* p, void* stream) {
+  RS_TRY(keep_pool_memory());
   RS_CHECK_ARG(p != nullptr, "null args");
   RS_CHECK_ARG(p->n >= 0 && p->nsys >= 0, "negative size");
   RS_CHECK_ARG(p->mode >= RS_INV_DIRECT && p->mode <= RS_LIN_GMRES, "unknown mode");
@@ -322,6 +343,7 @@ int rs_steady_solve(const rs_solver_args* p, void* stream) {
 int rs_postprocess(int32_t nsys, int32_t D, const rs_complex* x, const int32_t* forward,
                    const int32_t* plain_rp, const int32_t* plain_ci, const rs_complex* plain_v,
                    rs_complex* rho, double* residual, rs_complex* trace, void* stream) {
+  RS_TRY(keep_pool_memory());
   RS_CHECK_ARG(nsys >= 0 && D >= 1, "bad size");
   if (!nsys) return RS_OK;
   return postprocess(nsys, D, C2(x), forward, plain_rp, plain_ci, C2(plain_v), M2(rho),

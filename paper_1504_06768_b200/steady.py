@@ -17,6 +17,7 @@ config-4 parameter sweep) as one block-diagonal batch: one CTA per system.
 from __future__ import annotations
 
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -81,6 +82,13 @@ def start_vector(n, seed):
     """steady.py:171-174 (host PCG64 draw, normalised on the device later)."""
     rng = np.random.default_rng(seed)
     return rng.standard_normal(n) + 1j * rng.standard_normal(n)
+
+
+_POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="rhosolve-rng")
+
+
+def _start_vectors(n, seeds):
+    return np.concatenate([start_vector(n, s) for s in seeds])
 
 
 def _require_plain(L):
@@ -221,6 +229,9 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
         raise ValueError(f"unknown solver {solver!r}")
     _check_ops(None, max_iter, restart_m)
     t0 = _sync()
+    # the seeded start vectors (numpy PCG64, drawn exactly as steady.py:171-174)
+    # are generated on a host thread while the GPU orders and factors
+    x0_future = _POOL.submit(_start_vectors, L.n, list(seeds))
     shifted = liouville.shift(L, sigma)
     mat, _, plain, fwd, label = _prepare(shifted, ordering_name, plain=L.matrix)
     if plain is None:
@@ -237,9 +248,7 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
         f = factor.factor_batch(mat, float(d), float(p), raise_on_fail=raise_errors)
         mode = _lib.INV_GMRES if solver == "gmres" else _lib.INV_BICGSTAB
     t2 = _sync()
-    n, B = mat.n, mat.nsys
-    x0 = np.concatenate([start_vector(n, s) for s in seeds])
-    x0 = torch.from_numpy(x0).to(mat.values.device)
+    x0 = torch.from_numpy(x0_future.result()).to(mat.values.device)
     if f.L_rp is None:  # some system of the batch failed to factor
         return None, f, None, None, label, (t0, t1, t2, _sync())
     x, st = _solve(mode, mat, plain, f, x0, tol, max_iter, restart_m, inner == "iterative",
