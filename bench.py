@@ -291,7 +291,7 @@ def kernel_timings(L, skw, torch, seeds):
     def run_fact():
         state.zero_()
         _lib.call("rs_factorize", B, n, _lib.ptr(Ap), _lib.ptr(Ai), _lib.ptr(Ax), None,
-                  float(d), cap, _lib.ptr(rn), _lib.ptr(Lp), _lib.ptr(Li), _lib.ptr(Lx),
+                  float(d), cap, None, _lib.ptr(rn), _lib.ptr(Lp), _lib.ptr(Li), _lib.ptr(Lx),
                   f.capL, _lib.ptr(Up), _lib.ptr(Ui), _lib.ptr(Ux), f.capU, _lib.ptr(pinv),
                   _lib.ptr(state), _lib.stream_ptr())
 

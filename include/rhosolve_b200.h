@@ -69,7 +69,9 @@ int rs_csr_matvec(int32_t nsys, int32_t n, const int32_t* row_ptr,
 /* Left-looking LU / ILUTP.  Replaces factorize (_ckernels.pyx:144-385) as
  * called by factor._factor (factor.py:70-112).
  *   A is given column-major: Ap/Ai/Ax = CSR of A^T (sparse.transpose(a)),
- *   q (nullable) = elimination column order, drop_tol, fill_cap (-1 = none),
+ *   q (nullable) = elimination column order, drop_tol, fill_cap (-1 = none)
+ *   or fill_caps (nullable device int32[nsys], one cap per system: batches
+ *   whose systems differ in nnz, e.g. block-Jacobi blocks),
  *   row_norms (nullable unless drop_tol > 0) = max |re|+|im| per row.
  * Outputs per system b (raw CSC exactly as the reference returns them):
  *   Lp/Up [nsys*(n+1)], Li/Lx at b*capL, Ui/Ux at b*capU, pinv [nsys*n].
@@ -81,7 +83,8 @@ int rs_csr_matvec(int32_t nsys, int32_t n, const int32_t* row_ptr,
  * reference. */
 int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
                  const rs_complex* Ax, const int32_t* q, double drop_tol,
-                 int32_t fill_cap, const double* row_norms, int32_t* Lp,
+                 int32_t fill_cap, const int32_t* fill_caps, const double* row_norms,
+                 int32_t* Lp,
                  int32_t* Li, rs_complex* Lx, int64_t capL, int32_t* Up,
                  int32_t* Ui, rs_complex* Ux, int64_t capU, int32_t* pinv,
                  int32_t* state, void* stream);
@@ -240,6 +243,31 @@ int rs_postprocess(int32_t nsys, int32_t D, const rs_complex* x,
                    const int32_t* plain_ci, const rs_complex* plain_v,
                    rs_complex* rho, double* residual, rs_complex* trace,
                    void* stream);
+
+/* ---- grid-wide vector operations (large-system / sharded path) ---------- */
+
+/* out[2k], out[2k+1] = re, im of vdot(xs[k], ys[k]) = sum conj(x) y, k < npairs
+ * (<= 4); xs/ys are HOST arrays of device pointers; out is device.
+ * Deterministic: fixed grid, fixed reduction order (krylov.py np.vdot /
+ * np.linalg.norm**2 up to summation order). */
+int rs_vdots(int64_t n, int32_t npairs, const rs_complex* const* xs,
+             const rs_complex* const* ys, double* out, void* stream);
+
+/* out[0] = max_i |x_i| (steady.py:532 np.max(np.abs(.))); out is device. */
+int rs_amax(int64_t n, const rs_complex* x, double* out, void* stream);
+
+/* out = sum_{k < nv} (coef_re[k] + i coef_im[k]) * vs[k], nv <= 4; vs, coef_*
+ * are HOST arrays; out may alias an input (the BiCGStab updates). */
+int rs_lincomb(int64_t n, int32_t nv, const rs_complex* const* vs, const double* coef_re,
+               const double* coef_im, rs_complex* out, void* stream);
+
+/* Block-Jacobi blocks: rows [g*block, (g+1)*block) of an nrows-row CSR whose
+ * column indices are offset by col0, keeping entries whose (col - col0) lies
+ * in the same block, as a block-diagonal batch with local indices.  Two
+ * passes (out_ci == NULL: row pointers + *nnz). */
+int rs_block_extract(int64_t nrows, int32_t block, int32_t col0, const int32_t* rp,
+                     const int32_t* ci, const rs_complex* v, int32_t* out_rp,
+                     int32_t* out_ci, rs_complex* out_v, int64_t* nnz, void* stream);
 
 #ifdef __cplusplus
 }

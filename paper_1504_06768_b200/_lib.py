@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librhosolve_b200.so")
+LIB_PATH = os.environ.get("RHOSOLVE_B200_LIB") or os.path.join(_HERE, "_lib",
+                                                               "librhosolve_b200.so")
 
 # status codes (include/rhosolve_b200.h)
 RS_OK = 0
@@ -65,7 +66,7 @@ class SolverArgs(ctypes.Structure):
 _SIGS = {
     "rs_abi_version": [],
     "rs_csr_matvec": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
-    "rs_factorize": [_i32, _i32, _vp, _vp, _vp, _vp, _f64, _i32, _vp, _vp, _vp, _vp,
+    "rs_factorize": [_i32, _i32, _vp, _vp, _vp, _vp, _f64, _i32, _vp, _vp, _vp, _vp, _vp,
                      _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "rs_factor_rows": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64,
                        _vp, _vp, _vp, ctypes.POINTER(_i64), _vp, _vp, _vp, _vp,
@@ -84,6 +85,11 @@ _SIGS = {
     "rs_row_norms": [_i32, _i32, _vp, _vp, _vp, _vp],
     "rs_steady_solve": [ctypes.POINTER(SolverArgs), _vp],
     "rs_postprocess": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "rs_vdots": [_i64, _i32, _vp, _vp, _vp, _vp],
+    "rs_amax": [_i64, _vp, _vp, _vp],
+    "rs_lincomb": [_i64, _i32, _vp, _vp, _vp, _vp, _vp],
+    "rs_block_extract": [_i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.POINTER(_i64),
+                         _vp],
 }
 
 EXPORTED = tuple(_SIGS) + ("rs_last_error", "rs_launch_count")

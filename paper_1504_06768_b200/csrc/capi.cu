@@ -2,6 +2,7 @@
 // argument validation + dispatch to the launchers; no compute on the host and
 // no fallback path.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <atomic>
 #include <stdio.h>
 #include <string.h>
@@ -55,6 +56,14 @@ int postprocess(int B, int32_t D, const double2* x, const int32_t* fwd, const in
                 double2* trace_out, cudaStream_t st);
 int permute_vector(int B, int32_t n, const double2* x, const int32_t* fwd, double2* out,
                    int gather, cudaStream_t st);
+int vec_vdots(int64_t n, int np, const double2* const* xs, const double2* const* ys, double* out,
+              double* scratch, cudaStream_t st);
+int vec_amax(int64_t n, const double2* x, double* out, double* scratch, cudaStream_t st);
+int vec_lincomb(int64_t n, int nv, const double2* const* vs, const double* coef_re,
+                const double* coef_im, double2* out, cudaStream_t st);
+int block_extract(int64_t nrows, int32_t m, int32_t col0, const int32_t* rp, const int32_t* ci,
+                  const double2* v, int32_t* out_rp, int32_t* out_ci, double2* out_v,
+                  int64_t* nnz_out, cudaStream_t st);
 
 }  // namespace rs
 
@@ -102,7 +111,7 @@ int rs_csr_matvec(int32_t nsys, int32_t n, const int32_t* row_ptr, const int32_t
 
 int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
                  const rs_complex* Ax, const int32_t* q, double drop_tol, int32_t fill_cap,
-                 const double* row_norms, int32_t* Lp, int32_t* Li, rs_complex* Lx,
+                 const int32_t* fill_caps, const double* row_norms, int32_t* Lp, int32_t* Li, rs_complex* Lx,
                  int64_t capL, int32_t* Up, int32_t* Ui, rs_complex* Ux, int64_t capU,
                  int32_t* pinv, int32_t* state, void* stream) {
   RS_TRY(keep_pool_memory());
@@ -123,6 +132,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.rn = row_norms;
   a.drop_tol = drop_tol;
   a.fill_cap = fill_cap;
+  a.fill_caps = fill_caps;
   a.Lp = Lp;
   a.Li = Li;
   a.Lx = M2(Lx);
@@ -134,6 +144,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.pinv = pinv;
   a.state = state;
   a.warps = nsys >= 148 ? 8 : 32;
+  if (const char* e = getenv("RHOSOLVE_ILU_WARPS")) a.warps = atoi(e);  // tuning knob
   RS_TRY(ilutp_plan(n, a.warps, &a.smem_mode, &a.bits_in_smem));
   const int nwords = (n + 31) / 32;
   const int64_t NW = N * a.warps;  // per-warp slices
@@ -153,6 +164,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   const size_t o_lrow = take(4 * NW);
   const size_t o_uk = take(NW);
   const size_t o_lk = take(NW);
+  const size_t o_key = take(8 * NW);
   unsigned char* ws = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&ws, bytes, st));
   a.wx = reinterpret_cast<double2*>(ws + o_x);
@@ -165,6 +177,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.wlrow = reinterpret_cast<int32_t*>(ws + o_lrow);
   a.wukeep = ws + o_uk;
   a.wlkeep = ws + o_lk;
+  a.wkey = reinterpret_cast<uint64_t*>(ws + o_key);
   a.probe = g_factor_probe;
   // prow is scratch: a resumed launch rebuilds it as the inverse of pinv.
   const int rc = launch_ilutp(a, st);
@@ -348,6 +361,43 @@ int rs_postprocess(int32_t nsys, int32_t D, const rs_complex* x, const int32_t* 
   if (!nsys) return RS_OK;
   return postprocess(nsys, D, C2(x), forward, plain_rp, plain_ci, C2(plain_v), M2(rho),
                      residual, M2(trace), S(stream));
+}
+
+int rs_vdots(int64_t n, int32_t npairs, const rs_complex* const* xs, const rs_complex* const* ys,
+             double* out, void* stream) {
+  RS_CHECK_ARG(n >= 0, "negative length");
+  cudaStream_t st = S(stream);
+  double* scratch = nullptr;
+  RS_CUDA_TRY(cudaMallocAsync(&scratch, sizeof(double) * 592 * 8, st));
+  const int rc = vec_vdots(n, npairs, reinterpret_cast<const double2* const*>(xs),
+                           reinterpret_cast<const double2* const*>(ys), out, scratch, st);
+  cudaFreeAsync(scratch, st);
+  return rc;
+}
+
+int rs_amax(int64_t n, const rs_complex* x, double* out, void* stream) {
+  RS_CHECK_ARG(n >= 0, "negative length");
+  cudaStream_t st = S(stream);
+  double* scratch = nullptr;
+  RS_CUDA_TRY(cudaMallocAsync(&scratch, sizeof(double) * 592, st));
+  const int rc = vec_amax(n, C2(x), out, scratch, st);
+  cudaFreeAsync(scratch, st);
+  return rc;
+}
+
+int rs_lincomb(int64_t n, int32_t nv, const rs_complex* const* vs, const double* coef_re,
+               const double* coef_im, rs_complex* out, void* stream) {
+  RS_CHECK_ARG(n >= 0, "negative length");
+  return vec_lincomb(n, nv, reinterpret_cast<const double2* const*>(vs), coef_re, coef_im, M2(out),
+                     S(stream));
+}
+
+int rs_block_extract(int64_t nrows, int32_t block, int32_t col0, const int32_t* rp,
+                     const int32_t* ci, const rs_complex* v, int32_t* out_rp, int32_t* out_ci,
+                     rs_complex* out_v, int64_t* nnz, void* stream) {
+  RS_CHECK_ARG(block >= 1, "block size must be >= 1");
+  return block_extract(nrows, block, col0, rp, ci, C2(v), out_rp, out_ci, M2(out_v), nnz,
+                       S(stream));
 }
 
 }  // extern "C"

@@ -38,6 +38,9 @@
 // column k, records it, and the host grows the buffers and resumes.
 #include "common.cuh"
 #include "kernels.cuh"
+#ifndef RS_FENCE
+#define RS_FENCE() __threadfence_block()
+#endif
 
 namespace rs {
 
@@ -79,7 +82,7 @@ __device__ __forceinline__ void probe_mark(unsigned long long* pr, int k, int sl
 __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_smem,
                                             int bits_in_smem) {
   const size_t nwords = ((size_t)n + 31) / 32;
-  size_t b = 64;
+  size_t b = 64 + 1024 * (size_t)warps;  // control words + per-warp cap histograms
   if (shared_in_smem) b += 4 * ((size_t)n * 2 + (size_t)n + 1);
   if (bits_in_smem) b += 4 * nwords * (size_t)warps;
   return (b + 15) & ~(size_t)15;
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
 
   // control words: ctl[0] = number of finished columns, ctl[1] = abort
   volatile int32_t* ctl = reinterpret_cast<volatile int32_t*>(smem);
-  unsigned char* sp = smem + 64;
+  unsigned char* sp = smem + 64 + 1024 * (size_t)W;  // after the per-warp cap histograms
   int32_t *pinv, *prow, *Lp;
   if (a.smem_mode) {
     pinv = reinterpret_cast<int32_t*>(sp);
@@ -138,6 +141,8 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
   int32_t* lrow = a.wlrow + ws;
   uint8_t* ukeep = a.wukeep + ws;
   uint8_t* lkeep = a.wlkeep + ws;
+  uint64_t* keys = a.wkey + ws;
+  unsigned* hist = reinterpret_cast<unsigned*>(smem + 64) + 256 * wid;
 
   // ---- init -----------------------------------------------------------------
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -163,9 +168,10 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       Lp[0] = 0;
     }
   }
-  __threadfence_block();
+  RS_FENCE();
   __syncthreads();
-  const bool have_cap = a.fill_cap >= 0;
+  const int fill_cap = a.fill_caps ? a.fill_caps[b] : a.fill_cap;
+  const bool have_cap = fill_cap >= 0;
 
   // round-robin columns, starting at the resume point
   for (int k = k0 + wid; k < n; k += W) {
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
     int scanned = ctl[0];
     __syncwarp();
     if (ctl[1]) break;
-    __threadfence_block();
+    RS_FENCE();
     unsigned long long* const pr = (b == 0) ? a.probe : nullptr;
     probe_mark(pr, k, 0, lane);
     // ---- 1. scatter column j; seed pending with columns already finished --
@@ -196,6 +202,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
 
     // ---- 2. updates in ascending pivotal order, gated by the frontier -----
     int unum = 0;
+    int kept_u = 0;
     int w = (lowc == 0x7fffffff) ? ((scanned + 31) >> 5) : (lowc >> 5);
     bool aborted = false;
     // first chunk of the next pending column, fetched while the current one
@@ -236,7 +243,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
           aborted = true;
           break;
         }
-        __threadfence_block();
+        RS_FENCE();
         int newlow = 0x7fffffff;
         for (int m = scanned + lane; m < d; m += 32) {
           const int r = vload(prow + m);
@@ -253,6 +260,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       }
       const int pr = vload(prow + c);
       const double2 xc = x[pr];
+      const double rnc = (drop > 0.0) ? rn[pr] : 0.0;
       const int32_t p0 = vload(Lp + c) + 1, p1 = vload(Lp + c + 1);
       const bool use_pre = (pre_c == c);
       const int my_pre_i = pre_i;
@@ -270,80 +278,122 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
           }
         }
       }
+      // U entry for c: its value is final now, so its drop test is decided
+      // here instead of on the column's critical tail
+      const bool ukk = !(drop > 0.0 && cabs1(xc) < drop * rnc);
       __syncwarp();
       if (lane == 0) {
         atomicAnd(&bits[w], ~(1u << (c & 31)));
         urow[unum] = c;
         uval[unum] = xc;
+        ukeep[unum] = ukk;
       }
       ++unum;
-      for (int base = p0; base < p1; base += 32) {
-        const int p = base + lane;
-        const bool act = p < p1;
-        int i = 0;
-        double2 lv = make_double2(0.0, 0.0);
-        bool isnew = false;
-        if (act) {
+      kept_u += ukk;
+      // apply L[:,c] in blocks of 64 entries: all loads of a block are issued
+      // before any is consumed (one memory latency per block, not per entry)
+      for (int base = p0; base < p1; base += 64) {
+        const int pa = base + lane, pb = pa + 32;
+        const bool acta = pa < p1, actb = pb < p1;
+        int ia = 0, ib = 0;
+        double2 la = make_double2(0.0, 0.0), lb = la;
+        if (acta) {
           if (use_pre && base == p0) {
-            i = my_pre_i;
-            lv = my_pre_v;
+            ia = my_pre_i;
+            la = my_pre_v;
           } else {
-            i = Li[p];
-            lv = Lx[p];
+            ia = Li[pa];
+            la = Lx[pa];
           }
-          isnew = flag[i] != k;
         }
-        const unsigned nm = __ballot_sync(FULL, isnew);
-        if (act) {
-          double2 xi;
-          if (isnew) {
-            flag[i] = k;
-            xi = make_double2(0.0, 0.0);
-            pat[npat + __popc(nm & lanemask_lt())] = i;
-            const int pv = vload(pinv + i);
-            if (pv >= 0 && pv < scanned) atomicOr(&bits[pv >> 5], 1u << (pv & 31));
-          } else {
-            xi = x[i];
-          }
-          x[i] = csub(xi, cmul_plain(lv, xc));
+        if (actb) {
+          ib = Li[pb];
+          lb = Lx[pb];
         }
-        npat += __popc(nm);
+        const int fa = acta ? flag[ia] : k, fb = actb ? flag[ib] : k;
+        double2 xa = acta ? x[ia] : la, xb = actb ? x[ib] : lb;
+        const int va = acta ? vload(pinv + ia) : -1, vb = actb ? vload(pinv + ib) : -1;
+        const bool newa = acta && fa != k, newb = actb && fb != k;
+        const unsigned ma = __ballot_sync(FULL, newa);
+        const unsigned mb = __ballot_sync(FULL, newb);
+        const unsigned lt = lanemask_lt();
+        if (newa) {
+          flag[ia] = k;
+          xa = make_double2(0.0, 0.0);
+          pat[npat + __popc(ma & lt)] = ia;
+          if (va >= 0 && va < scanned) atomicOr(&bits[va >> 5], 1u << (va & 31));
+        }
+        npat += __popc(ma);
+        if (newb) {
+          flag[ib] = k;
+          xb = make_double2(0.0, 0.0);
+          pat[npat + __popc(mb & lt)] = ib;
+          if (vb >= 0 && vb < scanned) atomicOr(&bits[vb >> 5], 1u << (vb & 31));
+        }
+        npat += __popc(mb);
+        if (acta) x[ia] = csub(xa, cmul_plain(la, xc));
+        if (actb) x[ib] = csub(xb, cmul_plain(lb, xc));
       }
       __syncwarp();
     }
     if (aborted) break;
-    __threadfence_block();  // acquire: every column < k is final
+    RS_FENCE();  // acquire: every column < k is final
     probe_mark(pr, k, 1, lane);
 
-    // ---- 3. pivot: max |re|+|im| over non-pivotal rows, ties -> lowest row -
+    // ---- 3+4. pivot (max |re|+|im| over non-pivotal rows, ties -> lowest
+    // row) fused with the L drop test, 256 pattern entries per load batch -
     double best = -1.0;
-    int ipiv = -1;
-    int lnum = 0;
-    for (int base = 0; base < npat; base += 32) {
-      const int t = base + lane;
-      const bool act = t < npat;
-      const int i = act ? pat[t] : 0;
-      const bool cand = act && vload(pinv + i) < 0;
-      const unsigned cm = __ballot_sync(FULL, cand);
-      if (cand) {
-        lrow[lnum + __popc(cm & lanemask_lt())] = i;
-        const double mag = cabs1(x[i]);
-        if (mag > best || (mag == best && i < ipiv)) {
-          best = mag;
-          ipiv = i;
+    int ipiv = -1, ipos = -1, ikeep = 0;
+    int lnum = 0, kept_l = 0;
+    for (int blk = 0; blk < npat; blk += 256) {
+      int iu[8], pv[8];
+      double2 xv[8];
+      double rv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = blk + 32 * u + lane;
+        iu[u] = t < npat ? pat[t] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool act = iu[u] >= 0;
+        pv[u] = act ? vload(pinv + iu[u]) : 0;
+        xv[u] = act ? x[iu[u]] : make_double2(0.0, 0.0);
+        rv[u] = (act && drop > 0.0) ? rn[iu[u]] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = iu[u];
+        const bool cand = i >= 0 && pv[u] < 0;
+        const unsigned cm = __ballot_sync(FULL, cand);
+        if (cand) {
+          const int pos = lnum + __popc(cm & lanemask_lt());
+          const double mag = cabs1(xv[u]);
+          const bool keep = !(drop > 0.0 && mag < drop * rv[u]);
+          lrow[pos] = i;
+          lkeep[pos] = keep;
+          kept_l += keep;
+          if (mag > best || (mag == best && i < ipiv)) {
+            best = mag;
+            ipiv = i;
+            ipos = pos;
+            ikeep = keep;
+          }
         }
+        lnum += __popc(cm);
       }
-      lnum += __popc(cm);
     }
+    double gbest = best;
+    int gipiv = ipiv;
     for (int o = 16; o; o >>= 1) {
-      const double ob = __shfl_xor_sync(FULL, best, o);
-      const int oi = __shfl_xor_sync(FULL, ipiv, o);
-      if (ob > best || (ob == best && oi >= 0 && (ipiv < 0 || oi < ipiv))) {
-        best = ob;
-        ipiv = oi;
+      const double ob = __shfl_xor_sync(FULL, gbest, o);
+      const int oi = __shfl_xor_sync(FULL, gipiv, o);
+      if (ob > gbest || (ob == gbest && oi >= 0 && (gipiv < 0 || oi < gipiv))) {
+        gbest = ob;
+        gipiv = oi;
       }
     }
-    if (ipiv < 0 || best == 0.0) {
+    if (gipiv < 0 || gbest == 0.0) {
       if (lane == 0) {
         state[0] = FAC_ZERO_PIVOT;
         state[1] = k;
@@ -351,82 +401,121 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       }
       break;
     }
+    // the pivot row is never an L entry: the owning lane clears its keep
+    const bool owner = (ipiv == gipiv) && ipos >= 0;
+    if (owner) lkeep[ipos] = 0;
+    const unsigned om = __ballot_sync(FULL, owner && ikeep);
+    kept_l = warp_sum_i(kept_l) - (om ? 1 : 0);
+    ipiv = gipiv;
     const double2 piv = x[ipiv];
     __syncwarp();
     probe_mark(pr, k, 2, lane);
-
-    // ---- 4. dropping ------------------------------------------------------
-    int kept_u = 0, kept_l = 0;
-    for (int t = lane; t < unum; t += 32) {
-      bool keep = true;
-      if (drop > 0.0 && cabs1(uval[t]) < drop * rn[vload(prow + urow[t])]) keep = false;
-      ukeep[t] = keep;
-      kept_u += keep;
-    }
-    for (int t = lane; t < lnum; t += 32) {
-      const int i = lrow[t];
-      bool keep = true;
-      if (i == ipiv) keep = false;
-      else if (drop > 0.0 && cabs1(x[i]) < drop * rn[i]) keep = false;
-      lkeep[t] = keep;
-      kept_l += keep;
-    }
-    kept_u = warp_sum_i(kept_u);
-    kept_l = warp_sum_i(kept_l);
-    __syncwarp();
+    probe_mark(pr, k, 3, lane);
 
     // ---- 5. fill cap: keep the best (cap-2) by (-mag, U-before-L, index) --
-    if (have_cap && kept_u + kept_l + 2 > a.fill_cap && kept_u + kept_l > 0) {
+    // Exact top-k: an 8-bit radix select over the magnitude bit patterns
+    // (non-negative doubles order like their bits) finds the allowed-th
+    // largest key T; ties at T (rare) are resolved by (U-before-L, index)
+    // with a bitwise select over the tied candidates only.
+    if (have_cap && kept_u + kept_l + 2 > fill_cap && kept_u + kept_l > 0) {
       const int ncand = kept_u + kept_l;
-      int allowed = a.fill_cap - 2;
+      int allowed = fill_cap - 2;
       if (allowed < 0) allowed = 0;
       if (allowed > ncand) allowed = ncand;
+      uint64_t* key = keys;  // [0, unum): U candidates, [unum, unum + lnum): L
+      for (int t = lane; t < unum; t += 32) key[t] = ukeep[t] ? mag_key(uval[t]) : ~0ull;
+      for (int t = lane; t < lnum; t += 32)
+        key[unum + t] = lkeep[t] ? mag_key(x[lrow[t]]) : ~0ull;
+      __syncwarp();
+      const int ntot = unum + lnum;
       uint64_t T = 0;
       uint32_t S = 0xffffffffu;
       if (allowed > 0) {
-        for (int bit = 62; bit >= 0; --bit) {
-          const uint64_t cand = T | (1ull << bit);
-          int cnt = 0;
-          for (int t = lane; t < unum; t += 32) cnt += (ukeep[t] && mag_key(uval[t]) >= cand);
-          for (int t = lane; t < lnum; t += 32) cnt += (lkeep[t] && mag_key(x[lrow[t]]) >= cand);
-          cnt = warp_sum_i(cnt);
-          if (cnt >= allowed) T = cand;
+        uint64_t prefix = 0, pmask = 0;
+        int remaining = allowed;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          for (int j = lane; j < 256; j += 32) hist[j] = 0;
+          __syncwarp();
+          for (int t = lane; t < ntot; t += 32) {
+            const uint64_t kk = key[t];
+            if (kk != ~0ull && (kk & pmask) == prefix) atomicAdd(&hist[(kk >> shift) & 255], 1u);
+          }
+          __syncwarp();
+          // lane l owns digits 255-8l .. 248-8l (high digits first)
+          unsigned c8[8], tot = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            c8[j] = hist[255 - 8 * lane - j];
+            tot += c8[j];
+          }
+          unsigned incl = tot;  // inclusive scan over lanes (high digits first)
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+          }
+          const unsigned excl = incl - tot;
+          int digit = -1;
+          unsigned above = 0;
+          if (excl < (unsigned)remaining && (unsigned)remaining <= incl) {
+            unsigned run = excl;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (digit < 0 && run + c8[j] >= (unsigned)remaining) {
+                digit = 255 - 8 * lane - j;
+                above = run;
+              }
+              run += c8[j];
+            }
+          }
+          const unsigned hit = __ballot_sync(FULL, digit >= 0);
+          const int src = __ffs(hit) - 1;
+          digit = __shfl_sync(FULL, digit, src);
+          above = __shfl_sync(FULL, above, src);
+          remaining -= (int)above;
+          prefix |= (uint64_t)digit << shift;
+          pmask |= 255ull << shift;
+          __syncwarp();
         }
-        int gt = 0;
-        for (int t = lane; t < unum; t += 32) gt += (ukeep[t] && mag_key(uval[t]) > T);
-        for (int t = lane; t < lnum; t += 32) gt += (lkeep[t] && mag_key(x[lrow[t]]) > T);
+        T = prefix;
+        int gt = 0, ties = 0;
+        for (int t = lane; t < ntot; t += 32) {
+          const uint64_t kk = key[t];
+          if (kk != ~0ull) {
+            gt += kk > T;
+            ties += kk == T;
+          }
+        }
         gt = warp_sum_i(gt);
-        const int need = allowed - gt;
-        S = 0;
-        for (int bit = 31; bit >= 0; --bit) {
-          const uint32_t cand = S | (1u << bit);
-          int cnt = 0;
-          for (int t = lane; t < unum; t += 32)
-            cnt += (ukeep[t] && mag_key(uval[t]) == T && (uint32_t)urow[t] < cand);
-          for (int t = lane; t < lnum; t += 32)
-            cnt += (lkeep[t] && mag_key(x[lrow[t]]) == T &&
-                    ((1u << 31) | (uint32_t)lrow[t]) < cand);
-          cnt = warp_sum_i(cnt);
-          if (cnt < need) S = cand;
+        ties = warp_sum_i(ties);
+        const int need = allowed - gt;  // >= 1 ties at T to take
+        if (ties > need) {
+          // secondary key (dom<<31 | idx), smallest first, among the ties
+          S = 0;
+          for (int bit = 31; bit >= 0; --bit) {
+            const uint32_t cand = S | (1u << bit);
+            int cnt = 0;
+            for (int t = lane; t < unum; t += 32)
+              cnt += (key[t] == T && (uint32_t)urow[t] < cand);
+            for (int t = lane; t < lnum; t += 32)
+              cnt += (key[unum + t] == T && ((1u << 31) | (uint32_t)lrow[t]) < cand);
+            cnt = warp_sum_i(cnt);
+            if (cnt < need) S = cand;
+          }
         }
       }
       kept_u = 0;
       kept_l = 0;
       for (int t = lane; t < unum; t += 32) {
-        bool keep = false;
-        if (allowed > 0 && ukeep[t]) {
-          const uint64_t kk = mag_key(uval[t]);
-          keep = kk > T || (kk == T && (uint32_t)urow[t] <= S);
-        }
+        const uint64_t kk = key[t];
+        const bool keep = allowed > 0 && kk != ~0ull &&
+                          (kk > T || (kk == T && (uint32_t)urow[t] <= S));
         ukeep[t] = keep;
         kept_u += keep;
       }
       for (int t = lane; t < lnum; t += 32) {
-        bool keep = false;
-        if (allowed > 0 && lkeep[t]) {
-          const uint64_t kk = mag_key(x[lrow[t]]);
-          keep = kk > T || (kk == T && ((1u << 31) | (uint32_t)lrow[t]) <= S);
-        }
+        const uint64_t kk = key[unum + t];
+        const bool keep = allowed > 0 && kk != ~0ull &&
+                          (kk > T || (kk == T && ((1u << 31) | (uint32_t)lrow[t]) <= S));
         lkeep[t] = keep;
         kept_l += keep;
       }
@@ -435,8 +524,7 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       __syncwarp();
     }
 
-    probe_mark(pr, k, 3, lane);
-    // ---- 6. emit U (kept rows ascending, pivot last), L (unit first) ------
+    // ---- 6. emit L (unit diagonal first), publish the column, then U ------
     const int32_t lnnz = vload(Lp + k);
     const int32_t unnz = vload(gUp + k);
     if ((int64_t)unnz + kept_u + 1 > a.capU || (int64_t)lnnz + kept_l + 1 > a.capL) {
@@ -447,42 +535,38 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       }
       break;
     }
-    int off = unnz;
-    for (int base = 0; base < unum; base += 32) {
-      const int t = base + lane;
-      const bool keep = t < unum && ukeep[t];
-      const unsigned m = __ballot_sync(FULL, keep);
-      if (keep) {
-        const int o = off + __popc(m & lanemask_lt());
-        Ui[o] = urow[t];
-        Ux[o] = uval[t];
-      }
-      off += __popc(m);
-    }
-    if (lane == 0) {
-      Ui[off] = k;
-      Ux[off] = piv;
-    }
-    const int32_t unew = off + 1;
     const double2 rp = recipc(piv);
     if (lane == 0) {
       Li[lnnz] = ipiv;
       Lx[lnnz] = make_double2(1.0, 0.0);
     }
-    off = lnnz + 1;
-    for (int base = 0; base < lnum; base += 32) {
-      const int t = base + lane;
-      const bool keep = t < lnum && lkeep[t];
-      const unsigned m = __ballot_sync(FULL, keep);
-      if (keep) {
-        const int o = off + __popc(m & lanemask_lt());
-        const int i = lrow[t];
-        Li[o] = i;
-        Lx[o] = cmul_plain(x[i], rp);
+    int off = lnnz + 1;
+    for (int blk = 0; blk < lnum; blk += 256) {
+      int ir[8];
+      bool kp[8];
+      double2 xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = blk + 32 * u + lane;
+        const bool act = t < lnum;
+        kp[u] = act && lkeep[t];
+        ir[u] = act ? lrow[t] : 0;
       }
-      off += __popc(m);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = kp[u] ? x[ir[u]] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned m = __ballot_sync(FULL, kp[u]);
+        if (kp[u]) {
+          const int o = off + __popc(m & lanemask_lt());
+          Li[o] = ir[u];
+          Lx[o] = cmul_plain(xv[u], rp);
+        }
+        off += __popc(m);
+      }
     }
-    __threadfence_block();
+    const int32_t unew = unnz + kept_u + 1;
+    RS_FENCE();
     __syncwarp();
     if (lane == 0) {
       vstore(gUp + k + 1, unew);
@@ -491,10 +575,28 @@ __global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
       vstore(pinv + ipiv, k);
       if (a.smem_mode) gpinv[ipiv] = k;
       vstore(prow + k, ipiv);
-      __threadfence_block();  // release column k
+      RS_FENCE();  // release column k
       ctl[0] = k + 1;
     }
     probe_mark(pr, k, 4, lane);
+    // U column k (kept rows ascending, pivot last): not read by later
+    // columns, so it is written after the release, off the critical path
+    int uo = unnz;
+    for (int base = 0; base < unum; base += 32) {
+      const int t = base + lane;
+      const bool keep = t < unum && ukeep[t];
+      const unsigned m = __ballot_sync(FULL, keep);
+      if (keep) {
+        const int o = uo + __popc(m & lanemask_lt());
+        Ui[o] = urow[t];
+        Ux[o] = uval[t];
+      }
+      uo += __popc(m);
+    }
+    if (lane == 0) {
+      Ui[uo] = k;
+      Ux[uo] = piv;
+    }
     __syncwarp();
   }
   __syncthreads();

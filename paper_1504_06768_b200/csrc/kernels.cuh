@@ -31,6 +31,7 @@ struct FactorArgs {
   const double* rn;   // row norms [B*n] (required when drop_tol > 0)
   double drop_tol;
   int32_t fill_cap;   // -1: no cap
+  const int32_t* fill_caps;  // optional per-system caps (overrides fill_cap)
   // outputs per system b; pointers are relative to b*cap
   int32_t* Lp;  // [B*(n+1)]
   int32_t* Li;
@@ -53,6 +54,7 @@ struct FactorArgs {
   int32_t* wlrow;
   uint8_t* wukeep;
   uint8_t* wlkeep;
+  uint64_t* wkey;  // cap-selection keys
   int smem_mode;     // 1: pinv / prow / Lp shadow live in shared memory
   int bits_in_smem;  // 1: per-warp pending bitmaps in shared memory
   int warps;         // warps (columns in flight) per system

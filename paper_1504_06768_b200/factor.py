@@ -90,9 +90,10 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
         # per-system cap (factor.py:92); systems of a batch share n and, in
         # every configuration, nnz -- a differing nnz would change the cap.
         caps = [int(math.ceil(fill_limit * int(z) / n)) for z in nnz_rows]
-        if len(set(caps)) != 1:
-            raise ValueError("batched ILUTP needs equal nnz across systems")
-        cap = caps[0]
+        cap = max(caps)
+    caps_t = None
+    if cap >= 0 and len(set(caps)) > 1:  # per-system caps (e.g. block-Jacobi blocks)
+        caps_t = torch.tensor(caps, dtype=torch.int32, device=dev)
     Ap, Ai, Ax = _transpose(M)
     rn = None
     if drop_tol > 0.0:
@@ -116,7 +117,7 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
     st = _lib.stream_ptr()
     while True:
         _lib.call("rs_factorize", B, n, _lib.ptr(Ap), _lib.ptr(Ai), _lib.ptr(Ax), None,
-                  float(drop_tol), cap, _lib.ptr(rn), _lib.ptr(Lp), _lib.ptr(Li), _lib.ptr(Lx),
+                  float(drop_tol), cap, _lib.ptr(caps_t), _lib.ptr(rn), _lib.ptr(Lp), _lib.ptr(Li), _lib.ptr(Lx),
                   capL, _lib.ptr(Up), _lib.ptr(Ui), _lib.ptr(Ux), capU, _lib.ptr(pinv),
                   _lib.ptr(state), st)
         sh = state.reshape(B, 3).cpu().numpy()

@@ -1,0 +1,393 @@
+"""Large-system path: row-sharded, block-Jacobi, multi-kernel inverse power.
+
+For a Liouvillian too large for one CTA (config 5: two coupled Kerr cavities,
+n = 2,560,000, nnz = 37M) the RCM-ordered shifted matrix is split into
+contiguous row ranges, one per rank (one process per GPU).  Each rank keeps
+  * its rows of the shifted and plain matrices with column indices remapped
+    to an extended local vector [left halo | own rows | right halo] -- the RCM
+    band keeps every halo inside the neighbouring shard;
+  * a block-Jacobi ILUTP preconditioner: the diagonal blocks of its rows,
+    factored as one batch (csrc/ilu.cu, one CTA per block) and applied as one
+    batch (csrc/cta_ops.cuh, one CTA per block) -- no factor communication.
+Per Krylov step the only communication is the halo exchange before each
+SpMV (point-to-point with ranks r-1 and r+1) and all-reduces of the dot
+products (several scalars packed into one message) and of the max-norm.
+
+The iteration is the reference's, unchanged: inverse_power
+(pkg/src/rhosolve/steady.py:177-260) around an inner bicgstab
+(pkg/src/rhosolve/krylov.py:181-291) to tol/10.  Block-Jacobi is weaker than
+the reference's global ILUTP, so inner iteration counts are higher (SURVEY.md
+7.4 item 9); parity is judged on rho and the plain-L residual.
+
+The driver is written against a small `ops` interface so the distributed
+control flow can be exercised on CPU ranks (gloo) in tests; the GPU ops are
+`GpuOps` (C ABI kernels, NCCL collectives through torch.distributed).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+import torch
+
+from . import _lib, factor, liouville, ordering
+from .sparse import DeviceCSR
+from .steady import (InnerSolverError, PowerIterationError, SteadyStateResult, MAX_OUTER,
+                     start_vector)
+
+__all__ = ["shard_range", "ShardedMatrix", "GpuOps", "bicgstab_dist", "inverse_power_dist",
+           "inverse_power_sharded"]
+
+
+def shard_range(n, rank, world):
+    """Contiguous row range [r0, r1) of `rank`."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+class Comm:
+    """Collectives over an optional torch.distributed group (None = 1 rank)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.group = group
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+
+    def allreduce_sum(self, t):
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def allreduce_max(self, t):
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    def allgather_ints(self, vals, device):
+        t = torch.tensor(vals, dtype=torch.int64, device=device)
+        if self.world == 1:
+            return [vals]
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.tolist() for o in out]
+
+    def exchange(self, sends, recvs):
+        """Point-to-point: sends = [(peer, tensor)], recvs = [(peer, tensor)]."""
+        if self.world == 1 or (not sends and not recvs):
+            return
+        ops = [self.dist.P2POp(self.dist.isend, t, p, self.group) for p, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, t, p, self.group) for p, t in recvs]
+        for req in self.dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+class ShardedMatrix:
+    """Rows [r0, r1) of an n x n CSR with columns remapped to the extended
+    local vector x_ext = x[lo:hi] (lo <= r0, hi >= r1).  Built from host or
+    device CSR arrays of the whole (ordered) matrix."""
+
+    def __init__(self, n, row_ptr, col_idx, values, r0, r1, comm, device):
+        self.n, self.r0, self.r1 = n, r0, r1
+        rp = row_ptr[r0:r1 + 1]
+        base = int(rp[0])
+        end = int(rp[-1])
+        ci = col_idx[base:end]
+        self.lo = min(int(ci.min()), r0) if end > base else r0
+        self.hi = max(int(ci.max()) + 1, r1) if end > base else r1
+        self.row_ptr = (rp - base).to(device=device, dtype=torch.int32)
+        self.col_idx = (ci - self.lo).to(device=device, dtype=torch.int32)
+        self.values = values[base:end].to(device)
+        self.nloc = r1 - r0
+        self.comm = comm
+        self.device = device
+        self._plan()
+
+    def _plan(self):
+        allb = self.comm.allgather_ints([self.lo, self.hi, self.r0, self.r1], self.device)
+        rk, W = self.comm.rank, self.comm.world
+        self.left = self.r0 - self.lo    # halo entries needed from rank-1
+        self.right = self.hi - self.r1   # halo entries needed from rank+1
+        if rk > 0 and self.lo < allb[rk - 1][2]:
+            raise ValueError("RCM band wider than a shard: halo spans more than one rank")
+        if rk + 1 < W and self.hi > allb[rk + 1][3]:
+            raise ValueError("RCM band wider than a shard: halo spans more than one rank")
+        # what the neighbours need from me
+        self.send_left = (allb[rk - 1][1] - self.r0) if rk > 0 else 0
+        self.send_right = (self.r1 - allb[rk + 1][0]) if rk + 1 < W else 0
+        self.xe = torch.zeros(self.hi - self.lo, dtype=torch.complex128, device=self.device)
+
+    def extend(self, x_local):
+        """x_ext with own entries and the neighbours' halo values."""
+        xe = self.xe
+        xe[self.left:self.left + self.nloc] = x_local
+        sends, recvs = [], []
+        rk = self.comm.rank
+        if self.send_left:
+            sends.append((rk - 1, x_local[:self.send_left].contiguous()))
+        if self.send_right:
+            sends.append((rk + 1, x_local[self.nloc - self.send_right:].contiguous()))
+        lbuf = rbuf = None
+        if self.left:
+            lbuf = torch.empty(self.left, dtype=x_local.dtype, device=x_local.device)
+            recvs.append((rk - 1, lbuf))
+        if self.right:
+            rbuf = torch.empty(self.right, dtype=x_local.dtype, device=x_local.device)
+            recvs.append((rk + 1, rbuf))
+        self.comm.exchange(sends, recvs)
+        if lbuf is not None:
+            xe[:self.left] = lbuf
+        if rbuf is not None:
+            xe[self.left + self.nloc:] = rbuf
+        return xe
+
+
+class GpuOps:
+    """Distributed-vector primitives on the C ABI kernels."""
+
+    def __init__(self, comm):
+        self.comm = comm
+        self._scal = torch.empty(8, dtype=torch.float64, device="cuda")
+
+    def matvec(self, A, x_local):
+        xe = A.extend(x_local)
+        y = torch.empty(A.nloc, dtype=torch.complex128, device=x_local.device)
+        _lib.call("rs_csr_matvec", 1, A.nloc, _lib.ptr(A.row_ptr), _lib.ptr(A.col_idx),
+                  _lib.ptr(A.values), _lib.ptr(xe), _lib.ptr(y), _lib.stream_ptr())
+        return y
+
+    def psolve(self, M, v):
+        return factor.solve_lu_device(M, v) if M is not None else v.clone()
+
+    def dots(self, pairs):
+        """[vdot(x, y)] summed over ranks (one all-reduce for all pairs)."""
+        import ctypes
+        k = len(pairs)
+        P = ctypes.c_void_p * k
+        xs = P(*[x.data_ptr() for x, _ in pairs])
+        ys = P(*[y.data_ptr() for _, y in pairs])
+        out = self._scal[:2 * k]
+        _lib.call("rs_vdots", pairs[0][0].numel(), k, xs, ys, _lib.ptr(out), _lib.stream_ptr())
+        self.comm.allreduce_sum(out)
+        h = out.cpu().numpy()
+        return [complex(h[2 * j], h[2 * j + 1]) for j in range(k)]
+
+    def amax(self, x):
+        out = self._scal[:1]
+        _lib.call("rs_amax", x.numel(), _lib.ptr(x), _lib.ptr(out), _lib.stream_ptr())
+        self.comm.allreduce_max(out)
+        return float(out.item())
+
+    def lincomb(self, terms, out=None):
+        """sum c_k v_k for up to 4 (coefficient, vector) pairs."""
+        import ctypes
+        k = len(terms)
+        n = terms[0][1].numel()
+        if out is None:
+            out = torch.empty(n, dtype=torch.complex128, device=terms[0][1].device)
+        vs = (ctypes.c_void_p * k)(*[v.data_ptr() for _, v in terms])
+        cre = (ctypes.c_double * k)(*[complex(c).real for c, _ in terms])
+        cim = (ctypes.c_double * k)(*[complex(c).imag for c, _ in terms])
+        _lib.call("rs_lincomb", n, k, vs, cre, cim, _lib.ptr(out), _lib.stream_ptr())
+        return out
+
+
+def _norm(ops, v):
+    return math.sqrt(max(ops.dots([(v, v)])[0].real, 0.0))
+
+
+def bicgstab_dist(ops, A, M, b, tol, max_iter):
+    """krylov.bicgstab (krylov.py:181-291) over row-sharded vectors.
+    Returns (x_local, iterations, converged, breakdown)."""
+    z = torch.zeros_like(b)
+    bnorm = _norm(ops, b)
+    if bnorm == 0.0:
+        return z, 0, True, False
+    pb = ops.psolve(M, b)
+    pbn = _norm(ops, pb)
+    if pbn == 0.0 or not np.isfinite(pbn):
+        return z, 0, False, True
+    x = torch.zeros_like(b)
+    r = pb.clone()
+    rh = r.clone()
+    rhn = _norm(ops, rh)
+    rho_old = alpha = omega = 1.0 + 0.0j
+    v = torch.zeros_like(b)
+    p = torch.zeros_like(b)
+    target, prev, it = tol * pbn, math.inf, 0
+    conv = brk = False
+    while it < max_iter:
+        rn = _norm(ops, r)
+        if rn <= target:
+            tr = _norm(ops, ops.lincomb([(1.0, b), (-1.0, ops.matvec(A, x))]))
+            if tr <= tol * bnorm:
+                conv = True
+                break
+            if tr >= 0.5 * prev:
+                break
+            prev, target = tr, target * 0.1
+        rho = ops.dots([(rh, r)])[0]
+        if abs(rho) < 1e-30 or abs(rho) < 1e-16 * rhn * rn:
+            brk = True
+            break
+        if it == 0:
+            p = r.clone()
+        else:
+            beta = (rho / rho_old) * (alpha / omega)
+            p = ops.lincomb([(1.0, r), (beta, p), (-beta * omega, v)])
+        v = ops.psolve(M, ops.matvec(A, p))
+        den = ops.dots([(rh, v)])[0]
+        if den == 0.0:
+            brk = True
+            break
+        alpha = rho / den
+        s = ops.lincomb([(1.0, r), (-alpha, v)])
+        it += 1
+        if _norm(ops, s) <= target:
+            x = ops.lincomb([(1.0, x), (alpha, p)])
+            tr = _norm(ops, ops.lincomb([(1.0, b), (-1.0, ops.matvec(A, x))]))
+            if tr <= tol * bnorm:
+                conv = True
+                break
+            if tr >= 0.5 * prev:
+                break
+            prev, target = tr, target * 0.1
+            r = s
+            rh = r.clone()
+            rhn = _norm(ops, rh)
+            rho_old = alpha = omega = 1.0 + 0.0j
+            v = torch.zeros_like(b)
+            p = torch.zeros_like(b)
+            continue
+        t = ops.psolve(M, ops.matvec(A, s))
+        tt, ts = ops.dots([(t, t), (t, s)])
+        if tt == 0.0:
+            brk = True
+            break
+        omega = ts / tt
+        x = ops.lincomb([(1.0, x), (alpha, p), (omega, s)])
+        r = ops.lincomb([(1.0, s), (-omega, t)])
+        rho_old = rho
+        if omega == 0.0:
+            brk = True
+            break
+    return x, it, conv, brk
+
+
+def inverse_power_dist(ops, A, P, M, x0, tol, max_iter, max_outer=MAX_OUTER, log=None):
+    """steady.inverse_power outer loop (steady.py:518-541) over shards.
+    x0: this rank's slice of the (un-normalised) start vector."""
+    x = ops.lincomb([(1.0 / _norm(ops, x0), x0)])
+    outer, inner = 0, []
+    while outer < max_outer:
+        t = time.perf_counter()
+        y, its, _, brk = bicgstab_dist(ops, A, M, x, tol / 10, max_iter)
+        inner.append(its)
+        if log:
+            log(f"outer {outer}: {its} inner iterations in {time.perf_counter() - t:.2f}s")
+        ny = _norm(ops, y)
+        if brk or not np.isfinite(ny):
+            raise InnerSolverError("inner Krylov solve broke down; try a smaller drop "
+                                   "tolerance or a larger fill budget")
+        if ny == 0.0:
+            raise InnerSolverError("inner Krylov solve made no progress")
+        y = ops.lincomb([(1.0 / ny, y)])
+        outer += 1
+        ov = ops.dots([(y, x)])[0]
+        aligned = ops.lincomb([(ov / abs(ov), y)]) if ov != 0 else y
+        diff = _norm(ops, ops.lincomb([(1.0, aligned), (-1.0, x)]))
+        resid_inf = ops.amax(ops.matvec(P, y))
+        x = y
+        if diff <= tol or resid_inf <= tol:
+            return x, outer, inner
+    raise PowerIterationError(f"no convergence within {max_outer} outer iterations")
+
+
+def _block_jacobi(A_local_rows, r0, nloc, block, d, p):
+    """Diagonal blocks of this rank's rows -> batched ILUTP factors."""
+    import ctypes
+    dev = A_local_rows[0].device
+    rp, ci, v = A_local_rows
+    orp = torch.empty(nloc + 1, dtype=torch.int32, device=dev)
+    nnz = ctypes.c_int64(0)
+    st = _lib.stream_ptr()
+    _lib.call("rs_block_extract", nloc, block, r0, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(v),
+              _lib.ptr(orp), None, None, ctypes.byref(nnz), st)
+    oci = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+    ov = torch.empty(max(nnz.value, 1), dtype=torch.complex128, device=dev)
+    _lib.call("rs_block_extract", nloc, block, r0, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(v),
+              _lib.ptr(orp), _lib.ptr(oci), _lib.ptr(ov), ctypes.byref(nnz), st)
+    B = DeviceCSR(block, nloc // block, orp, oci[:nnz.value], ov[:nnz.value])
+    return factor.factor_batch(B, d, p, raise_on_fail=True)
+
+
+def pick_block(nloc, target=5000):
+    """Largest divisor of nloc not above `target` (block size)."""
+    best = 1
+    for b in range(1, int(math.isqrt(nloc)) + 1):
+        if nloc % b == 0:
+            for c in (b, nloc // b):
+                if c <= target and c > best:
+                    best = c
+    return best
+
+
+def inverse_power_sharded(L, sigma=liouville.DEFAULT_SIGMA, tol=1e-10, d=1e-5, p=10.0,
+                          max_iter=1000, seed=3, blocks=8, group=None, log=None):
+    """Doubly-iterative inverse power (inner BiCGStab, block-Jacobi ILUTP under
+    RCM) with the rows sharded over the ranks of `group` (one GPU each).
+    `blocks` = total block-Jacobi blocks (a multiple of the world size), so
+    every world size runs the same preconditioner.  Block-Jacobi is much
+    weaker than a global ILUTP when blocks are small compared with the RCM
+    level width, hence few large blocks.  Every rank
+    passes the same plain LiouvillianSystem; rho is returned on every rank."""
+    comm = Comm(group)
+    ops = GpuOps(comm)
+    say = (lambda m: log(f"[rank {comm.rank}] {m}")) if log else (lambda m: None)
+    t0 = time.perf_counter()
+    torch.cuda.synchronize()
+    shifted = liouville.shift(L, sigma)
+    fwd, inv = ordering.rcm_device(shifted.matrix)   # deterministic: same on every rank
+    torch.cuda.synchronize()
+    say(f"shift + rcm {time.perf_counter() - t0:.2f}s")
+    S = ordering.permute(shifted.matrix, fwd, inv)
+    Pm = ordering.permute(L.matrix, fwd, inv)
+    n = S.n
+    r0, r1 = shard_range(n, comm.rank, comm.world)
+    A = ShardedMatrix(n, S.row_ptr, S.col_idx, S.values, r0, r1, comm, S.values.device)
+    P = ShardedMatrix(n, Pm.row_ptr, Pm.col_idx, Pm.values, r0, r1, comm, S.values.device)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    nloc = r1 - r0
+    if blocks % comm.world or n % blocks:
+        raise ValueError(f"blocks={blocks} must be a multiple of the world size and divide n")
+    block = n // blocks
+    rp = S.row_ptr[r0:r1 + 1]
+    say(f"permute + shard {t1 - t0:.2f}s total; factoring {nloc // block} blocks of {block}")
+    M = _block_jacobi((rp, S.col_idx, S.values), r0, nloc, block, d, p)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    say(f"block-Jacobi ILUTP {t2 - t1:.2f}s, fill {float(np.sum(M.lnnz + M.unnz)):.3e} entries")
+    x0 = torch.from_numpy(start_vector(n, seed)[r0:r1].copy()).to(S.values.device)
+    x, outer, inner = inverse_power_dist(ops, A, P, M, x0, tol, max_iter, log=say)
+    # gather the (permuted) solution and post-process on every rank
+    if comm.world > 1:
+        parts = [torch.empty(shard_range(n, k, comm.world)[1] - shard_range(n, k, comm.world)[0],
+                             dtype=x.dtype, device=x.device) for k in range(comm.world)]
+        comm.dist.all_gather(parts, x.contiguous(), group=group)
+        xg = torch.cat(parts)
+    else:
+        xg = x
+    from .steady import _postprocess
+    rho, res = _postprocess(xg, fwd, L)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    return SteadyStateResult(
+        rho=rho[0], method="power-doubly-iterative", ordering="rcm", residual=float(res[0]),
+        iterations=outer, fill_factor=float(np.sum(M.lnnz + M.unnz) / max(M.nsys, 1)),
+        condest=None, build_time=t1 - t0, factor_time=t2 - t1, solve_time=t3 - t2, seed=seed,
+        inner_iterations=int(sum(inner)),
+        extra={"block": block, "blocks_per_rank": nloc // block, "world": comm.world,
+               "inner_per_outer": inner})

@@ -128,3 +128,77 @@ def test_factorize_batch_matches_single(cuda):
         xs[b * m.n:(b + 1) * m.n] = x
         got = factor.solve_lu(f, xs)[b * m.n:(b + 1) * m.n]
         assert bits_equal(got, fo.solve(x))
+
+
+def test_rcm_random_corpus_bit_exact(cuda):
+    """The 30 seeded random structures (some disconnected, isolated nodes) the
+    reference ordered in tests/golden/make_golden.py, as one batch."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "rcm_corpus.npz"))
+    k = 0
+    while f"s{k}_n" in g:
+        n = int(g[f"s{k}_n"])
+        m = CSRMatrix(n, n, g[f"s{k}_rp"], g[f"s{k}_ci"], np.ones(len(g[f"s{k}_ci"])))
+        p = ordering.rcm(from_host(m))
+        assert bits_equal(p.inverse, g[f"s{k}_inv"]), k
+        k += 1
+    assert k == 30
+
+
+def test_rcm_batch_equals_single(cuda):
+    mats = [_host(O.shift(oracle_L(*model("c4", i=i)))) for i in (0, 100, 511)]
+    fwd, inv = ordering.rcm_device(from_host(mats))
+    for b, m in enumerate(mats):
+        f1, _ = O.rcm(O.CSR(m.nrows, m.ncols, m.row_ptr, m.col_idx, m.values))
+        assert bits_equal(fwd[b * m.nrows:(b + 1) * m.nrows].cpu().numpy().astype(np.int64), f1)
+
+
+def test_vector_kernels(cuda):
+    import ctypes
+    n = 100_003
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
+    y = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
+    out = torch.empty(4, dtype=torch.float64, device="cuda")
+    P = ctypes.c_void_p * 2
+    _lib.call("rs_vdots", n, 2, P(x.data_ptr(), y.data_ptr()), P(y.data_ptr(), y.data_ptr()),
+              _lib.ptr(out), _lib.stream_ptr())
+    h = out.cpu().numpy()
+    ref = np.vdot(x.cpu().numpy(), y.cpu().numpy())
+    assert abs(complex(h[0], h[1]) - ref) <= 1e-12 * abs(ref) * 10
+    assert abs(h[2] - np.vdot(y.cpu().numpy(), y.cpu().numpy()).real) <= 1e-10
+    _lib.call("rs_amax", n, _lib.ptr(x), _lib.ptr(out), _lib.stream_ptr())
+    assert out[0].item() == x.abs().max().item()
+    z = torch.empty_like(x)
+    c = (ctypes.c_double * 2)
+    _lib.call("rs_lincomb", n, 2, P(x.data_ptr(), y.data_ptr()), c(2.0, 0.5), c(0.0, -1.0),
+              _lib.ptr(z), _lib.stream_ptr())
+    assert torch.allclose(z, 2 * x + (0.5 - 1j) * y, rtol=1e-14, atol=1e-14)
+
+
+def test_block_extract(cuda):
+    import ctypes
+    H, c = model("c1")
+    Lo = O.shift(oracle_L(H, c))
+    A = from_host(_host(Lo))
+    rp = torch.empty(401, dtype=torch.int32, device="cuda")
+    nnz = ctypes.c_int64(0)
+    _lib.call("rs_block_extract", 400, 100, 0, _lib.ptr(A.row_ptr), _lib.ptr(A.col_idx),
+              _lib.ptr(A.values), _lib.ptr(rp), None, None, ctypes.byref(nnz), _lib.stream_ptr())
+    ci = torch.empty(nnz.value, dtype=torch.int32, device="cuda")
+    v = torch.empty(nnz.value, dtype=torch.complex128, device="cuda")
+    _lib.call("rs_block_extract", 400, 100, 0, _lib.ptr(A.row_ptr), _lib.ptr(A.col_idx),
+              _lib.ptr(A.values), _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(v), ctypes.byref(nnz),
+              _lib.stream_ptr())
+    d = Lo.dense()
+    got = np.zeros((400, 400), complex)
+    rph = rp.cpu().numpy()
+    for r in range(400):
+        b = r // 100
+        for q in range(rph[r], rph[r + 1]):
+            got[r, b * 100 + ci[q].item()] = v[q].item()
+    want = np.zeros_like(d)
+    for b in range(4):
+        want[b * 100:(b + 1) * 100, b * 100:(b + 1) * 100] = d[b * 100:(b + 1) * 100,
+                                                                b * 100:(b + 1) * 100]
+    assert bits_equal(got, want)

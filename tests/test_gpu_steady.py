@@ -77,3 +77,29 @@ def test_c4_batch_power_direct(cuda):
         ref = O.inverse_power(oracle_L(H, c), 40, tol=1e-12, inner="direct", seed=2 + i)
         assert r.error is None
         _check(r, ref)
+
+
+@pytest.mark.slow
+def test_c3_inverse_power_bicgstab_defaults(cuda):
+    """Optomechanics 6x40 (n = 57,600): inverse power with ILUTP(1e-4, 300)
+    BiCGStab under RCM, against the rho the reference itself produced."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c3.npz"))
+    H, c = model("c3")
+    L = liouville.build_liouvillian(H, c)
+    res = steady.inverse_power(L, tol=1e-12, inner="iterative", ordering_name="rcm",
+                               solver="bicgstab", d=1e-4, p=300.0)
+    assert res.residual <= 1e-10
+    assert O.trace_distance(res.rho, g["power_bicgstab_rho"]) <= 1e-6
+
+
+def test_sharded_path_single_gpu_kerr_kerr(cuda):
+    """Config-5 code path (row-sharded driver, block-Jacobi ILUTP, grid-wide
+    BiCGStab) at N=8 on one GPU, against the oracle's direct inverse power."""
+    from paper_1504_06768_b200 import configs, sharded
+    H, c = configs.kerr_kerr(N=8)
+    L = liouville.build_liouvillian(H, c)
+    res = sharded.inverse_power_sharded(L, tol=1e-10, d=1e-5, p=10.0, seed=3, blocks=2)
+    ref = O.inverse_power(oracle_L(H, c), 64, tol=1e-12, inner="direct", seed=3)
+    assert res.residual <= 1e-10
+    assert O.trace_distance(res.rho, ref["rho"]) <= 1e-6
