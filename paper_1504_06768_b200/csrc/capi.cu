@@ -143,7 +143,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.capU = capU;
   a.pinv = pinv;
   a.state = state;
-  a.warps = nsys >= 148 ? 8 : 32;
+  a.warps = nsys >= 148 ? 8 : 16;
   if (const char* e = getenv("RHOSOLVE_ILU_WARPS")) a.warps = atoi(e);  // tuning knob
   RS_TRY(ilutp_plan(n, a.warps, &a.smem_mode, &a.bits_in_smem));
   const int nwords = (n + 31) / 32;

@@ -388,24 +388,26 @@ __global__ void factor_strip_count_kernel(int B, int32_t n, const int32_t* cp, i
   (void)lower;
 }
 
+// one warp per factor column: coalesced copy of its off-diagonal entries
 __global__ void factor_strip_fill_kernel(int B, int32_t n, const int32_t* cp,
                                          const int32_t* ri, const double2* rv, int64_t cap,
                                          int lower, const int32_t* out_rp, int32_t* out_ci,
                                          double2* out_v, double2* rU) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (r >= (int64_t)B * n) return;
   const int64_t b = r / n, k = r % n;
   const int32_t* p = cp + b * (n + 1);
   const int32_t* I = ri + b * cap;
   const double2* X = rv + b * cap;
-  int32_t o = out_rp[r];
+  const int32_t o = out_rp[r];
   const int32_t s = lower ? p[k] + 1 : p[k];
   const int32_t e = lower ? p[k + 1] : p[k + 1] - 1;
-  for (int32_t q = s; q < e; ++q, ++o) {
-    out_ci[o] = I[q];
-    out_v[o] = X[q];
+  for (int32_t q = s + lane; q < e; q += 32) {
+    out_ci[o + (q - s)] = I[q];
+    out_v[o + (q - s)] = X[q];
   }
-  if (!lower) rU[r] = recipc(X[p[k + 1] - 1]);
+  if (!lower && lane == 0) rU[r] = recipc(X[p[k + 1] - 1]);
 }
 
 int factor_to_csr(int B, int32_t n, const int32_t* cp, const int32_t* ri, const double2* rv,
@@ -430,8 +432,8 @@ int factor_to_csr(int B, int32_t n, const int32_t* cp, const int32_t* ri, const 
   double2* cv = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&cci, sizeof(int32_t) * (nnz + 1), st));
   RS_CUDA_TRY(cudaMallocAsync(&cv, sizeof(double2) * (nnz + 1), st));
-  factor_strip_fill_kernel<<<grid_for(nrows, 256), 256, 0, st>>>(B, n, cp, ri, rv, cap, lower,
-                                                                 crp, cci, cv, rU); ::rs::count_launch();
+  factor_strip_fill_kernel<<<grid_for(nrows * 32, 256), 256, 0, st>>>(B, n, cp, ri, rv, cap,
+                                                                      lower, crp, cci, cv, rU); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   rc = csr_transpose(B, n, crp, cci, cv, out_rp, out_ci, out_v, st);
   cudaFreeAsync(crp, st);

@@ -88,7 +88,8 @@ __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_
   return (b + 15) & ~(size_t)15;
 }
 
-__global__ void __launch_bounds__(1024) ilutp_pipeline_kernel(FactorArgs a) {
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -614,9 +615,25 @@ int launch_ilutp(const FactorArgs& a, cudaStream_t st) {
   if (a.B == 0 || a.n == 0) return RS_OK;
   const int W = a.warps;
   const size_t smem = ilutp_smem_bytes(a.n, W, a.smem_mode, a.bits_in_smem);
-  RS_CUDA_TRY(cudaFuncSetAttribute(ilutp_pipeline_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  ilutp_pipeline_kernel<<<a.B, 32 * W, smem, st>>>(a); ::rs::count_launch();
+  // one instantiation per block size so each gets its full register budget
+  // (a 1024-thread bound caps registers at 64 and spills the tail loops)
+  auto launch = [&](auto kern) -> int {
+    RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    kern<<<a.B, 32 * W, smem, st>>>(a);
+    ::rs::count_launch();
+    return RS_OK;
+  };
+  // batches: keep 4 systems per SM resident (512 systems ~ one wave)
+  const bool batch = a.B > 148;
+  int rc;
+  (void)0;
+  if (W <= 4) rc = batch ? launch(ilutp_pipeline_kernel<128, 4>) : launch(ilutp_pipeline_kernel<128, 1>);
+  else if (W <= 6) rc = batch ? launch(ilutp_pipeline_kernel<192, 4>) : launch(ilutp_pipeline_kernel<192, 1>);
+  else if (W <= 8) rc = batch ? launch(ilutp_pipeline_kernel<256, 4>) : launch(ilutp_pipeline_kernel<256, 1>);
+  else if (W <= 16) rc = launch(ilutp_pipeline_kernel<512, 1>);
+  else rc = launch(ilutp_pipeline_kernel<1024, 1>);
+  if (rc) return rc;
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
