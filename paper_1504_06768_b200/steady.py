@@ -119,6 +119,11 @@ def _prepare(system, ordering_name, plain=None):
 def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0):
     dev = A.values.device
     B, n = A.nsys, A.n
+    if not threads:
+        # one CTA per system: big batches use 4-warp CTAs so four systems stay
+        # resident per SM (one wave for the 512-instance sweep); a lone system
+        # gets 16 warps
+        threads = 128 if B > 148 else 512
     x = torch.empty(B * n, dtype=torch.complex128, device=dev)
     stats = torch.zeros(B * _STATS_DT.itemsize, dtype=torch.uint8, device=dev)
     a = _lib.SolverArgs()
