@@ -100,6 +100,47 @@ int rs_factor_rows(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li
                    int32_t* U_rp, int32_t* U_ci, rs_complex* U_v,
                    rs_complex* rdiag, int64_t* U_nnz, void* stream);
 
+/* SELL-32 copy of a row-oriented triangular factor from rs_factor_rows for
+ * the lane-per-row sweeps: sweep order q (L: row q; U: row n-1-q), slice s =
+ * positions 32s..32s+31, entry k of lane l at sptr[s] + 32k + l, terms in the
+ * reference fold order (L ascending, U descending column; _ckernels.pyx:
+ * 53-85), padding column -1.  sptr has nsys*ceil(n/32)+1 entries (absolute).
+ * Call with sci == NULL to fill sptr and *total (host), then again to fill. */
+int rs_sell_build(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp,
+                  const int32_t* ci, const rs_complex* v, int32_t* sptr, int32_t* sci,
+                  rs_complex* sv, int64_t* total, void* stream);
+
+/* rdiag[b*n + k] = recipc(U_kk) (_ckernels.pyx:25-31, 70-85) from the raw
+ * CSC U of rs_factorize (pivot = last entry of each column). */
+int rs_pivot_recip(int32_t nsys, int32_t n, const int32_t* Up, const rs_complex* Ux,
+                   int64_t capU, rs_complex* rdiag, void* stream);
+
+/* 1 when systems of order n run the column-oriented sweeps (the sweep vector
+ * and the factor staging ring fit one CTA's shared memory), else 0. */
+int rs_col_sweep_supported(int32_t n);
+
+/* Column stream of one triangle of the raw CSC factors (rs_factorize) for
+ * the column-oriented sweeps: columns in sweep order j (L: column j; U:
+ * column n-1-j), each column's off-diagonal entries padded to whole 32-entry
+ * rows (index -1 = padding); meta[row] = 1 when the row continues the
+ * previous column; for U, rrd[first row of column c] = rdiag[c].  rowoff
+ * (nsys*n+1, absolute) gives each column's first row.  Call with idx ==
+ * NULL to fill rowoff and *total_rows (host), then again to fill. */
+int rs_col_stream_build(int32_t nsys, int32_t n, int32_t upper, const int32_t* cp,
+                        const int32_t* ci, const rs_complex* cv, int64_t cap,
+                        const rs_complex* rdiag, int32_t* rowoff, int32_t* idx,
+                        rs_complex* val, int32_t* meta, rs_complex* rrd, int64_t* total_rows,
+                        void* stream);
+
+/* x = M^{-1} b through the column streams: y[pinv] = b, then the reference
+ * lower_solve / upper_solve column loops (_ckernels.pyx:53-85) verbatim on
+ * shared memory; bit-identical.  Requires rs_col_sweep_supported(n). */
+int rs_lu_solve_cols(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t* Ls_rowoff,
+                     const int32_t* Ls_idx, const rs_complex* Ls_val, const int32_t* Ls_meta,
+                     const int32_t* Us_rowoff, const int32_t* Us_idx, const rs_complex* Us_val,
+                     const int32_t* Us_meta, const rs_complex* Us_rd, const rs_complex* b,
+                     rs_complex* x, void* stream);
+
 /* x = M^{-1} b through the factors: y[pinv] = b; lower_solve; upper_solve;
  * x = y.  Replaces factor.solve_lu (factor.py:137-149) with
  * lower_solve/upper_solve (_ckernels.pyx:53-85); bit-identical. */
@@ -230,6 +271,20 @@ typedef struct rs_solver_args {
   int32_t restart_m;
   int32_t max_outer;
   int32_t want_condest;
+  /* optional column streams of L and U from rs_col_stream_build.  When set
+   * and rs_col_sweep_supported(n), the preconditioner apply runs the
+   * reference's column-oriented lower/upper solves on shared memory and
+   * L_rp..U_v may be NULL (rdiag is still required); otherwise the
+   * row-oriented factors above are required. */
+  const int32_t* Ls_rowoff;
+  const int32_t* Ls_idx;
+  const rs_complex* Ls_val;
+  const int32_t* Ls_meta;
+  const int32_t* Us_rowoff;
+  const int32_t* Us_idx;
+  const rs_complex* Us_val;
+  const int32_t* Us_meta;
+  const rs_complex* Us_rd;
 } rs_solver_args;
 
 /* One launch runs the whole solve of every system on the device. */

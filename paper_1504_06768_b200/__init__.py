@@ -7,7 +7,7 @@ include/rhosolve_b200.h (library: _lib/librhosolve_b200.so).  There is no
 CPU fallback: without the library or a GPU the solver entry points raise.
 """
 
-from .sparse import CSRMatrix, Permutation, DeviceCSR, from_host
+from .sparse import CSRMatrix, Permutation, DeviceCSR, PinnedBatchCSR, from_host, pin_batch
 from .operators import QuantumOperator, destroy, spin_ops, embed, identity_operator
 from .liouville import (LiouvillianSystem, build_liouvillian, build_liouvillian_batch, shift,
                         build_modified, default_weight, DEFAULT_SIGMA)

@@ -59,7 +59,10 @@ class SolverArgs(ctypes.Structure):
                 ("U_rp", _vp), ("U_ci", _vp), ("U_v", _vp), ("rdiag", _vp),
                 ("pinv", _vp), ("rhs", _vp), ("x", _vp), ("stats", _vp),
                 ("tol", _f64), ("max_iter", _i32), ("restart_m", _i32),
-                ("max_outer", _i32), ("want_condest", _i32)]
+                ("max_outer", _i32), ("want_condest", _i32),
+                ("Ls_rowoff", _vp), ("Ls_idx", _vp), ("Ls_val", _vp), ("Ls_meta", _vp),
+                ("Us_rowoff", _vp), ("Us_idx", _vp), ("Us_val", _vp), ("Us_meta", _vp),
+                ("Us_rd", _vp)]
 
 
 # name -> argtypes; every function returns int32 status
@@ -71,6 +74,13 @@ _SIGS = {
     "rs_factor_rows": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64,
                        _vp, _vp, _vp, ctypes.POINTER(_i64), _vp, _vp, _vp, _vp,
                        ctypes.POINTER(_i64), _vp],
+    "rs_sell_build": [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "rs_pivot_recip": [_i32, _i32, _vp, _vp, _i64, _vp, _vp],
+    "rs_col_sweep_supported": [_i32],
+    "rs_col_stream_build": [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
+                            _vp, ctypes.POINTER(_i64), _vp],
+    "rs_lu_solve_cols": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                         _vp, _vp],
     "rs_lu_solve": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "rs_liouvillian": [_i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
                        ctypes.POINTER(_f64), _vp, _vp, _vp, ctypes.POINTER(_i64), _vp],

@@ -200,6 +200,66 @@ int rs_factor_rows(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li
   return RS_OK;
 }
 
+int rs_sell_build(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp,
+                  const int32_t* ci, const rs_complex* v, int32_t* sptr, int32_t* sci,
+                  rs_complex* sv, int64_t* total, void* stream) {
+  RS_TRY(keep_pool_memory());
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  RS_CHECK_ARG(sptr != nullptr, "sptr is required");
+  return sell_build(nsys, n, upper ? 1 : 0, rp, ci, C2(v), sptr, sci, M2(sv), total, S(stream));
+}
+
+int rs_col_sweep_supported(int32_t n) { return rs::col_ring_size(n, 1) > 0 ? 1 : 0; }
+
+int rs_pivot_recip(int32_t nsys, int32_t n, const int32_t* Up, const rs_complex* Ux,
+                   int64_t capU, rs_complex* rdiag, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  return pivot_recip(nsys, n, Up, C2(Ux), capU, M2(rdiag), S(stream));
+}
+
+int rs_col_stream_build(int32_t nsys, int32_t n, int32_t upper, const int32_t* cp,
+                        const int32_t* ci, const rs_complex* cv, int64_t cap,
+                        const rs_complex* rdiag, int32_t* rowoff, int32_t* idx,
+                        rs_complex* val, int32_t* meta, rs_complex* rrd, int64_t* total_rows,
+                        void* stream) {
+  RS_TRY(keep_pool_memory());
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  RS_CHECK_ARG(rowoff != nullptr, "rowoff is required");
+  RS_CHECK_ARG(!upper || !idx || (rdiag && rrd), "U streams need rdiag and rrd");
+  return col_stream_build(nsys, n, upper ? 1 : 0, cp, ci, C2(cv), cap, C2(rdiag), rowoff, idx,
+                          M2(val), meta, M2(rrd), total_rows, S(stream));
+}
+
+int rs_lu_solve_cols(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t* Ls_rowoff,
+                     const int32_t* Ls_idx, const rs_complex* Ls_val, const int32_t* Ls_meta,
+                     const int32_t* Us_rowoff, const int32_t* Us_idx, const rs_complex* Us_val,
+                     const int32_t* Us_meta, const rs_complex* Us_rd, const rs_complex* b,
+                     rs_complex* x, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  if (!nsys || !n) return RS_OK;
+  SolverArgs a{};
+  a.n = n;
+  a.B = nsys;
+  a.Lso = Ls_rowoff;
+  a.Lsi = Ls_idx;
+  a.Lsv = C2(Ls_val);
+  a.Lsm = Ls_meta;
+  a.Uso = Us_rowoff;
+  a.Usi = Us_idx;
+  a.Usv = C2(Us_val);
+  a.Usm = Us_meta;
+  a.Usr = C2(Us_rd);
+  a.pinv = pinv;
+  a.rhs = C2(b);
+  a.xout = M2(x);
+  a.ring_R = col_ring_size(n, nsys);
+  if (a.ring_R <= 0) {
+    set_error("lu_solve_cols: n=%d does not fit the column sweeps", n);
+    return RS_ERR_UNSUPPORTED;
+  }
+  return launch_lu_solve(a, S(stream));
+}
+
 int rs_lu_solve(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t* L_rp,
                 const int32_t* L_ci, const rs_complex* L_v, const int32_t* U_rp,
                 const int32_t* U_ci, const rs_complex* U_v, const rs_complex* rdiag,
@@ -344,6 +404,20 @@ int rs_steady_solve(const rs_solver_args* p, void* stream) {
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   a.y_in_smem = (32 * (size_t)a.n + 4096 <= (size_t)max_smem) ? 1 : 0;
+  if (p->Ls_rowoff && p->Us_rowoff) {
+    a.Lso = p->Ls_rowoff;
+    a.Lsi = p->Ls_idx;
+    a.Lsv = C2(p->Ls_val);
+    a.Lsm = p->Ls_meta;
+    a.Uso = p->Us_rowoff;
+    a.Usi = p->Us_idx;
+    a.Usv = C2(p->Us_val);
+    a.Usm = p->Us_meta;
+    a.Usr = C2(p->Us_rd);
+    a.ring_R = col_ring_size(a.n, a.B);
+  }
+  RS_CHECK_ARG(a.ring_R > 0 || a.Lrp != nullptr || p->Ls_rowoff == nullptr,
+               "row-oriented factors required: n too large for the column sweeps");
   a.work_stride = solver_work_stride(a.n, a.restart_m);
   double2* work = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&work, sizeof(double2) * a.work_stride * a.B, st));

@@ -403,6 +403,102 @@ __device__ __forceinline__ void tri_sweep_fold(int n, const int32_t* __restrict_
   }
 }
 
+// Lane-per-row sweep over the SELL-32 factor layout (sell.cu).  Warp w takes
+// slices w, w+W, ...; lane l of slice s owns sweep position 32s+l and folds
+// its row's terms in the reference order straight from registers: the next
+// 2*G entries sit in two register groups (refilled one group at a time with
+// coalesced loads while the other is consumed), each loop iteration polls
+// every unconsumed source of the current group at once and folds the ready
+// prefix.  A row's far terms (sources finished long before) fold at G terms
+// per iteration; its last term -- the row just published -- costs one poll,
+// one complex multiply-subtract and the publishing store.  No shuffles, no
+// cross-lane fold: 32 rows advance per warp instruction.
+template <int G>
+struct SellGroup {
+  int c[G];
+  double2 l[G];
+};
+
+template <int G>
+__device__ __forceinline__ void sell_load(SellGroup<G>& g, const int32_t* __restrict__ cp,
+                                          const double2* __restrict__ vp, int k, int w) {
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    if (k + j < w) {
+      g.c[j] = __ldg(cp + 32 * (k + j));
+      g.l[j] = __ldg(vp + 32 * (k + j));
+    } else {
+      g.c[j] = -1;
+    }
+  }
+}
+
+template <bool UPPER, int G = 4>
+__device__ __forceinline__ void tri_sweep_sell(int n, const int32_t* __restrict__ sptr,
+                                               const int32_t* __restrict__ sci,
+                                               const double2* __restrict__ sv,
+                                               const double2* __restrict__ rU,
+                                               const double2* in, double2* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const int nsl = (n + 31) >> 5;
+  for (int s = wid; s < nsl; s += nw) {
+    const int q = 32 * s + lane;
+    const bool act = q < n;
+    const int r = UPPER ? n - 1 - q : q;
+    const int32_t p0 = __ldg(sptr + s);
+    const int w = (__ldg(sptr + s + 1) - p0) >> 5;
+    const int32_t* cp = sci + p0 + lane;
+    const double2* vp = sv + p0 + lane;
+    double2 acc = act ? in[r] : make_double2(0.0, 0.0);
+    const double2 rr = (UPPER && act) ? __ldg(rU + r) : make_double2(0.0, 0.0);
+    SellGroup<G> A, B;
+    sell_load<G>(A, cp, vp, 0, w);
+    sell_load<G>(B, cp, vp, G, w);
+    int k = 0, apos = 0;
+    bool pending = act;
+    if (pending && A.c[0] < 0) {  // empty row
+      vst2(out + r, UPPER ? cmul_plain(acc, rr) : acc);
+      pending = false;
+    }
+    while (__any_sync(FULL, pending)) {
+      if (pending) {
+        double2 src[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          src[j] = (j >= apos && A.c[j] >= 0) ? vld2(out + A.c[j]) : make_double2(0.0, 0.0);
+        bool stop = false;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          if (j >= apos && !stop) {
+            if (A.c[j] >= 0 && is_ready(src[j])) {
+              acc = csub(acc, cmul_plain(A.l[j], src[j]));
+              apos = j + 1;
+            } else {
+              stop = true;
+            }
+          }
+        }
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          if (j == apos) done = A.c[j] < 0;  // next term is padding: row complete
+        if (apos == G) {
+          k += G;
+          A = B;
+          sell_load<G>(B, cp, vp, k + G, w);
+          apos = 0;
+          done = A.c[0] < 0;
+        }
+        if (done) {
+          vst2(out + r, UPPER ? cmul_plain(acc, rr) : acc);
+          pending = false;
+        }
+      }
+    }
+  }
+}
+
 // Unit-lower solve: out[r] = in[r] - sum_{c<r, ascending} L[r,c] out[c]
 // (reference lower_solve, _ckernels.pyx:53-67).  out pre-filled with the
 // sentinel.

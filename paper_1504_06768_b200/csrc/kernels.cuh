@@ -20,6 +20,12 @@ int csr_transpose(int B, int32_t n, const int32_t* rp, const int32_t* ci,
                   const double2* v, int32_t* out_rp, int32_t* out_ci,
                   double2* out_v, cudaStream_t st);
 
+// ---- sell.cu: SELL-32 layout of the triangular factors -------------------
+// Pass 1 (sci == null): sptr[B*nsl+1] and *total padded entries; pass 2 fills.
+int sell_build(int B, int32_t n, int upper, const int32_t* rp, const int32_t* ci,
+               const double2* v, int32_t* sptr, int32_t* sci, double2* sv, int64_t* total,
+               cudaStream_t st);
+
 // ---- factorization (ilu.cu) -----------------------------------------------
 struct FactorArgs {
   int32_t n;

@@ -14,6 +14,8 @@
 // costs one launch.  A batch of B independent systems (config-4 sweep) is a
 // grid of B CTAs.
 #include "common.cuh"
+#include "colsweep.cuh"
+#include "kernels.cuh"
 #include "cta_ops.cuh"
 #include "solver.cuh"
 
@@ -48,6 +50,10 @@ struct Ctx {
   const int32_t *Lrp, *Lci, *Urp, *Uci, *pinv;
   const double2 *Lv, *Uv, *rU;
   bool have_M;
+  // column sweeps on the raw CSC factors (colsweep.cuh): the launch's
+  // arguments, read in place from the grid-constant parameter space
+  bool csc;
+  const SolverArgs* sa;
   // scratch
   double2* y;   // triangular-solve scratch P (smem or global)
   double2* y2;  // triangular-solve scratch Q
@@ -60,6 +66,35 @@ struct Ctx {
 // x[q] = y with q = identity on the natural/RCM path).  out may alias in.
 // Two scratch vectors P, Q (shared memory when they fit): P = permuted rhs,
 // Q = lower-solve output, then P is reused as the upper-solve output.
+// M^{-1} through the reference column loops on shared memory: one
+// out-of-line copy shared by every call site (the sweep code is large).
+// Shared memory: [y: 16 n][factor staging ring].
+__device__ __noinline__ void csc_psolve(const SolverArgs* a, const double2* in, double2* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a->n;
+  const int64_t b = blockIdx.x;
+  double2* P = reinterpret_cast<double2*>(smem);
+  const int32_t* pinv = a->pinv + b * n;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) P[pinv[i]] = in[i];
+  __syncthreads();
+  cta::ColStream Ls, Us;
+  const int32_t l0 = a->Lso[b * n], u0 = a->Uso[b * n];
+  Ls.idx = a->Lsi + 32 * (int64_t)l0;
+  Ls.val = a->Lsv + 32 * (int64_t)l0;
+  Ls.meta = a->Lsm + l0;
+  Ls.rd = nullptr;
+  Ls.rows = a->Lso[b * n + n] - l0;
+  Us.idx = a->Usi + 32 * (int64_t)u0;
+  Us.val = a->Usv + 32 * (int64_t)u0;
+  Us.meta = a->Usm + u0;
+  Us.rd = a->Usr + u0;
+  Us.rows = a->Uso[b * n + n] - u0;
+  cta::col_lu_sweeps(n, Ls, Us, cta::col_ring_at(smem + 16 * (size_t)n, a->ring_R), P);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[i];
+  __syncthreads();
+}
+
 __device__ void psolve(const Ctx& C, const double2* in, double2* out) {
   const int n = C.n;
   if (!C.have_M) {
@@ -70,6 +105,10 @@ __device__ void psolve(const Ctx& C, const double2* in, double2* out) {
   }
   double2* P = C.y;
   double2* Q = C.y2;
+  if (C.csc) {  // reference column loops on shared memory (colsweep.cuh)
+    csc_psolve(C.sa, in, out);
+    return;
+  }
   const double2 s = cta::sentinel2();
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -398,7 +437,7 @@ __device__ IterOut gmres(const Ctx& C, const double2* b, const Vecs& W, double t
 
 }  // namespace
 
-__global__ void __launch_bounds__(512) steady_solver_kernel(SolverArgs a) {
+__global__ void __launch_bounds__(512) steady_solver_kernel(const __grid_constant__ SolverArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[32 * 4];
   const int b = blockIdx.x;
@@ -411,7 +450,7 @@ __global__ void __launch_bounds__(512) steady_solver_kernel(SolverArgs a) {
   C.Arp = a.Arp + bn;  // local-offset views: rows of system b
   C.Aci = a.Aci;
   C.Av = a.Av;
-  C.have_M = a.Lrp != nullptr;
+  C.have_M = a.Lrp != nullptr || a.ring_R > 0;
   C.Lrp = a.Lrp ? a.Lrp + bn : nullptr;
   C.Lci = a.Lci;
   C.Lv = a.Lv;
@@ -422,7 +461,12 @@ __global__ void __launch_bounds__(512) steady_solver_kernel(SolverArgs a) {
   C.pinv = a.pinv ? a.pinv + bn : nullptr;
   C.red = red;
   double2* ws = a.work + (int64_t)b * a.work_stride;
-  if (a.y_in_smem) {
+  C.csc = a.ring_R > 0;
+  C.sa = &a;
+  if (C.csc) {
+    C.y = reinterpret_cast<double2*>(smem);
+    C.y2 = nullptr;
+  } else if (a.y_in_smem) {
     C.y = reinterpret_cast<double2*>(smem);
     C.y2 = C.y + n;
   } else {
@@ -595,7 +639,8 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  size_t smem = a.y_in_smem ? 32 * (size_t)a.n : 0;
+  size_t smem = a.ring_R > 0 ? 16 * (size_t)a.n + cta::col_ring_bytes(a.ring_R)
+                             : (a.y_in_smem ? 32 * (size_t)a.n : 0);
   if (smem + 2048 > (size_t)max_smem) {
     set_error("steady solver: n=%d needs %zu B of shared memory", a.n, smem);
     return RS_ERR_UNSUPPORTED;
@@ -612,7 +657,8 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
 namespace rs {
 
 // Standalone preconditioner apply (factor.solve_lu), one CTA per system.
-__global__ void __launch_bounds__(512) lu_solve_kernel(SolverArgs a, int y_in_smem) {
+__global__ void __launch_bounds__(512) lu_solve_kernel(const __grid_constant__ SolverArgs a,
+                                                      int y_in_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.x;
   const int n = a.n;
@@ -628,7 +674,12 @@ __global__ void __launch_bounds__(512) lu_solve_kernel(SolverArgs a, int y_in_sm
   C.Uv = a.Uv;
   C.rU = a.rU + bn;
   C.pinv = a.pinv + bn;
-  if (y_in_smem) {
+  C.csc = a.ring_R > 0;
+  C.sa = &a;
+  if (C.csc) {
+    C.y = reinterpret_cast<double2*>(smem);
+    C.y2 = nullptr;
+  } else if (y_in_smem) {
     C.y = reinterpret_cast<double2*>(smem);
     C.y2 = C.y + n;
   } else {
@@ -638,20 +689,136 @@ __global__ void __launch_bounds__(512) lu_solve_kernel(SolverArgs a, int y_in_sm
   psolve(C, a.rhs + bn, a.xout + bn);
 }
 
+__global__ void pivot_recip_kernel(int B, int32_t n, const int32_t* __restrict__ Up,
+                                   const double2* __restrict__ Ux, int64_t capU,
+                                   double2* __restrict__ rd) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)B * n) return;
+  const int64_t b = t / n, k = t % n;
+  rd[t] = recipc(Ux[b * capU + Up[b * (n + 1) + k + 1] - 1]);
+}
+
+int pivot_recip(int B, int32_t n, const int32_t* Up, const double2* Ux, int64_t capU,
+                double2* rd, cudaStream_t st) {
+  if (!B || !n) return RS_OK;
+  const int64_t N = (int64_t)B * n;
+  pivot_recip_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(B, n, Up, Ux, capU, rd);
+  ::rs::count_launch();
+  RS_CUDA_TRY(cudaGetLastError());
+  return RS_OK;
+}
+
+// ---- column streams (colsweep.cuh) ---------------------------------------
+__global__ void col_stream_count_kernel(int B, int32_t n, int upper, const int32_t* __restrict__ cp,
+                                        int32_t* __restrict__ rows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)B * n) return;
+  const int64_t b = t / n;
+  const int32_t j = (int32_t)(t % n);
+  const int32_t c = upper ? n - 1 - j : j;
+  const int32_t* p = cp + b * (n + 1);
+  const int32_t len = p[c + 1] - p[c] - 1;  // off-diagonal entries
+  rows[t] = len > 0 ? (len + 31) >> 5 : 1;
+}
+
+// one warp per column: coalesced copy into its padded rows
+__global__ void col_stream_fill_kernel(int B, int32_t n, int upper, const int32_t* __restrict__ cp,
+                                       const int32_t* __restrict__ ci,
+                                       const double2* __restrict__ cv, int64_t cap,
+                                       const double2* __restrict__ rdiag,
+                                       const int32_t* __restrict__ rowoff,
+                                       int32_t* __restrict__ idx, double2* __restrict__ val,
+                                       int32_t* __restrict__ meta, double2* __restrict__ rrd) {
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= (int64_t)B * n) return;
+  const int64_t b = t / n;
+  const int32_t j = (int32_t)(t % n);
+  const int32_t c = upper ? n - 1 - j : j;
+  const int32_t* p = cp + b * (n + 1);
+  const int32_t s = upper ? p[c] : p[c] + 1;
+  const int32_t len = p[c + 1] - p[c] - 1;
+  const int32_t r0 = rowoff[t], nr = rowoff[t + 1] - r0;
+  const int32_t* I = ci + b * cap;
+  const double2* X = cv + b * cap;
+  for (int32_t k = lane; k < 32 * nr; k += 32) {
+    const int64_t o = 32 * (int64_t)r0 + k;
+    if (k < len) {
+      idx[o] = I[s + k];
+      val[o] = X[s + k];
+    } else {
+      idx[o] = -1;
+      val[o] = make_double2(0.0, 0.0);
+    }
+  }
+  for (int32_t q = lane; q < nr; q += 32) {
+    meta[r0 + q] = q > 0 ? 1 : 0;
+    if (upper) rrd[r0 + q] = q == 0 ? rdiag[b * n + c] : make_double2(0.0, 0.0);
+  }
+}
+
+int col_stream_build(int B, int32_t n, int upper, const int32_t* cp, const int32_t* ci,
+                     const double2* cv, int64_t cap, const double2* rdiag, int32_t* rowoff,
+                     int32_t* idx, double2* val, int32_t* meta, double2* rrd, int64_t* total,
+                     cudaStream_t st) {
+  const int64_t N = (int64_t)B * n;
+  if (!idx) {
+    int32_t* rows = nullptr;
+    RS_CUDA_TRY(cudaMallocAsync(&rows, sizeof(int32_t) * (N + 1), st));
+    if (N > 0) {
+      col_stream_count_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(B, n, upper, cp, rows);
+      ::rs::count_launch();
+      RS_CUDA_TRY(cudaGetLastError());
+    }
+    int64_t tot = 0;
+    const int rc = scan_counts(rows, rowoff, N, &tot, st);
+    cudaFreeAsync(rows, st);
+    if (rc) return rc;
+    if (tot < 0 || tot >= ((int64_t)1 << 26)) {
+      set_error("col_stream_build: %lld rows exceed 32-bit entry indexing", (long long)tot);
+      return RS_ERR_OVERFLOW;
+    }
+    if (total) *total = tot;
+    return RS_OK;
+  }
+  if (N > 0) {
+    col_stream_fill_kernel<<<(unsigned)((N * 32 + 255) / 256), 256, 0, st>>>(
+        B, n, upper, cp, ci, cv, cap, rdiag, rowoff, idx, val, meta, rrd);
+    ::rs::count_launch();
+    RS_CUDA_TRY(cudaGetLastError());
+  }
+  return RS_OK;
+}
+
+int col_ring_size(int32_t n, int B) {
+  int dev = 0, max_smem = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) !=
+      cudaSuccess)
+    return 0;
+  // batches keep four CTAs per SM resident: a 32-slot ring (21 KB); a lone
+  // system takes a deeper ring
+  for (int S = (B > 148 ? 32 : 128); S >= 8; S >>= 1)
+    if (16 * (size_t)n + cta::col_ring_bytes(S) + 4096 <= (size_t)max_smem) return S;
+  return 0;
+}
+
 int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
   if (a.B == 0 || a.n == 0) return RS_OK;
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int y_smem = 32 * (size_t)a.n + 2048 <= (size_t)max_smem;
-  size_t smem = y_smem ? 32 * (size_t)a.n : 0;
-  if (!y_smem && !a.work) {
+  size_t smem = a.ring_R > 0 ? 16 * (size_t)a.n + cta::col_ring_bytes(a.ring_R)
+                             : (y_smem ? 32 * (size_t)a.n : 0);
+  if (a.ring_R <= 0 && !y_smem && !a.work) {
     set_error("lu_solve: n=%d needs global scratch", a.n);
     return RS_ERR_UNSUPPORTED;
   }
   RS_CUDA_TRY(cudaFuncSetAttribute(lu_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-  lu_solve_kernel<<<a.B, 512, smem, st>>>(a, y_smem); ::rs::count_launch();
+  // column sweeps: 1 consumer + 4 producer warps; row sweeps: 16 warps
+  lu_solve_kernel<<<a.B, a.ring_R > 0 ? 160 : 512, smem, st>>>(a, y_smem); ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -686,11 +853,45 @@ __global__ void __launch_bounds__(1024) tri_probe_kernel(int n, const int32_t* r
     for (int i = threadIdx.x; i < n; i += blockDim.x) gout[i] = out[i];
 }
 
+// SELL lane-per-row sweep in isolation (rp/ci/v = sptr/sci/sv of one system)
+template <int G>
+__global__ void __launch_bounds__(512) sell_probe_kernel(int n, const int32_t* sptr,
+                                                         const int32_t* sci, const double2* sv,
+                                                         const double2* rU, const double2* in,
+                                                         double2* gout, int which,
+                                                         int smem_buf) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double2* out = smem_buf ? reinterpret_cast<double2*>(smem) : gout;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = cta::sentinel2();
+  __syncthreads();
+  if (which == 0) cta::tri_sweep_sell<false, G>(n, sptr, sci, sv, rU, in, out);
+  else cta::tri_sweep_sell<true, G>(n, sptr, sci, sv, rU, in, out);
+  __syncthreads();
+  if (smem_buf)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) gout[i] = out[i];
+}
+
 }  // namespace rs
 
 extern "C" int rs_debug_tri_probe(int n, const int32_t* rp, const int32_t* ci, const void* v,
                                   const void* rU, const void* in, void* out, int which,
                                   int variant, int smem_buf, int threads, void* stream) {
+  if (variant >= 3) {  // 3: SELL G=4, 4: SELL G=2, 5: SELL G=8
+    const size_t sm = smem_buf ? 16 * (size_t)n : 0;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto go = [&](auto kern) -> int {
+      RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      kern<<<1, threads, sm, s>>>(n, rp, ci, reinterpret_cast<const double2*>(v),
+                                  reinterpret_cast<const double2*>(rU),
+                                  reinterpret_cast<const double2*>(in),
+                                  reinterpret_cast<double2*>(out), which, smem_buf);
+      RS_CUDA_TRY(cudaGetLastError());
+      return 0;
+    };
+    if (variant == 3) return go(rs::sell_probe_kernel<4>);
+    if (variant == 4) return go(rs::sell_probe_kernel<2>);
+    return go(rs::sell_probe_kernel<8>);
+  }
   const size_t smem = (smem_buf ? 16 * (size_t)n : 0) + sizeof(rs::cta::FoldBuf) * 32;
   RS_CUDA_TRY(cudaFuncSetAttribute(rs::tri_probe_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

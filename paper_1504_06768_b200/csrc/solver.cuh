@@ -68,7 +68,30 @@ struct SolverArgs {
   int32_t max_outer;
   int32_t want_condest;
   int32_t y_in_smem;
+  // column streams for the column-oriented sweeps (colsweep.cuh)
+  const int32_t* Lso;
+  const int32_t* Lsi;
+  const double2* Lsv;
+  const int32_t* Lsm;
+  const int32_t* Uso;
+  const int32_t* Usi;
+  const double2* Usv;
+  const int32_t* Usm;
+  const double2* Usr;
+  int32_t ring_R;  // > 0: column sweeps with a ring of ring_R 32-entry slots
 };
+
+// Ring size for the column sweeps of systems of order n in a launch of B
+// CTAs (0 = not supported: the sweep vector and ring do not fit).
+int col_ring_size(int32_t n, int B);
+// column streams of one triangle (pass 1: idx == null -> rowoff + *total)
+int col_stream_build(int B, int32_t n, int upper, const int32_t* cp, const int32_t* ci,
+                     const double2* cv, int64_t cap, const double2* rdiag, int32_t* rowoff,
+                     int32_t* idx, double2* val, int32_t* meta, double2* rrd, int64_t* total,
+                     cudaStream_t st);
+// rd[b*n+k] = recipc(last entry of U column k) from the raw CSC factor
+int pivot_recip(int B, int32_t n, const int32_t* Up, const double2* Ux, int64_t capU,
+                double2* rd, cudaStream_t st);
 
 int64_t solver_work_stride(int32_t n, int restart_m);
 int launch_steady_solver(const SolverArgs& a, cudaStream_t st);

@@ -4,8 +4,10 @@ Drop-in for the reference factor module (pkg/src/rhosolve/factor.py):
 `lu`, `ilutp`, `solve_lu`, `condest`, `LUFactors`, `SingularMatrixError`,
 `PreconditionerBreakdownError`, same argument checks and messages.  The
 factorization itself is the column-pipelined kernel in csrc/ilu.cu, the apply
-the row-oriented triangular solves in csrc/cta_ops.cuh; both are
-bit-identical to the reference kernels.
+the reference's own column-oriented triangular solves run on shared memory
+(csrc/colsweep.cuh; row-oriented sweeps in csrc/cta_ops.cuh for systems too
+large for one CTA's shared memory); all are bit-identical to the reference
+kernels.
 """
 
 from __future__ import annotations
@@ -43,7 +45,13 @@ class LUFactors:
 
     __slots__ = ("n", "nsys", "raw", "capL", "capU", "pinv", "L_rp", "L_ci", "L_v", "U_rp",
                  "U_ci", "U_v", "rdiag", "fill_factors", "complete", "drop_tol",
-                 "fill_limit", "fail", "lnnz", "unnz")
+                 "fill_limit", "fail", "lnnz", "unnz", "ok", "csc", "Ls", "Us")
+
+    def ensure_rows(self):
+        """Build the row-oriented factor copy (row sweeps, exports) once."""
+        if self.L_rp is None and self.ok:
+            _build_rows(self, self.pinv.device)
+        return self
 
     @property
     def fill_factor(self):
@@ -146,11 +154,43 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
     f.drop_tol = float(drop_tol) if incomplete else None
     f.fill_limit = float(fill_limit) if incomplete else None
     f.fail = fail
-    if np.all(fail < 0):
-        _build_rows(f, dev)
-    else:
-        f.L_rp = None
+    f.ok = bool(np.all(fail < 0))
+    f.L_rp = f.L_ci = f.L_v = f.U_rp = f.U_ci = f.U_v = None
+    f.rdiag = None
+    # the preconditioner apply consumes the raw CSC factors directly (the
+    # reference's column loops) whenever the sweep vector fits shared memory;
+    # larger systems use the row-oriented copy
+    f.csc = bool(_lib.load().rs_col_sweep_supported(n))
+    f.Ls = f.Us = None
+    if f.ok:
+        f.rdiag = torch.empty(B * n, dtype=torch.complex128, device=dev)
+        _lib.call("rs_pivot_recip", B, n, _lib.ptr(Up), _lib.ptr(Ux), capU,
+                  _lib.ptr(f.rdiag), st)
+        if f.csc:
+            f.Ls = _col_stream(B, n, 0, Lp, Li, Lx, capL, None, dev)
+            f.Us = _col_stream(B, n, 1, Up, Ui, Ux, capU, f.rdiag, dev)
+        else:
+            _build_rows(f, dev)
     return f
+
+
+def _col_stream(B, n, upper, cp, ci, cv, cap, rdiag, dev):
+    """Column stream of one triangle (csrc/colsweep.cuh): (rowoff, idx, val,
+    meta, rrd)."""
+    rowoff = torch.empty(B * n + 1, dtype=torch.int32, device=dev)
+    rows = ctypes.c_int64(0)
+    st = _lib.stream_ptr()
+    _lib.call("rs_col_stream_build", B, n, upper, _lib.ptr(cp), _lib.ptr(ci), _lib.ptr(cv), cap,
+              _lib.ptr(rdiag), _lib.ptr(rowoff), None, None, None, None, ctypes.byref(rows), st)
+    R = max(rows.value, 1)
+    idx = torch.empty(32 * R, dtype=torch.int32, device=dev)
+    val = torch.empty(32 * R, dtype=torch.complex128, device=dev)
+    meta = torch.empty(R, dtype=torch.int32, device=dev)
+    rrd = torch.empty(R, dtype=torch.complex128, device=dev) if upper else None
+    _lib.call("rs_col_stream_build", B, n, upper, _lib.ptr(cp), _lib.ptr(ci), _lib.ptr(cv), cap,
+              _lib.ptr(rdiag), _lib.ptr(rowoff), _lib.ptr(idx), _lib.ptr(val), _lib.ptr(meta),
+              _lib.ptr(rrd), ctypes.byref(rows), st)
+    return rowoff, idx, val, meta, rrd
 
 
 def _regrow(t, B, old, new):
@@ -175,9 +215,10 @@ def _build_rows(f, dev):
     f.L_v = torch.empty(max(ln.value, 1), dtype=torch.complex128, device=dev)
     f.U_ci = torch.empty(max(un.value, 1), dtype=torch.int32, device=dev)
     f.U_v = torch.empty(max(un.value, 1), dtype=torch.complex128, device=dev)
-    f.rdiag = torch.empty(B * n, dtype=torch.complex128, device=dev)
+    rd = torch.empty(B * n, dtype=torch.complex128, device=dev)
     _lib.call("rs_factor_rows", *args(_lib.ptr(f.L_ci), _lib.ptr(f.L_v), _lib.ptr(f.U_ci),
-                                      _lib.ptr(f.U_v), _lib.ptr(f.rdiag)))
+                                      _lib.ptr(f.U_v), _lib.ptr(rd)))
+    f.rdiag = rd
 
 
 def _mat(a):
@@ -210,6 +251,13 @@ def ilutp(a, d=1e-4, p=300.0, col_perm=None):
 def solve_lu_device(f, b):
     """x = M^{-1} b on the device for every system (b: nsys*n complex128)."""
     x = torch.empty_like(b)
+    if f.csc:
+        (lo, li, lv, lm, _), (uo, ui, uv, um, ur) = f.Ls, f.Us
+        _lib.call("rs_lu_solve_cols", f.nsys, f.n, _lib.ptr(f.pinv), _lib.ptr(lo), _lib.ptr(li),
+                  _lib.ptr(lv), _lib.ptr(lm), _lib.ptr(uo), _lib.ptr(ui), _lib.ptr(uv),
+                  _lib.ptr(um), _lib.ptr(ur), _lib.ptr(b), _lib.ptr(x), _lib.stream_ptr())
+        return x
+    f.ensure_rows()
     _lib.call("rs_lu_solve", f.nsys, f.n, _lib.ptr(f.pinv), _lib.ptr(f.L_rp), _lib.ptr(f.L_ci),
               _lib.ptr(f.L_v), _lib.ptr(f.U_rp), _lib.ptr(f.U_ci), _lib.ptr(f.U_v),
               _lib.ptr(f.rdiag), _lib.ptr(b), _lib.ptr(x), _lib.stream_ptr())

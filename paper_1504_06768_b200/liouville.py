@@ -14,10 +14,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from .sparse import DeviceCSR, as_host_csr
+from .sparse import DeviceCSR, as_host_csr, from_host
 
 __all__ = ["LiouvillianSystem", "build_liouvillian", "build_liouvillian_batch", "shift",
-           "build_modified", "default_weight", "DEFAULT_SIGMA", "concat_systems"]
+           "build_modified", "default_weight", "DEFAULT_SIGMA", "concat_systems", "on_device"]
 
 DEFAULT_SIGMA = 1e-15
 _HERM_TOL = 1e-12
@@ -54,6 +54,16 @@ class LiouvillianSystem:
     def __repr__(self):
         return (f"LiouvillianSystem(D={self.hilbert_dim}, variant={self.variant!r}, "
                 f"nsys={self.nsys}, nnz={self.matrix.nnz})")
+
+
+def on_device(L, device=None):
+    """L with its matrix resident on the GPU: a host CSRMatrix, a list-built
+    batch or a PinnedBatchCSR is uploaded (pinned batches asynchronously on
+    the current stream); a DeviceCSR passes through unchanged."""
+    if isinstance(L.matrix, DeviceCSR):
+        return L
+    return LiouvillianSystem(from_host(L.matrix, device), L.hilbert_dim, L.variant,
+                             sigma=L.sigma, weight=L.weight, rhs=L.rhs)
 
 
 def _dev_op(m, dev):

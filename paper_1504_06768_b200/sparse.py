@@ -22,8 +22,9 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-__all__ = ["CSRMatrix", "Permutation", "DeviceCSR", "identity", "kron", "transpose",
-           "conjugate", "adjoint", "add", "matmul", "from_host", "as_host_csr"]
+__all__ = ["CSRMatrix", "Permutation", "DeviceCSR", "PinnedBatchCSR", "identity", "kron",
+           "transpose", "conjugate", "adjoint", "add", "matmul", "from_host", "pin_batch",
+           "as_host_csr"]
 
 
 class CSRMatrix:
@@ -230,10 +231,28 @@ class DeviceCSR:
         return f"DeviceCSR(n={self.n}, nsys={self.nsys}, nnz={self.nnz})"
 
 
-def from_host(mats, device=None):
-    """Upload one CSR (or a list of equal-order CSRs as a batch) to the GPU."""
-    if not isinstance(mats, (list, tuple)):
-        mats = [mats]
+class PinnedBatchCSR:
+    """A block-diagonal batch of equal-order CSR matrices staged in pinned
+    (page-locked) host memory in the DeviceCSR layout (int32 row_ptr over
+    nsys*n rows, int32 local column indices, complex128 values), so that
+    `from_host` moves it with three asynchronous DMA copies."""
+
+    __slots__ = ("n", "nsys", "row_ptr", "col_idx", "values")
+
+    def __init__(self, n, nsys, row_ptr, col_idx, values):
+        self.n, self.nsys = int(n), int(nsys)
+        self.row_ptr, self.col_idx, self.values = row_ptr, col_idx, values
+
+    @property
+    def nnz(self):
+        return int(self.values.numel())
+
+    @property
+    def nbytes(self):
+        return 4 * self.row_ptr.numel() + 4 * self.col_idx.numel() + 16 * self.values.numel()
+
+
+def _pack(mats):
     mats = [as_host_csr(m) for m in mats]
     n = mats[0].nrows
     if any(m.nrows != n or m.ncols != n for m in mats):
@@ -241,8 +260,39 @@ def from_host(mats, device=None):
     offs = np.cumsum([0] + [m.nnz for m in mats])
     if offs[-1] >= 2 ** 31:
         raise ValueError("nnz exceeds int32 indexing")
-    rp = np.concatenate([m.row_ptr[:-1] + o for m, o in zip(mats, offs[:-1])] + [[offs[-1]]])
+    return mats, n, offs
+
+
+def pin_batch(mats):
+    """Pack host CSRs (one, or a list of equal order) into a PinnedBatchCSR."""
+    if not isinstance(mats, (list, tuple)):
+        mats = [mats]
+    mats, n, offs = _pack(mats)
+    B, nnz = len(mats), int(offs[-1])
+    rp = torch.empty(B * n + 1, dtype=torch.int32, pin_memory=True)
+    ci = torch.empty(nnz, dtype=torch.int32, pin_memory=True)
+    v = torch.empty(nnz, dtype=torch.complex128, pin_memory=True)
+    rpn, cin, vn = rp.numpy(), ci.numpy(), v.numpy()
+    for b, (m, o) in enumerate(zip(mats, offs[:-1])):
+        rpn[b * n:(b + 1) * n] = m.row_ptr[:-1] + o
+        cin[o:o + m.nnz] = m.col_idx
+        vn[o:o + m.nnz] = m.values
+    rpn[B * n] = nnz
+    return PinnedBatchCSR(n, B, rp, ci, v)
+
+
+def from_host(mats, device=None):
+    """Upload one CSR, a list of equal-order CSRs (as a batch), or a
+    PinnedBatchCSR (asynchronous copies on the current stream) to the GPU."""
     dev = device or torch.device("cuda")
+    if isinstance(mats, PinnedBatchCSR):
+        return DeviceCSR(mats.n, mats.nsys, mats.row_ptr.to(dev, non_blocking=True),
+                         mats.col_idx.to(dev, non_blocking=True),
+                         mats.values.to(dev, non_blocking=True))
+    if not isinstance(mats, (list, tuple)):
+        mats = [mats]
+    mats, n, offs = _pack(mats)
+    rp = np.concatenate([m.row_ptr[:-1] + o for m, o in zip(mats, offs[:-1])] + [[offs[-1]]])
     return DeviceCSR(
         n, len(mats),
         torch.from_numpy(rp.astype(np.int32)).to(dev),

@@ -94,6 +94,7 @@ def _start_vectors(n, seeds):
 def _require_plain(L):
     if L.variant != "plain":
         raise ValueError(f"expected the plain variant, got {L.variant!r}")
+    return liouville.on_device(L)
 
 
 def _prepare(system, ordering_name, plain=None):
@@ -132,8 +133,16 @@ def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0
     if P is not None:
         a.P_rp, a.P_ci, a.P_v = P.row_ptr.data_ptr(), P.col_idx.data_ptr(), P.values.data_ptr()
     if f is not None:
-        a.L_rp, a.L_ci, a.L_v = f.L_rp.data_ptr(), f.L_ci.data_ptr(), f.L_v.data_ptr()
-        a.U_rp, a.U_ci, a.U_v = f.U_rp.data_ptr(), f.U_ci.data_ptr(), f.U_v.data_ptr()
+        if f.csc:  # column streams, reference column sweeps on shared memory
+            (lo, li, lv, lm, _), (uo, ui, uv, um, ur) = f.Ls, f.Us
+            a.Ls_rowoff, a.Ls_idx, a.Ls_val, a.Ls_meta = (_lib.ptr(lo), _lib.ptr(li),
+                                                          _lib.ptr(lv), _lib.ptr(lm))
+            a.Us_rowoff, a.Us_idx, a.Us_val, a.Us_meta, a.Us_rd = (
+                _lib.ptr(uo), _lib.ptr(ui), _lib.ptr(uv), _lib.ptr(um), _lib.ptr(ur))
+        else:
+            f.ensure_rows()
+            a.L_rp, a.L_ci, a.L_v = f.L_rp.data_ptr(), f.L_ci.data_ptr(), f.L_v.data_ptr()
+            a.U_rp, a.U_ci, a.U_v = f.U_rp.data_ptr(), f.U_ci.data_ptr(), f.U_v.data_ptr()
         a.rdiag, a.pinv = f.rdiag.data_ptr(), f.pinv.data_ptr()
     a.rhs, a.x, a.stats = rhs.data_ptr(), x.data_ptr(), stats.data_ptr()
     a.tol, a.max_iter, a.restart_m = float(tol), int(max_iter), int(restart_m)
@@ -153,7 +162,14 @@ def _postprocess(x, fwd, L):
     _lib.call("rs_postprocess", M.nsys, D, _lib.ptr(x), _lib.ptr(fwd), _lib.ptr(M.row_ptr),
               _lib.ptr(M.col_idx), _lib.ptr(M.values), _lib.ptr(rho), _lib.ptr(res), None,
               _lib.stream_ptr())
-    return rho.reshape(M.nsys, D, D).cpu().numpy(), res.cpu().numpy()
+    # one D2H into pinned host memory (torch caches pinned blocks)
+    out = torch.empty(rho.numel() + M.nsys * 2, dtype=torch.complex128, pin_memory=True)
+    out[:rho.numel()].copy_(rho, non_blocking=True)
+    out[rho.numel():].view(torch.float64)[:M.nsys].copy_(res, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    on = out.numpy()
+    return (on[:rho.numel()].reshape(M.nsys, D, D).copy(),
+            on[rho.numel():].view(np.float64)[:M.nsys].copy())
 
 
 def _check_ops(tol=None, max_iter=None, restart_m=None):
@@ -169,7 +185,7 @@ def _check_ops(tol=None, max_iter=None, restart_m=None):
 def solve_direct(L, ordering_name="natural", w=None):
     """Steady state by one complete-LU solve of the trace-modified system
     (steady.py:116-134)."""
-    _require_plain(L)
+    L = _require_plain(L)
     t0 = _sync()
     modified = liouville.build_modified(L, w)
     mat, rhs, _, fwd, label = _prepare(modified, ordering_name)
@@ -188,7 +204,7 @@ def solve_iterative(L, ordering_name="natural", solver="gmres", d=1e-4, p=300.0,
                     restart_m=20, max_iter=1000, w=None):
     """Preconditioned Krylov on the trace-modified system (steady.py:137-168).
     Non-convergence and solver breakdown are reported, not raised."""
-    _require_plain(L)
+    L = _require_plain(L)
     if solver not in ("gmres", "bicgstab"):
         raise ValueError(f"unknown solver {solver!r}")
     _check_ops(tol, max_iter, restart_m)
@@ -225,7 +241,7 @@ _STATUS_MSG = {
 
 def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, max_iter, seeds,
                 raise_errors, threads=0):
-    _require_plain(L)
+    L = _require_plain(L)
     if inner not in ("direct", "iterative"):
         raise ValueError(f"unknown inner solve {inner!r}")
     if not tol > 0:
@@ -254,7 +270,7 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
         mode = _lib.INV_GMRES if solver == "gmres" else _lib.INV_BICGSTAB
     t2 = _sync()
     x0 = torch.from_numpy(x0_future.result()).to(mat.values.device)
-    if f.L_rp is None:  # some system of the batch failed to factor
+    if not f.ok:  # some system of the batch failed to factor
         return None, f, None, None, label, (t0, t1, t2, _sync())
     x, st = _solve(mode, mat, plain, f, x0, tol, max_iter, restart_m, inner == "iterative",
                    threads)
@@ -324,7 +340,7 @@ def inverse_power_batch(L, seeds, sigma=DEFAULT_SIGMA, tol=1e-14, inner="direct"
 def solve_batch(L, method="bicgstab", ordering_name="natural", d=1e-4, p=300.0, tol=1e-14,
                 restart_m=20, max_iter=1000, w=None, threads=0):
     """solve_iterative / solve_direct (method="direct") over a batch."""
-    _require_plain(L)
+    L = _require_plain(L)
     t0 = _sync()
     modified = liouville.build_modified(L, w)
     mat, rhs, _, fwd, label = _prepare(modified, ordering_name)

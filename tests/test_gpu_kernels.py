@@ -63,6 +63,59 @@ def test_spmv_bit_exact(cuda, name, kw):
     assert bits_equal(y.cpu().numpy(), O.csr_matvec(Lo, x))
 
 
+def _rand_csr(rng, n, density, long_rows=(), empty_rows=()):
+    """Random n x n CSR with sorted columns; some rows forced long / empty."""
+    rows = []
+    for r in range(n):
+        if r in empty_rows:
+            cols = np.empty(0, dtype=np.int64)
+        elif r in long_rows:
+            cols = np.arange(n, dtype=np.int64)
+        else:
+            cols = np.flatnonzero(rng.random(n) < density)
+        rows.append(cols)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[1:] = np.cumsum([len(c) for c in rows])
+    ci = np.concatenate(rows) if rp[-1] else np.empty(0, dtype=np.int64)
+    v = rng.standard_normal(len(ci)) + 1j * rng.standard_normal(len(ci))
+    return O.CSR(n, n, rp, ci, v)
+
+
+@pytest.mark.parametrize("n,nsys,density,long_rows,empty_rows", [
+    (7, 300, 0.4, (), (3,)),           # many systems inside one CTA
+    (6000, 1, 0.0015, (17, 4000), (0, 5, 5999)),  # rows longer than a staging chunk
+    (1600, 5, 0.005, (1599,), (0,)),   # CTAs straddling system boundaries
+    (1, 3, 1.0, (), ()),
+])
+def test_spmv_random_batches_bit_exact(cuda, n, nsys, density, long_rows, empty_rows):
+    rng = np.random.default_rng(n + nsys)
+    mats = [_rand_csr(rng, n, density, long_rows, empty_rows) for _ in range(nsys)]
+    A = from_host([_host(m) for m in mats])
+    x = rng.standard_normal(n * nsys) + 1j * rng.standard_normal(n * nsys)
+    y = torch.empty(n * nsys, dtype=torch.complex128, device="cuda")
+    xd = torch.from_numpy(x).cuda()
+    _lib.call("rs_csr_matvec", nsys, n, _lib.ptr(A.row_ptr), _lib.ptr(A.col_idx),
+              _lib.ptr(A.values), _lib.ptr(xd), _lib.ptr(y), _lib.stream_ptr())
+    ref = np.concatenate([O.csr_matvec(m, x[b * n:(b + 1) * n]) for b, m in enumerate(mats)])
+    assert bits_equal(y.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("name,kw", SMALL)
+def test_spmv_modified_bit_exact(cuda, name, kw):
+    H, c = model(name, **kw)
+    Lo = oracle_L(H, c)
+    mo, _, _ = O.build_modified(Lo, H.matrix.nrows, O.default_weight(Lo))
+    fwd, _ = O.rcm(mo)
+    m = O.permute(mo, fwd)
+    x = np.random.default_rng(9).standard_normal(m.n) + 1j * np.random.default_rng(10).standard_normal(m.n)
+    A = from_host(_host(m))
+    y = torch.empty(m.n, dtype=torch.complex128, device="cuda")
+    _lib.call("rs_csr_matvec", 1, A.n, _lib.ptr(A.row_ptr), _lib.ptr(A.col_idx),
+              _lib.ptr(A.values), _lib.ptr(torch.from_numpy(x).cuda()), _lib.ptr(y),
+              _lib.stream_ptr())
+    assert bits_equal(y.cpu().numpy(), O.csr_matvec(m, x))
+
+
 FACTOR_CASES = [("c1", {}, 1e-5, 10.0), ("c1", {}, 0.0, math.inf), ("c1", {}, 1e-4, 300.0),
                 ("c4", {"i": 0}, 0.0, math.inf), ("c2", {}, 1e-4, 300.0)]
 
