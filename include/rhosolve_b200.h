@@ -121,8 +121,8 @@ int rs_col_sweep_supported(int32_t n);
 
 /* Column stream of one triangle of the raw CSC factors (rs_factorize) for
  * the column-oriented sweeps: columns in sweep order j (L: column j; U:
- * column n-1-j), each column's off-diagonal entries padded to whole 32-entry
- * rows (index -1 = padding); meta[row] = 1 when the row continues the
+ * column n-1-j), each column's off-diagonal entries padded to whole 64-entry
+ * rows (index -1 = padding; idx/val hold 64 * rows entries); meta[row] = 1 when the row continues the
  * previous column; for U, rrd[first row of column c] = rdiag[c].  rowoff
  * (nsys*n+1, absolute) gives each column's first row.  Call with idx ==
  * NULL to fill rowoff and *total_rows (host), then again to fill. */

@@ -18,7 +18,7 @@
 // consumer's per-column work is cut to the minimum by a precomputed COLUMN
 // STREAM (built once per factorization, sell.cu col_stream_build): the
 // columns in sweep order (L ascending, U descending), each padded to whole
-// 32-entry rows (row index -1 = padding), every row tagged "continues the
+// 64-entry rows (row index -1 = padding), every row tagged "continues the
 // previous column" or not, and U's first rows carrying recipc(U_cc).
 // PRODUCER warps copy stream rows into a shared-memory ring (coalesced, four
 // rows in flight per warp); the consumer reads one ring row per step, with
@@ -35,26 +35,33 @@
 namespace rs {
 namespace cta {
 
+// Stream row width: two entries per lane, so the typical banded column
+// (~50-70 off-diagonal entries) is one or two consumer steps.
+constexpr int CW = 64;
+
 // One triangle's column stream for one system.
 struct ColStream {
-  const int32_t* idx;   // [rows * 32], -1 = padding
-  const double2* val;   // [rows * 32]
+  const int32_t* idx;   // [rows * CW], -1 = padding
+  const double2* val;   // [rows * CW]
   const int32_t* meta;  // [rows]: 1 = continues the previous column
   const double2* rd;    // [rows]: recipc(U_cc) on U's first rows (U only)
   int rows;
 };
 
 struct ColRing {
-  int32_t* idx;  // [S * 32]
-  double2* val;  // [S * 32]
+  int32_t* idx;  // [S * CW]
+  double2* val;  // [S * CW]
   double2* rd;   // [S]
   int* seq;      // [S]: (stream row << 1) | continuation, -1 = empty
   int* head;     // consumer progress (rows fully consumed)
   int S;         // slots (power of two)
 };
 
+// shared bytes of the sweep vector: y[0..n-1] plus one dummy slot
+__host__ __device__ inline size_t col_y_bytes(int n) { return 16 * ((size_t)n + 1); }
+
 __host__ __device__ inline size_t col_ring_bytes(int S) {
-  return (size_t)S * 32 * (sizeof(int32_t) + sizeof(double2)) + (size_t)S * sizeof(double2) +
+  return (size_t)S * CW * (sizeof(int32_t) + sizeof(double2)) + (size_t)S * sizeof(double2) +
          sizeof(int) * ((size_t)S + 4);
 }
 
@@ -62,9 +69,9 @@ __host__ __device__ inline size_t col_ring_bytes(int S) {
 __device__ __forceinline__ ColRing col_ring_at(unsigned char* p, int S) {
   ColRing g;
   g.val = reinterpret_cast<double2*>(p);
-  g.rd = g.val + 32 * S;
+  g.rd = g.val + CW * S;
   g.idx = reinterpret_cast<int32_t*>(g.rd + S);
-  g.seq = g.idx + 32 * S;
+  g.seq = g.idx + CW * S;
   g.head = g.seq + S;
   g.S = S;
   return g;
@@ -108,90 +115,193 @@ __device__ __forceinline__ void col_ring_reset(const ColRing& g) {
   if (threadIdx.x == 0) *g.head = 0;
 }
 
-// Producer warp pw of P: rows pw, pw + P, ... of the stream into the ring,
-// four rows' loads in flight before the first store.
+// cp.async helpers (16-byte global -> shared copies that bypass registers)
+__device__ __forceinline__ void cp16(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Producer warp pw of P: batches of PB consecutive rows (batch k = pw, pw+P,
+// ...) copied into the ring with cp.async (no registers held: two batches
+// in flight per warp), each batch published once it has landed.
+constexpr int PB = 4;
+
 __device__ __forceinline__ void col_ring_produce(const ColRing& g, const ColStream& cs,
                                                  bool upper, int pw, int P) {
-  constexpr int U = 4;
   const int lane = threadIdx.x & 31;
-  for (int r0 = pw; r0 < cs.rows; r0 += U * P) {
-    int ci[U], mt[U];
-    double2 cv[U], rd[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = r0 + u * P;
-      if (r < cs.rows) {
-        ci[u] = __ldg(cs.idx + 32 * (int64_t)r + lane);
-        cv[u] = __ldg(cs.val + 32 * (int64_t)r + lane);
-        mt[u] = __ldg(cs.meta + r);
-        if (upper) rd[u] = __ldg(cs.rd + r);
-      }
+  const int nb = (cs.rows + PB - 1) / PB;
+  const unsigned sidx = saddr(g.idx), sval = saddr(g.val), srd = saddr(g.rd);
+  int pend = -1;       // batch issued but not yet published
+  int pend_meta = 0;   // lane j < PB: meta of row j of the pending batch
+  auto publish = [&]() {
+    __syncwarp();
+    __threadfence_block();
+    const int r0 = pend * PB;
+    if (lane < min(PB, cs.rows - r0)) {
+      const int r = r0 + lane;
+      st_rlx(g.seq + (r & (g.S - 1)), (r << 1) | (pend_meta & 1));
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = r0 + u * P;
-      if (r >= cs.rows) break;
-      // slot r % S last held row r - S: wait until it is consumed
-      if (r >= g.S) {
+    pend = -1;
+  };
+  for (int k = pw; k < nb; k += P) {
+    const int r0 = k * PB;
+    const int cnt = min(PB, cs.rows - r0);
+    const int meta = lane < cnt ? __ldg(cs.meta + r0 + lane) : 0;
+    // space: slots of rows r0 .. r0+cnt-1 last held rows - S.  Never block
+    // while holding an unpublished batch (the consumer may need it first).
+    const int need = r0 + cnt - g.S;
+    if (need > 0) {
+      int h = 0;
+      if (lane == 0) h = ld_rlx(g.head);
+      h = __shfl_sync(FULL, h, 0);
+      if (h < need) {
+        if (pend >= 0) {
+          cp_wait<0>();
+          publish();
+        }
         if (lane == 0)
-          while (ld_rlx(g.head) <= r - g.S) __nanosleep(20);
+          while (ld_rlx(g.head) < need) __nanosleep(20);
         __syncwarp();
       }
-      const int slot = r & (g.S - 1);
-      g.idx[32 * slot + lane] = ci[u];
-      g.val[32 * slot + lane] = cv[u];
-      if (upper && lane == 0) g.rd[slot] = rd[u];
-      __syncwarp();
-      if (lane == 0) st_rel(g.seq + slot, (r << 1) | (mt[u] & 1));
     }
+    for (int j = 0; j < cnt; ++j) {
+      const int r = r0 + j;
+      const int slot = r & (g.S - 1);
+      // idx row: 256 B = 16 x 16 B; val row: 1 KB = 64 x 16 B
+      if (lane < 16)
+        cp16(sidx + (unsigned)(CW * 4 * slot + 16 * lane), cs.idx + CW * (int64_t)r + 4 * lane);
+      cp16(sval + (unsigned)(CW * 16 * slot + 16 * lane), cs.val + CW * (int64_t)r + lane);
+      cp16(sval + (unsigned)(CW * 16 * slot + 16 * (lane + 32)),
+           cs.val + CW * (int64_t)r + lane + 32);
+      if (upper && lane == 0) cp16(srd + 16u * slot, cs.rd + r);
+    }
+    cp_commit();
+    if (pend >= 0) {  // the previous batch has had a batch's time to land
+      cp_wait<1>();
+      publish();
+    }
+    pend = k;
+    pend_meta = meta;
+  }
+  if (pend >= 0) {
+    cp_wait<0>();
+    publish();
   }
 }
 
 // One staged stream row in registers.
 struct ColRow {
-  int i;       // this lane's row index (-1 = padding)
-  double2 v;   // this lane's factor entry
-  double2 rd;  // recipc(U_cc) (U first rows)
-  int cont;    // continues the previous column
+  unsigned a0, a1;  // shared addresses of this lane's two y entries (dummy slot for padding)
+  double2 v0, v1;   // this lane's two factor entries
+  double2 rd;       // recipc(U_cc) (U first rows)
+  int cont;         // continues the previous column
 };
 
-__device__ __forceinline__ void col_row_fetch(const ColRing& g, int r, bool upper, ColRow& x) {
+// tuning hook: per-row consumer clocks [3 * rows] of the first system's L sweep
+__device__ long long* g_col_times = nullptr;
+
+// Raw ring row r (known staged) in registers; the y addresses are derived
+// from it one step later (col_row_addr), after the current row's math, so
+// the consumer never stalls on these loads.
+struct ColRaw {
+  int seq, i0, i1;
+  double2 v0, v1, rd;
+};
+template <bool UPPER>
+__device__ __forceinline__ void col_row_raw(const ColRing& g, int r, ColRaw& x) {
   const int lane = threadIdx.x & 31;
   const int slot = r & (g.S - 1);
-  int s;
-  while (((s = ld_acq(g.seq + slot)) >> 1) != r) {
-  }
-  x.cont = s & 1;
-  x.i = g.idx[32 * slot + lane];
-  x.v = g.val[32 * slot + lane];
-  if (upper) x.rd = g.rd[slot];
+  x.seq = g.seq[slot];
+  x.i0 = g.idx[CW * slot + lane];
+  x.i1 = g.idx[CW * slot + 32 + lane];
+  x.v0 = g.val[CW * slot + lane];
+  x.v1 = g.val[CW * slot + 32 + lane];
+  if (UPPER) x.rd = g.rd[slot];
+}
+__device__ __forceinline__ void col_row_addr(const ColRaw& w, unsigned yb, unsigned dummy,
+                                             ColRow& x) {
+  x.cont = w.seq & 1;
+  x.a0 = w.i0 >= 0 ? yb + 16u * w.i0 : dummy;
+  x.a1 = w.i1 >= 0 ? yb + 16u * w.i1 : dummy;
+  x.v0 = w.v0;
+  x.v1 = w.v1;
+  x.rd = w.rd;
+}
+template <bool UPPER>
+__device__ __forceinline__ void col_row_load(const ColRing& g, int r, unsigned yb, unsigned dummy,
+                                             ColRow& x) {
+  ColRaw w;
+  col_row_raw<UPPER>(g, r, w);
+  col_row_addr(w, yb, dummy, x);
 }
 
-// Consumer warp: the whole sweep, in place on y (shared memory).
+// Rows below the returned bound are staged: the warp checks the next 32
+// slots at once (one acquire load per lane + ballot), so the common-case
+// per-row cost is a uniform compare.
+__device__ __forceinline__ int col_ring_ready(const ColRing& g, int r, int rows) {
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    const int rr = r + lane;
+    const bool ok = rr >= rows || ((ld_acq(g.seq + (rr & (g.S - 1))) >> 1) == rr);
+    const unsigned bad = __ballot_sync(FULL, !ok);
+    const int cnt = bad ? __ffs(bad) - 1 : 32;
+    if (cnt > 0) return r + cnt;
+  }
+}
+
+// One consumer step: apply row r (cur) and stage row r+1 (nxt).  Order:
+// issue the y loads of row r, issue the raw ring loads of row r+1, do row
+// r's math and stores, then derive row r+1's addresses.
+template <bool UPPER>
+__device__ __forceinline__ void col_step(const ColRing& g, int r, int rows, unsigned yb,
+                                         unsigned dummy, int& c, double2& xc, int& ready,
+                                         const ColRow& cur, ColRow& nxt, long long* tt) {
+  const int lane = threadIdx.x & 31;
+  if (tt) tt[3 * r] = clock64();
+  // first row of a column: xc = y[c'] (U: times recipc(U_cc), stored back)
+  const int cn = cur.cont ? c : c + (UPPER ? -1 : 1);
+  double2 xn = lds2(yb + 16u * cn);
+  const double2 y0 = lds2(cur.a0), y1 = lds2(cur.a1);
+  const bool more = r + 1 < rows;
+  ColRaw w;
+  if (more) {
+    if (r + 1 >= ready) ready = col_ring_ready(g, r + 1, rows);
+    col_row_raw<UPPER>(g, r + 1, w);
+  }
+  if (tt) tt[3 * r + 1] = clock64();
+  if (UPPER) xn = cmul_plain(xn, cur.rd);
+  xc = cur.cont ? xc : xn;
+  c = cn;
+  if (UPPER && lane == 0 && !cur.cont) sts2(yb + 16u * cn, xc);
+  sts2(cur.a0, csub(y0, cmul_plain(cur.v0, xc)));
+  sts2(cur.a1, csub(y1, cmul_plain(cur.v1, xc)));
+  __syncwarp();
+  if (more) col_row_addr(w, yb, dummy, nxt);
+  if (tt) tt[3 * r + 2] = clock64();
+  if (lane == 0 && (r & 7) == 7) st_rlx(g.head, r + 1);
+}
+
+// Consumer warp: the whole sweep, in place on y (shared memory, with one
+// dummy slot after y[n-1] absorbing padding updates).
 template <bool UPPER>
 __device__ __forceinline__ void col_consume(int n, int rows, const ColRing& g, double2* y) {
   const int lane = threadIdx.x & 31;
-  const unsigned yb = saddr(y);
+  const unsigned yb = saddr(y), dummy = yb + 16u * n;
+  long long* const tt = (!UPPER && blockIdx.x == 0 && lane == 0) ? g_col_times : nullptr;
   int c = UPPER ? n : -1;
   double2 xc = make_double2(0.0, 0.0);
-  ColRow nxt;
-  if (rows > 0) col_row_fetch(g, 0, UPPER, nxt);
-  for (int r = 0; r < rows; ++r) {
-    const ColRow cur = nxt;
-    if (!cur.cont) {  // first row of the next column (warp-uniform)
-      c += UPPER ? -1 : 1;
-      xc = lds2(yb + 16u * c);
-      if (UPPER) {
-        xc = cmul_plain(xc, cur.rd);
-        if (lane == 0) sts2(yb + 16u * c, xc);
-      }
-    }
-    double2 yi;
-    if (cur.i >= 0) yi = lds2(yb + 16u * cur.i);
-    if (r + 1 < rows) col_row_fetch(g, r + 1, UPPER, nxt);
-    if (cur.i >= 0) sts2(yb + 16u * cur.i, csub(yi, cmul_plain(cur.v, xc)));
-    __syncwarp();
-    if (lane == 0 && (r & 3) == 3) st_rlx(g.head, r + 1);
+  if (rows <= 0) return;
+  int ready = col_ring_ready(g, 0, rows);
+  ColRow A, B;
+  col_row_load<UPPER>(g, 0, yb, dummy, A);
+  for (int r = 0; r < rows; r += 2) {  // unrolled by two: no register moves
+    col_step<UPPER>(g, r, rows, yb, dummy, c, xc, ready, A, B, tt);
+    if (r + 1 >= rows) break;
+    col_step<UPPER>(g, r + 1, rows, yb, dummy, c, xc, ready, B, A, tt);
   }
 }
 
@@ -202,7 +312,7 @@ __device__ __forceinline__ void col_lu_sweeps(int n, const ColStream& Ls, const 
                                               const ColRing& g, double2* y) {
   const int wid = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  const int P = max(1, min(nw - 1, 4));
+  const int P = max(1, min(nw - 1, 8));
   col_ring_reset(g);
   __syncthreads();
   if (wid == 0) col_consume<false>(n, Ls.rows, g, y);

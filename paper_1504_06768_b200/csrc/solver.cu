@@ -80,22 +80,36 @@ __device__ __noinline__ void csc_psolve(const SolverArgs* a, const double2* in, 
   __syncthreads();
   cta::ColStream Ls, Us;
   const int32_t l0 = a->Lso[b * n], u0 = a->Uso[b * n];
-  Ls.idx = a->Lsi + 32 * (int64_t)l0;
-  Ls.val = a->Lsv + 32 * (int64_t)l0;
+  Ls.idx = a->Lsi + cta::CW * (int64_t)l0;
+  Ls.val = a->Lsv + cta::CW * (int64_t)l0;
   Ls.meta = a->Lsm + l0;
   Ls.rd = nullptr;
   Ls.rows = a->Lso[b * n + n] - l0;
-  Us.idx = a->Usi + 32 * (int64_t)u0;
-  Us.val = a->Usv + 32 * (int64_t)u0;
+  Us.idx = a->Usi + cta::CW * (int64_t)u0;
+  Us.val = a->Usv + cta::CW * (int64_t)u0;
   Us.meta = a->Usm + u0;
   Us.rd = a->Usr + u0;
   Us.rows = a->Uso[b * n + n] - u0;
-  cta::col_lu_sweeps(n, Ls, Us, cta::col_ring_at(smem + 16 * (size_t)n, a->ring_R), P);
+  cta::col_lu_sweeps(n, Ls, Us, cta::col_ring_at(smem + cta::col_y_bytes(n), a->ring_R), P);
   for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[i];
   __syncthreads();
 }
 
+// tuning hook: [0] cycles in psolve, [1] psolve calls, [2] cycles in apply_op SpMV
+__device__ unsigned long long* g_solver_prof = nullptr;
+
+__device__ void psolve_body(const Ctx& C, const double2* in, double2* out);
 __device__ void psolve(const Ctx& C, const double2* in, double2* out) {
+  unsigned long long* const pf = (blockIdx.x == 0 && threadIdx.x == 0) ? g_solver_prof : nullptr;
+  const long long t0 = pf ? clock64() : 0;
+  psolve_body(C, in, out);
+  if (pf) {
+    pf[0] += clock64() - t0;
+    pf[1] += 1;
+  }
+}
+
+__device__ void psolve_body(const Ctx& C, const double2* in, double2* out) {
   const int n = C.n;
   if (!C.have_M) {
     if (in != out)
@@ -129,8 +143,11 @@ __device__ void psolve(const Ctx& C, const double2* in, double2* out) {
 
 // out = M^{-1} (A v)
 __device__ void apply_op(const Ctx& C, const double2* v, double2* tmp, double2* out) {
+  unsigned long long* const pf = (blockIdx.x == 0 && threadIdx.x == 0) ? g_solver_prof : nullptr;
+  const long long t0 = pf ? clock64() : 0;
   cta::spmv(C.n, C.Arp, C.Aci, C.Av, v, tmp);
   __syncthreads();
+  if (pf) pf[2] += clock64() - t0;
   psolve(C, tmp, out);
 }
 
@@ -437,7 +454,7 @@ __device__ IterOut gmres(const Ctx& C, const double2* b, const Vecs& W, double t
 
 }  // namespace
 
-__global__ void __launch_bounds__(512) steady_solver_kernel(const __grid_constant__ SolverArgs a) {
+__global__ void __launch_bounds__(512, 1) steady_solver_kernel(SolverArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[32 * 4];
   const int b = blockIdx.x;
@@ -462,7 +479,7 @@ __global__ void __launch_bounds__(512) steady_solver_kernel(const __grid_constan
   C.red = red;
   double2* ws = a.work + (int64_t)b * a.work_stride;
   C.csc = a.ring_R > 0;
-  C.sa = &a;
+  C.sa = a.self;  // device copy of the launch arguments
   if (C.csc) {
     C.y = reinterpret_cast<double2*>(smem);
     C.y2 = nullptr;
@@ -639,7 +656,7 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  size_t smem = a.ring_R > 0 ? 16 * (size_t)a.n + cta::col_ring_bytes(a.ring_R)
+  size_t smem = a.ring_R > 0 ? cta::col_y_bytes(a.n) + cta::col_ring_bytes(a.ring_R)
                              : (a.y_in_smem ? 32 * (size_t)a.n : 0);
   if (smem + 2048 > (size_t)max_smem) {
     set_error("steady solver: n=%d needs %zu B of shared memory", a.n, smem);
@@ -647,7 +664,15 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
   }
   RS_CUDA_TRY(cudaFuncSetAttribute(steady_solver_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  steady_solver_kernel<<<a.B, a.threads, smem, st>>>(a); ::rs::count_launch();
+  SolverArgs la = a;
+  SolverArgs* dev_args = nullptr;
+  if (la.ring_R > 0) {  // the out-of-line column sweeps read the arguments from here
+    RS_CUDA_TRY(cudaMallocAsync(&dev_args, sizeof(SolverArgs), st));
+    RS_CUDA_TRY(cudaMemcpyAsync(dev_args, &la, sizeof(SolverArgs), cudaMemcpyHostToDevice, st));
+    la.self = dev_args;
+  }
+  steady_solver_kernel<<<a.B, a.threads, smem, st>>>(la); ::rs::count_launch();
+  if (dev_args) cudaFreeAsync(dev_args, st);
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -657,8 +682,7 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
 namespace rs {
 
 // Standalone preconditioner apply (factor.solve_lu), one CTA per system.
-__global__ void __launch_bounds__(512) lu_solve_kernel(const __grid_constant__ SolverArgs a,
-                                                      int y_in_smem) {
+__global__ void __launch_bounds__(512) lu_solve_kernel(SolverArgs a, int y_in_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.x;
   const int n = a.n;
@@ -675,7 +699,7 @@ __global__ void __launch_bounds__(512) lu_solve_kernel(const __grid_constant__ S
   C.rU = a.rU + bn;
   C.pinv = a.pinv + bn;
   C.csc = a.ring_R > 0;
-  C.sa = &a;
+  C.sa = a.self;  // device copy of the launch arguments
   if (C.csc) {
     C.y = reinterpret_cast<double2*>(smem);
     C.y2 = nullptr;
@@ -718,7 +742,7 @@ __global__ void col_stream_count_kernel(int B, int32_t n, int upper, const int32
   const int32_t c = upper ? n - 1 - j : j;
   const int32_t* p = cp + b * (n + 1);
   const int32_t len = p[c + 1] - p[c] - 1;  // off-diagonal entries
-  rows[t] = len > 0 ? (len + 31) >> 5 : 1;
+  rows[t] = len > 0 ? (len + cta::CW - 1) / cta::CW : 1;
 }
 
 // one warp per column: coalesced copy into its padded rows
@@ -741,8 +765,8 @@ __global__ void col_stream_fill_kernel(int B, int32_t n, int upper, const int32_
   const int32_t r0 = rowoff[t], nr = rowoff[t + 1] - r0;
   const int32_t* I = ci + b * cap;
   const double2* X = cv + b * cap;
-  for (int32_t k = lane; k < 32 * nr; k += 32) {
-    const int64_t o = 32 * (int64_t)r0 + k;
+  for (int32_t k = lane; k < cta::CW * nr; k += 32) {
+    const int64_t o = cta::CW * (int64_t)r0 + k;
     if (k < len) {
       idx[o] = I[s + k];
       val[o] = X[s + k];
@@ -774,7 +798,7 @@ int col_stream_build(int B, int32_t n, int upper, const int32_t* cp, const int32
     const int rc = scan_counts(rows, rowoff, N, &tot, st);
     cudaFreeAsync(rows, st);
     if (rc) return rc;
-    if (tot < 0 || tot >= ((int64_t)1 << 26)) {
+    if (tot < 0 || tot >= ((int64_t)1 << 25)) {
       set_error("col_stream_build: %lld rows exceed 32-bit entry indexing", (long long)tot);
       return RS_ERR_OVERFLOW;
     }
@@ -796,10 +820,10 @@ int col_ring_size(int32_t n, int B) {
   if (cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) !=
       cudaSuccess)
     return 0;
-  // batches keep four CTAs per SM resident: a 32-slot ring (21 KB); a lone
+  // batches keep four CTAs per SM resident: a 16-slot ring (21 KB); a lone
   // system takes a deeper ring
-  for (int S = (B > 148 ? 32 : 128); S >= 8; S >>= 1)
-    if (16 * (size_t)n + cta::col_ring_bytes(S) + 4096 <= (size_t)max_smem) return S;
+  for (int S = (B > 148 ? 16 : 64); S >= 8; S >>= 1)
+    if (cta::col_y_bytes(n) + cta::col_ring_bytes(S) + 4096 <= (size_t)max_smem) return S;
   return 0;
 }
 
@@ -809,7 +833,7 @@ int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int y_smem = 32 * (size_t)a.n + 2048 <= (size_t)max_smem;
-  size_t smem = a.ring_R > 0 ? 16 * (size_t)a.n + cta::col_ring_bytes(a.ring_R)
+  size_t smem = a.ring_R > 0 ? cta::col_y_bytes(a.n) + cta::col_ring_bytes(a.ring_R)
                              : (y_smem ? 32 * (size_t)a.n : 0);
   if (a.ring_R <= 0 && !y_smem && !a.work) {
     set_error("lu_solve: n=%d needs global scratch", a.n);
@@ -818,7 +842,16 @@ int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
   RS_CUDA_TRY(cudaFuncSetAttribute(lu_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
   // column sweeps: 1 consumer + 4 producer warps; row sweeps: 16 warps
-  lu_solve_kernel<<<a.B, a.ring_R > 0 ? 160 : 512, smem, st>>>(a, y_smem); ::rs::count_launch();
+  SolverArgs la = a;
+  SolverArgs* dev_args = nullptr;
+  if (la.ring_R > 0) {
+    RS_CUDA_TRY(cudaMallocAsync(&dev_args, sizeof(SolverArgs), st));
+    RS_CUDA_TRY(cudaMemcpyAsync(dev_args, &la, sizeof(SolverArgs), cudaMemcpyHostToDevice, st));
+    la.self = dev_args;
+  }
+  lu_solve_kernel<<<a.B, a.ring_R > 0 ? (a.B > 148 ? 128 : 288) : 512, smem, st>>>(la, y_smem);
+  ::rs::count_launch();
+  if (dev_args) cudaFreeAsync(dev_args, st);
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
 }
@@ -906,6 +939,18 @@ extern "C" int rs_debug_tri_probe(int n, const int32_t* rp, const int32_t* ci, c
 extern "C" int rs_debug_tri_backoff(unsigned nap_min, unsigned nap_max) {
   RS_CUDA_TRY(cudaMemcpyToSymbol(rs::cta::g_tri_nap_min, &nap_min, sizeof(unsigned)));
   RS_CUDA_TRY(cudaMemcpyToSymbol(rs::cta::g_tri_nap_max, &nap_max, sizeof(unsigned)));
+  return 0;
+}
+
+extern "C" int rs_debug_solver_prof(void* buf) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+  RS_CUDA_TRY(cudaMemcpyToSymbol(rs::g_solver_prof, &p, sizeof(p)));
+  return 0;
+}
+
+extern "C" int rs_debug_col_times(void* buf) {
+  long long* p = reinterpret_cast<long long*>(buf);
+  RS_CUDA_TRY(cudaMemcpyToSymbol(rs::cta::g_col_times, &p, sizeof(p)));
   return 0;
 }
 

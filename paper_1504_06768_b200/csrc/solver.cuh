@@ -78,7 +78,8 @@ struct SolverArgs {
   const double2* Usv;
   const int32_t* Usm;
   const double2* Usr;
-  int32_t ring_R;  // > 0: column sweeps with a ring of ring_R 32-entry slots
+  int32_t ring_R;  // > 0: column sweeps with a ring of ring_R 64-entry slots
+  const SolverArgs* self;  // device copy of these arguments (set by the launcher)
 };
 
 // Ring size for the column sweeps of systems of order n in a launch of B

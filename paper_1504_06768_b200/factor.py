@@ -174,6 +174,9 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
     return f
 
 
+COL_STREAM_WIDTH = 64  # entries per stream row (csrc/colsweep.cuh CW)
+
+
 def _col_stream(B, n, upper, cp, ci, cv, cap, rdiag, dev):
     """Column stream of one triangle (csrc/colsweep.cuh): (rowoff, idx, val,
     meta, rrd)."""
@@ -183,8 +186,8 @@ def _col_stream(B, n, upper, cp, ci, cv, cap, rdiag, dev):
     _lib.call("rs_col_stream_build", B, n, upper, _lib.ptr(cp), _lib.ptr(ci), _lib.ptr(cv), cap,
               _lib.ptr(rdiag), _lib.ptr(rowoff), None, None, None, None, ctypes.byref(rows), st)
     R = max(rows.value, 1)
-    idx = torch.empty(32 * R, dtype=torch.int32, device=dev)
-    val = torch.empty(32 * R, dtype=torch.complex128, device=dev)
+    idx = torch.empty(COL_STREAM_WIDTH * R, dtype=torch.int32, device=dev)
+    val = torch.empty(COL_STREAM_WIDTH * R, dtype=torch.complex128, device=dev)
     meta = torch.empty(R, dtype=torch.int32, device=dev)
     rrd = torch.empty(R, dtype=torch.complex128, device=dev) if upper else None
     _lib.call("rs_col_stream_build", B, n, upper, _lib.ptr(cp), _lib.ptr(ci), _lib.ptr(cv), cap,
