@@ -145,6 +145,10 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.state = state;
   a.warps = nsys >= 148 ? 8 : 16;
   if (const char* e = getenv("RHOSOLVE_ILU_WARPS")) a.warps = atoi(e);  // tuning knob
+  // the critical column's owner polls the frontier hot (naps measured: no
+  // gain at 16-128 ns on the 512-system batch)
+  a.hot_nap = 0;
+  if (const char* e = getenv("RHOSOLVE_ILU_HOTNAP")) a.hot_nap = atoi(e);  // tuning knob
   RS_TRY(ilutp_plan(n, a.warps, &a.smem_mode, &a.bits_in_smem));
   const int nwords = (n + 31) / 32;
   const int64_t NW = N * a.warps;  // per-warp slices

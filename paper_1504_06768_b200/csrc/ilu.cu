@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
         // back off so they do not steal issue slots from the critical tail
         // nap length grows with the distance to this column's turn
         const int dist = k - scanned - 1;
-        const unsigned nap = dist <= 0 ? 0u : (dist < 4 ? 64u * dist : 512u);
+        const unsigned nap = dist <= 0 ? (unsigned)a.hot_nap : (dist < 4 ? 64u * dist : 512u);
         while ((d = ctl[0]) == scanned && !ctl[1]) {
           if (nap) __nanosleep(nap);
         }
