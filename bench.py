@@ -313,7 +313,7 @@ def kernel_timings(L, skw, torch, seeds):
 
     b_spmv = 20 * nnz + 4 * (B * n + 1) + 32 * B * n
     out["spmv"] = {"seconds": timed(run_spmv, reps=20), "bytes": b_spmv,
-                   "kernel": "spmv_kernel"}
+                   "kernel": "spmv_warp_kernel"}
 
     def run_apply():
         factor.solve_lu_device(f, x)

@@ -5,16 +5,20 @@
 //
 // B200 layout -- products element-parallel, sums row-sequential.  The only
 // ordering constraint of the reference is the left fold of each row's
-// products; the products themselves are independent.  A CTA owns SPMV_T
+// products; the products themselves are independent.  Each warp owns 32
 // consecutive rows, whose nonzeros form one contiguous slice of the CSR
-// arrays.  Pass 1 streams that slice in chunks of SPMV_CHUNK entries: thread t
-// takes entries t, t+T, ... (fully coalesced 4-byte index and 16-byte value
-// loads, SPMV_UNROLL independent loads in flight per thread), gathers x
-// through the read-only path and writes the complex product to shared memory.
-// Pass 2: thread t folds its own row's products out of shared memory in
-// storage order, carrying the partial sum across chunks -- so rows of any
-// length (the modified Liouvillian's trace row) need no special path.  The
-// kernel streams 20 B per nonzero once: the HBM roofline case.
+// arrays.  Pass 1 streams that slice in chunks of 32*UNROLL entries: lane l
+// takes entries l, l+32, ... (fully coalesced 4-byte index and 16-byte value
+// loads, UNROLL independent loads in flight per lane), gathers x through the
+// read-only path and writes the complex product to a warp-private shared
+// buffer.  Pass 2: lane l folds its own row's products in storage order,
+// carrying the partial sum across chunks -- so rows of any length (the
+// modified Liouvillian's trace row) need no special path.  Warps never wait
+// on each other (no CTA barrier), so load and fold phases of different warps
+// overlap.  The kernel streams 20 B per nonzero once: the HBM roofline case.
+// Tuning (tools/spmv_probe.py): CTA-wide staging with 256-row CTAs reached
+// 2.27-2.86 TB/s on the c4 batch, this warp-granular form 2.86 TB/s (158 MB)
+// and 3.77 TB/s (633 MB); software-pipelining the next chunk spilled and lost.
 //
 // Batches of B equal-size systems are stored block-diagonally: row_ptr spans
 // all B*n rows, column indices are local to their system, and system b reads
@@ -26,68 +30,69 @@
 
 namespace rs {
 
-constexpr int SPMV_T = 256;        // threads = rows per CTA
-constexpr int SPMV_CHUNK = 2048;   // products staged per pass (32 KB)
-constexpr int SPMV_UNROLL = SPMV_CHUNK / SPMV_T;
-constexpr int SPMV_MAXSYS = SPMV_T + 2;
+// shared slot of staged product e (CTA-relative): one pad slot per 8 keeps
+// the row-sequential fold (lane t reads ~8t + q for ~8-entry rows) off a
+// single bank quad
+template <bool PAD>
+__device__ __forceinline__ int slot_of(int e) { return PAD ? e + (e >> 3) : e; }
 
-__global__ void __launch_bounds__(SPMV_T)
-spmv_kernel(int64_t nrows, int32_t n, const int32_t* __restrict__ rp,
-            const int32_t* __restrict__ ci, const double2* __restrict__ v,
-            const double2* __restrict__ x, double2* __restrict__ y) {
-  __shared__ __align__(16) double2 s_p[SPMV_CHUNK];
-  __shared__ int32_t s_sysbeg[SPMV_MAXSYS];  // element where each later system starts
-  __shared__ int s_nb;
-
-  const int tid = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.x * SPMV_T;
-  const int64_t r1 = min(r0 + SPMV_T, nrows);
-  const int64_t row = r0 + tid;
+// Warp-granular variant: each warp owns 32 consecutive rows and stages its
+// own products in a private shared buffer, so warps never wait on each other
+// (no CTA barrier) and load / fold phases of different warps overlap.
+template <int UNROLL, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+spmv_warp_kernel(int64_t nrows, int32_t n, const int32_t* __restrict__ rp,
+                 const int32_t* __restrict__ ci, const double2* __restrict__ v,
+                 const double2* __restrict__ x, double2* __restrict__ y) {
+  constexpr int CH = 32 * UNROLL;
+  __shared__ __align__(16) double2 s_buf[8][CH + CH / 8];
+  __shared__ int32_t s_beg[8][34];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double2* s_p = s_buf[wid];
+  int32_t* s_sysbeg = s_beg[wid];
+  const int64_t r0 = ((int64_t)blockIdx.x * 8 + wid) * 32;
+  if (r0 >= nrows) return;
+  const int64_t r1 = min(r0 + 32, nrows);
+  const int64_t row = r0 + lane;
   const bool have = row < r1;
   const int32_t base = __ldg(rp + r0), end = __ldg(rp + r1);
   const int32_t p0 = have ? __ldg(rp + row) : 0, p1 = have ? __ldg(rp + row + 1) : 0;
-
-  // system boundaries inside [r0, r1): rows that are multiples of n
   const int64_t s0 = r0 / n;
-  if (tid == 0) s_nb = 0;
-  __syncthreads();
-  if (have && row > r0 && row % n == 0) {
-    const int k = (int)(row / n - s0) - 1;
-    s_sysbeg[k] = p0;
-    atomicMax(&s_nb, k + 1);
-  }
-  __syncthreads();
-  const int nb = s_nb;
-
+  // system starts inside the warp's rows (ballot-compacted, ascending)
+  const bool starts = have && row > r0 && row % n == 0;
+  const unsigned sm = __ballot_sync(0xffffffffu, starts);
+  if (starts) s_sysbeg[__popc(sm & ((1u << lane) - 1u))] = p0;
+  const int nb = __popc(sm);
+  __syncwarp();
   double2 acc = make_double2(0.0, 0.0);
-  for (int32_t cb = base; cb < end; cb += SPMV_CHUNK) {
-    const int32_t ce = min(cb + SPMV_CHUNK, end);
-    int c[SPMV_UNROLL];
-    double2 a[SPMV_UNROLL];
+  for (int32_t cb = base; cb < end; cb += CH) {
+    const int32_t ce = min(cb + CH, end);
+    int c[UNROLL];
+    double2 a[UNROLL];
 #pragma unroll
-    for (int u = 0; u < SPMV_UNROLL; ++u) {
-      const int32_t e = cb + u * SPMV_T + tid;
+    for (int u = 0; u < UNROLL; ++u) {
+      const int32_t e = cb + 32 * u + lane;
       if (e < ce) {
         c[u] = __ldg(ci + e);
         a[u] = ldg2(v + e);
       }
     }
 #pragma unroll
-    for (int u = 0; u < SPMV_UNROLL; ++u) {
-      const int32_t e = cb + u * SPMV_T + tid;
+    for (int u = 0; u < UNROLL; ++u) {
+      const int32_t e = cb + 32 * u + lane;
       if (e < ce) {
         int64_t sys = s0;
         for (int k = 0; k < nb && e >= s_sysbeg[k]; ++k) ++sys;
-        s_p[e - cb] = cmul_plain(a[u], ldg2(x + sys * n + c[u]));
+        s_p[slot_of<true>(e - cb)] = cmul_plain(a[u], ldg2(x + sys * n + c[u]));
       }
     }
-    __syncthreads();
+    __syncwarp();
     const int32_t qa = max(p0, cb), qb = min(p1, ce);
     for (int32_t q = qa; q < qb; ++q) {
-      const double2 pq = s_p[q - cb];
+      const double2 pq = s_p[slot_of<true>(q - cb)];
       acc = (q == p0) ? pq : cadd(acc, pq);
     }
-    __syncthreads();
+    __syncwarp();
   }
   if (have) y[row] = acc;
 }
@@ -97,8 +102,9 @@ int launch_spmv(int64_t nrows, int32_t n, const int32_t* rp, const int32_t* ci,
                 cudaStream_t st) {
   if (nrows == 0) return RS_OK;
   RS_CHECK_ARG(n > 0, "n must be positive");
-  const int64_t grid = (nrows + SPMV_T - 1) / SPMV_T;
-  spmv_kernel<<<(unsigned)grid, SPMV_T, 0, st>>>(nrows, n, rp, ci, v, x, y);
+  // 8 warps x 32 rows per CTA; 4 chunks of 32 products per warp pass
+  const unsigned grid = (unsigned)((nrows + 255) / 256);
+  spmv_warp_kernel<4, 4><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y);
   ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
