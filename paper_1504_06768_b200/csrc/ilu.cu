@@ -88,7 +88,9 @@ __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_
   return (b + 15) & ~(size_t)15;
 }
 
-template <int MAXT, int MINB>
+// INC = false: complete LU (drop 0, no cap) -- the drop tests, keep flags
+// and cap selection compile away.
+template <int MAXT, int MINB, bool INC>
 __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
   int32_t* gpinv = a.pinv + bn;
   const double* rn = a.rn ? a.rn + bn : nullptr;
   const int32_t* Ap = a.Ap + bn;
-  const double drop = a.drop_tol;
+  const double drop = INC ? a.drop_tol : 0.0;
 
   // control words: ctl[0] = number of finished columns, ctl[1] = abort
   volatile int32_t* ctl = reinterpret_cast<volatile int32_t*>(smem);
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
   RS_FENCE();
   __syncthreads();
   const int fill_cap = a.fill_caps ? a.fill_caps[b] : a.fill_cap;
-  const bool have_cap = fill_cap >= 0;
+  const bool have_cap = INC && fill_cap >= 0;
 
   // round-robin columns, starting at the resume point
   for (int k = k0 + wid; k < n; k += W) {
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
         atomicAnd(&bits[w], ~(1u << (c & 31)));
         urow[unum] = c;
         uval[unum] = xc;
-        ukeep[unum] = ukk;
+        if (INC) ukeep[unum] = ukk;
       }
       ++unum;
       kept_u += ukk;
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
           const double mag = cabs1(xv[u]);
           const bool keep = !(drop > 0.0 && mag < drop * rv[u]);
           lrow[pos] = i;
-          lkeep[pos] = keep;
+          if (INC) lkeep[pos] = keep;
           kept_l += keep;
           if (mag > best || (mag == best && i < ipiv)) {
             best = mag;
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
     }
     // the pivot row is never an L entry: the owning lane clears its keep
     const bool owner = (ipiv == gipiv) && ipos >= 0;
-    if (owner) lkeep[ipos] = 0;
+    if (INC && owner) lkeep[ipos] = 0;
     const unsigned om = __ballot_sync(FULL, owner && ikeep);
     kept_l = warp_sum_i(kept_l) - (om ? 1 : 0);
     ipiv = gipiv;
@@ -550,8 +552,8 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
       for (int u = 0; u < 8; ++u) {
         const int t = blk + 32 * u + lane;
         const bool act = t < lnum;
-        kp[u] = act && lkeep[t];
         ir[u] = act ? lrow[t] : 0;
+        kp[u] = act && (INC ? lkeep[t] != 0 : ir[u] != ipiv);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) xv[u] = kp[u] ? x[ir[u]] : make_double2(0.0, 0.0);
@@ -585,7 +587,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
     int uo = unnz;
     for (int base = 0; base < unum; base += 32) {
       const int t = base + lane;
-      const bool keep = t < unum && ukeep[t];
+      const bool keep = t < unum && (INC ? ukeep[t] != 0 : true);
       const unsigned m = __ballot_sync(FULL, keep);
       if (keep) {
         const int o = uo + __popc(m & lanemask_lt());
@@ -628,11 +630,21 @@ int launch_ilutp(const FactorArgs& a, cudaStream_t st) {
   const bool batch = a.B > 148;
   int rc;
   (void)0;
-  if (W <= 4) rc = batch ? launch(ilutp_pipeline_kernel<128, 4>) : launch(ilutp_pipeline_kernel<128, 1>);
-  else if (W <= 6) rc = batch ? launch(ilutp_pipeline_kernel<192, 4>) : launch(ilutp_pipeline_kernel<192, 1>);
-  else if (W <= 8) rc = batch ? launch(ilutp_pipeline_kernel<256, 4>) : launch(ilutp_pipeline_kernel<256, 1>);
-  else if (W <= 16) rc = launch(ilutp_pipeline_kernel<512, 1>);
-  else rc = launch(ilutp_pipeline_kernel<1024, 1>);
+  const bool inc = a.drop_tol > 0.0 || a.fill_cap >= 0 || a.fill_caps != nullptr;
+  auto pick = [&](auto kc, auto ki) -> int { return inc ? launch(ki) : launch(kc); };
+  if (W <= 4)
+    rc = batch ? pick(ilutp_pipeline_kernel<128, 4, false>, ilutp_pipeline_kernel<128, 4, true>)
+               : pick(ilutp_pipeline_kernel<128, 1, false>, ilutp_pipeline_kernel<128, 1, true>);
+  else if (W <= 6)
+    rc = batch ? pick(ilutp_pipeline_kernel<192, 4, false>, ilutp_pipeline_kernel<192, 4, true>)
+               : pick(ilutp_pipeline_kernel<192, 1, false>, ilutp_pipeline_kernel<192, 1, true>);
+  else if (W <= 8)
+    rc = batch ? pick(ilutp_pipeline_kernel<256, 4, false>, ilutp_pipeline_kernel<256, 4, true>)
+               : pick(ilutp_pipeline_kernel<256, 1, false>, ilutp_pipeline_kernel<256, 1, true>);
+  else if (W <= 16)
+    rc = pick(ilutp_pipeline_kernel<512, 1, false>, ilutp_pipeline_kernel<512, 1, true>);
+  else
+    rc = pick(ilutp_pipeline_kernel<1024, 1, false>, ilutp_pipeline_kernel<1024, 1, true>);
   if (rc) return rc;
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;
