@@ -149,6 +149,8 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   // gain at 16-128 ns on the 512-system batch)
   a.hot_nap = 0;
   if (const char* e = getenv("RHOSOLVE_ILU_HOTNAP")) a.hot_nap = atoi(e);  // tuning knob
+  a.nap_step = 64;
+  if (const char* e = getenv("RHOSOLVE_ILU_NAPSTEP")) a.nap_step = atoi(e);  // tuning knob
   RS_TRY(ilutp_plan(n, a.warps, &a.smem_mode, &a.bits_in_smem));
   const int nwords = (n + 31) / 32;
   const int64_t NW = N * a.warps;  // per-warp slices

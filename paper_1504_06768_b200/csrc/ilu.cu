@@ -64,11 +64,16 @@ __device__ __forceinline__ int warp_min_i(int v) {
 __device__ __forceinline__ uint64_t mag_key(double2 z) {
   return (uint64_t)__double_as_longlong(cabs1(z));
 }
+// Cross-warp shared state (pinv / prow / Lp / Up, in shared or global
+// memory) is only ever exchanged inside one CTA: CTA-scope relaxed accesses
+// (a plain volatile generic access compiles to a system-scope strong load).
 __device__ __forceinline__ int vload(const int32_t* p) {
-  return *reinterpret_cast<const volatile int32_t*>(p);
+  int v;
+  asm volatile("ld.relaxed.cta.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
 }
 __device__ __forceinline__ void vstore(int32_t* p, int v) {
-  *reinterpret_cast<volatile int32_t*>(p) = v;
+  asm volatile("st.relaxed.cta.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void probe_mark(unsigned long long* pr, int k, int slot, int lane) {
@@ -238,7 +243,8 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
         // back off so they do not steal issue slots from the critical tail
         // nap length grows with the distance to this column's turn
         const int dist = k - scanned - 1;
-        const unsigned nap = dist <= 0 ? (unsigned)a.hot_nap : (dist < 4 ? 64u * dist : 512u);
+        const unsigned nap =
+            dist <= 0 ? (unsigned)a.hot_nap : (dist < 4 ? a.nap_step * dist : 8u * a.nap_step);
         while ((d = ctl[0]) == scanned && !ctl[1]) {
           if (nap) __nanosleep(nap);
         }

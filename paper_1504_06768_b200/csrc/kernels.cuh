@@ -65,6 +65,7 @@ struct FactorArgs {
   int bits_in_smem;  // 1: per-warp pending bitmaps in shared memory
   int warps;         // warps (columns in flight) per system
   int hot_nap;       // ns the next column's owner naps between frontier polls
+  unsigned nap_step; // ns per column of distance for the other warps' naps
   unsigned long long* probe;  // optional per-column phase clocks [n*6] (tuning)
 };
 // state[3b+0] codes
