@@ -3,6 +3,7 @@
 // no fallback path.
 #include <stdarg.h>
 #include <stdlib.h>
+#include <algorithm>
 #include <atomic>
 #include <stdio.h>
 #include <string.h>
@@ -151,9 +152,17 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   if (const char* e = getenv("RHOSOLVE_ILU_HOTNAP")) a.hot_nap = atoi(e);  // tuning knob
   a.nap_step = 64;
   if (const char* e = getenv("RHOSOLVE_ILU_NAPSTEP")) a.nap_step = atoi(e);  // tuning knob
+  // large systems: one system spans several CTAs (columns in flight across
+  // SMs; the per-column work of c3 / the c5 blocks dwarfs the cross-SM
+  // hand-off)
+  a.cps = 1;
+  if (n >= 8192 && nsys < 148) a.cps = std::min(16, std::max(1, 148 / nsys));
+  if (const char* e = getenv("RHOSOLVE_ILU_CPS")) a.cps = std::max(1, atoi(e));  // tuning knob
+  if (a.cps > 1) a.warps = 16;
   RS_TRY(ilutp_plan(n, a.warps, &a.smem_mode, &a.bits_in_smem));
+  if (a.cps > 1) a.smem_mode = 0;  // pinv / prow / Lp are shared across CTAs
   const int nwords = (n + 31) / 32;
-  const int64_t NW = N * a.warps;  // per-warp slices
+  const int64_t NW = N * a.warps * a.cps;  // per-warp slices
   size_t bytes = 0;
   auto take = [&](size_t b) {
     size_t o = bytes;
@@ -162,7 +171,9 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   };
   const size_t o_x = take(16 * NW);
   const size_t o_flag = take(4 * NW);
-  const size_t o_bits = a.bits_in_smem ? 0 : take(4 * (size_t)nwords * nsys * a.warps);
+  const size_t o_bits =
+      a.bits_in_smem ? 0 : take(4 * (size_t)nwords * nsys * a.warps * a.cps);
+  const size_t o_ctl = take(8 * (size_t)nsys);
   const size_t o_prow = take(4 * N);
   const size_t o_pat = take(4 * NW);
   const size_t o_urow = take(4 * NW);
@@ -184,6 +195,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.wukeep = ws + o_uk;
   a.wlkeep = ws + o_lk;
   a.wkey = reinterpret_cast<uint64_t*>(ws + o_key);
+  a.gctl = reinterpret_cast<int32_t*>(ws + o_ctl);
   a.probe = g_factor_probe;
   // prow is scratch: a resumed launch rebuilds it as the inverse of pinv.
   const int rc = launch_ilutp(a, st);

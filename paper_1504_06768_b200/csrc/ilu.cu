@@ -41,6 +41,7 @@
 #ifndef RS_FENCE
 #define RS_FENCE() __threadfence_block()
 #endif
+#define RS_FENCE_CTA() __threadfence_block()
 
 namespace rs {
 
@@ -67,13 +68,18 @@ __device__ __forceinline__ uint64_t mag_key(double2 z) {
 // Cross-warp shared state (pinv / prow / Lp / Up, in shared or global
 // memory) is only ever exchanged inside one CTA: CTA-scope relaxed accesses
 // (a plain volatile generic access compiles to a system-scope strong load).
-__device__ __forceinline__ int vload(const int32_t* p) {
+// (MULTI: a system spans several CTAs, so the exchange is GPU-scope.)
+template <bool MULTI = false>
+__device__ __forceinline__ int vload_(const int32_t* p) {
   int v;
-  asm volatile("ld.relaxed.cta.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  if (MULTI) asm volatile("ld.relaxed.gpu.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  else asm volatile("ld.relaxed.cta.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
-__device__ __forceinline__ void vstore(int32_t* p, int v) {
-  asm volatile("st.relaxed.cta.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+template <bool MULTI = false>
+__device__ __forceinline__ void vstore_(int32_t* p, int v) {
+  if (MULTI) asm volatile("st.relaxed.gpu.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else asm volatile("st.relaxed.cta.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void probe_mark(unsigned long long* pr, int k, int slot, int lane) {
@@ -95,13 +101,26 @@ __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_
 
 // INC = false: complete LU (drop 0, no cap) -- the drop tests, keep flags
 // and cap selection compile away.
-template <int MAXT, int MINB, bool INC>
+// MULTI = true: one system spans a.cps CTAs (large systems: c3, the c5
+// block-Jacobi blocks).  Warp gw = cta * Wl + wid of the system owns columns
+// gw, gw + W, ... with W = cps * Wl; the finished-column counter and abort
+// flag live in global memory (a.gctl), exchanges are GPU-scope, and the
+// CTA-wide init / finish steps run as separate kernels.
+template <int MAXT, int MINB, bool INC, bool MULTI>
 __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  const int W = blockDim.x >> 5;
-  const int b = blockIdx.x;
+  const int Wl = blockDim.x >> 5;
+  const int cps = MULTI ? a.cps : 1;
+  const int b = MULTI ? blockIdx.x / cps : blockIdx.x;
+  const int wid = MULTI ? (blockIdx.x % cps) * Wl + (threadIdx.x >> 5) : (threadIdx.x >> 5);
+  const int lw = threadIdx.x >> 5;  // warp index inside this CTA (shared-memory slices)
+  const int W = Wl * cps;
+  auto vload = [](const int32_t* p) { return vload_<MULTI>(p); };
+#define FENCE() (MULTI ? __threadfence() : RS_FENCE_CTA())
+  // L columns written by another SM must not be served from a stale L1 line
+  auto ldL = [](const auto* p) { return MULTI ? __ldcg(p) : *p; };
+  auto vstore = [](int32_t* p, int v) { vstore_<MULTI>(p, v); };
   const int32_t n = a.n;
   const int nwords = (n + 31) >> 5;
   int32_t* state = a.state + 3 * (int64_t)b;
@@ -122,8 +141,9 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
   const double drop = INC ? a.drop_tol : 0.0;
 
   // control words: ctl[0] = number of finished columns, ctl[1] = abort
-  volatile int32_t* ctl = reinterpret_cast<volatile int32_t*>(smem);
-  unsigned char* sp = smem + 64 + 1024 * (size_t)W;  // after the per-warp cap histograms
+  volatile int32_t* ctl = MULTI ? reinterpret_cast<volatile int32_t*>(a.gctl + 2 * (int64_t)b)
+                                : reinterpret_cast<volatile int32_t*>(smem);
+  unsigned char* sp = smem + 64 + 1024 * (size_t)Wl;  // after the per-warp cap histograms
   int32_t *pinv, *prow, *Lp;
   if (a.smem_mode) {
     pinv = reinterpret_cast<int32_t*>(sp);
@@ -136,7 +156,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
     Lp = gLp;
   }
   uint32_t* bits;
-  if (a.bits_in_smem) bits = reinterpret_cast<uint32_t*>(sp) + (size_t)wid * nwords;
+  if (a.bits_in_smem) bits = reinterpret_cast<uint32_t*>(sp) + (size_t)lw * nwords;
   else bits = a.wbits + ((int64_t)b * W + wid) * nwords;
 
   // per-warp private scratch (global, L1/L2 resident)
@@ -150,24 +170,26 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
   uint8_t* ukeep = a.wukeep + ws;
   uint8_t* lkeep = a.wlkeep + ws;
   uint64_t* keys = a.wkey + ws;
-  unsigned* hist = reinterpret_cast<unsigned*>(smem + 64) + 256 * wid;
+  unsigned* hist = reinterpret_cast<unsigned*>(smem + 64) + 256 * lw;
 
   // ---- init -----------------------------------------------------------------
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    if (k0 == 0) gpinv[i] = -1;
-    prow[i] = -1;
+  if (!MULTI) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (k0 == 0) gpinv[i] = -1;
+      prow[i] = -1;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int pv = gpinv[i];
+      if (a.smem_mode) pinv[i] = pv;
+      if (pv >= 0) prow[pv] = i;  // resume after overflow: prow = pinv^-1
+    }
+    if (a.smem_mode)
+      for (int i = threadIdx.x; i <= n; i += blockDim.x) Lp[i] = (i <= k0) ? gLp[i] : 0;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int pv = gpinv[i];
-    if (a.smem_mode) pinv[i] = pv;
-    if (pv >= 0) prow[pv] = i;  // resume after overflow: prow = pinv^-1
-  }
-  if (a.smem_mode)
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) Lp[i] = (i <= k0) ? gLp[i] : 0;
   for (int i = lane; i < n; i += 32) flag[i] = -1;
   for (int w = lane; w < nwords; w += 32) bits[w] = 0u;
-  if (threadIdx.x == 0) {
+  if (!MULTI && threadIdx.x == 0) {
     ctl[0] = k0;
     ctl[1] = 0;
     if (k0 == 0) {
@@ -176,7 +198,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
       Lp[0] = 0;
     }
   }
-  RS_FENCE();
+  FENCE();
   __syncthreads();
   const int fill_cap = a.fill_caps ? a.fill_caps[b] : a.fill_cap;
   const bool have_cap = INC && fill_cap >= 0;
@@ -187,7 +209,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
     int scanned = ctl[0];
     __syncwarp();
     if (ctl[1]) break;
-    RS_FENCE();
+    FENCE();
     unsigned long long* const pr = (b == 0) ? a.probe : nullptr;
     probe_mark(pr, k, 0, lane);
     // ---- 1. scatter column j; seed pending with columns already finished --
@@ -252,7 +274,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
           aborted = true;
           break;
         }
-        RS_FENCE();
+        FENCE();
         int newlow = 0x7fffffff;
         for (int m = scanned + lane; m < d; m += 32) {
           const int r = vload(prow + m);
@@ -282,8 +304,8 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
           const int q0 = vload(Lp + cn) + 1 + lane, q1 = vload(Lp + cn + 1);
           pre_c = cn;
           if (q0 < q1) {
-            pre_i = Li[q0];
-            pre_v = Lx[q0];
+            pre_i = ldL(Li + q0);
+            pre_v = ldL(Lx + q0);
           }
         }
       }
@@ -311,13 +333,13 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
             ia = my_pre_i;
             la = my_pre_v;
           } else {
-            ia = Li[pa];
-            la = Lx[pa];
+            ia = ldL(Li + pa);
+            la = ldL(Lx + pa);
           }
         }
         if (actb) {
-          ib = Li[pb];
-          lb = Lx[pb];
+          ib = ldL(Li + pb);
+          lb = ldL(Lx + pb);
         }
         const int fa = acta ? flag[ia] : k, fb = actb ? flag[ib] : k;
         double2 xa = acta ? x[ia] : la, xb = actb ? x[ib] : lb;
@@ -346,7 +368,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
       __syncwarp();
     }
     if (aborted) break;
-    RS_FENCE();  // acquire: every column < k is final
+    FENCE();  // acquire: every column < k is final
     probe_mark(pr, k, 1, lane);
 
     // ---- 3+4. pivot (max |re|+|im| over non-pivotal rows, ties -> lowest
@@ -575,7 +597,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
       }
     }
     const int32_t unew = unnz + kept_u + 1;
-    RS_FENCE();
+    FENCE();
     __syncwarp();
     if (lane == 0) {
       vstore(gUp + k + 1, unew);
@@ -584,7 +606,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
       vstore(pinv + ipiv, k);
       if (a.smem_mode) gpinv[ipiv] = k;
       vstore(prow + k, ipiv);
-      RS_FENCE();  // release column k
+      FENCE();  // release column k
       ctl[0] = k + 1;
     }
     probe_mark(pr, k, 4, lane);
@@ -608,6 +630,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
     }
     __syncwarp();
   }
+  if (MULTI) return;  // finish runs as ilutp_multi_finish_kernel
   __syncthreads();
   if (ctl[1]) return;  // zero pivot or overflow: state already recorded
   // ---- finish: remap L rows to pivotal indices ------------------------------
@@ -619,10 +642,81 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
   }
 }
 
+// MULTI init, pass 1: reset pinv (fresh start) and prow of unfinished systems
+__global__ void ilutp_multi_init1_kernel(FactorArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)a.B * a.n) return;
+  const int64_t b = t / a.n;
+  const int st0 = a.state[3 * b];
+  if (st0 == FAC_DONE || st0 == FAC_ZERO_PIVOT) return;
+  if (st0 != FAC_OVERFLOW) a.pinv[t] = -1;
+  a.prow[t] = -1;
+}
+// pass 2: prow = pinv^-1 (resume after overflow), control words, Lp/Up[0]
+__global__ void ilutp_multi_init2_kernel(FactorArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)a.B * a.n) return;
+  const int64_t b = t / a.n, i = t % a.n;
+  const int st0 = a.state[3 * b];
+  if (st0 == FAC_DONE || st0 == FAC_ZERO_PIVOT) return;
+  const int pv = a.pinv[t];
+  if (pv >= 0) a.prow[b * a.n + pv] = (int32_t)i;
+  if (i == 0) {
+    const int k0 = st0 == FAC_OVERFLOW ? a.state[3 * b + 1] : 0;
+    a.gctl[2 * b] = k0;
+    a.gctl[2 * b + 1] = 0;
+    if (k0 == 0) {
+      a.Lp[b * (a.n + 1)] = 0;
+      a.Up[b * (a.n + 1)] = 0;
+    }
+  }
+}
+// finish: remap L rows to pivotal indices for systems that completed
+__global__ void ilutp_multi_finish_kernel(FactorArgs a) {
+  const int b = blockIdx.y;
+  const int st0 = a.state[3 * b];
+  if (st0 == FAC_DONE || st0 == FAC_ZERO_PIVOT || a.gctl[2 * b + 1]) return;
+  const int32_t lnnz = a.Lp[(int64_t)b * (a.n + 1) + a.n];
+  int32_t* Li = a.Li + (int64_t)b * a.capL;
+  const int32_t* pinv = a.pinv + (int64_t)b * a.n;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < lnnz;
+       p += (int64_t)gridDim.x * blockDim.x)
+    Li[p] = pinv[Li[p]];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.state[3 * b] = FAC_DONE;
+    a.state[3 * b + 1] = -1;
+  }
+}
+
+static int launch_ilutp_multi(const FactorArgs& a, size_t smem, cudaStream_t st) {
+  const int64_t N = (int64_t)a.B * a.n;
+  const unsigned g = (unsigned)((N + 255) / 256);
+  ilutp_multi_init1_kernel<<<g, 256, 0, st>>>(a);
+  ::rs::count_launch();
+  ilutp_multi_init2_kernel<<<g, 256, 0, st>>>(a);
+  ::rs::count_launch();
+  const bool inc = a.drop_tol > 0.0 || a.fill_cap >= 0 || a.fill_caps != nullptr;
+  void* kern = inc ? (void*)ilutp_pipeline_kernel<512, 1, true, true>
+                   : (void*)ilutp_pipeline_kernel<512, 1, false, true>;
+  RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // every CTA of a system waits on the others: cooperative launch guarantees
+  // they are co-resident
+  FactorArgs aa = a;
+  void* args[] = {&aa};
+  RS_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3((unsigned)(a.B * a.cps)), dim3(32 * a.warps),
+                                          args, smem, st));
+  ::rs::count_launch();
+  ilutp_multi_finish_kernel<<<dim3(64, (unsigned)a.B), 256, 0, st>>>(a);
+  ::rs::count_launch();
+  RS_CUDA_TRY(cudaGetLastError());
+  return RS_OK;
+}
+
 int launch_ilutp(const FactorArgs& a, cudaStream_t st) {
   if (a.B == 0 || a.n == 0) return RS_OK;
   const int W = a.warps;
   const size_t smem = ilutp_smem_bytes(a.n, W, a.smem_mode, a.bits_in_smem);
+  if (a.cps > 1) return launch_ilutp_multi(a, smem, st);
   // one instantiation per block size so each gets its full register budget
   // (a 1024-thread bound caps registers at 64 and spills the tail loops)
   auto launch = [&](auto kern) -> int {
@@ -639,18 +733,18 @@ int launch_ilutp(const FactorArgs& a, cudaStream_t st) {
   const bool inc = a.drop_tol > 0.0 || a.fill_cap >= 0 || a.fill_caps != nullptr;
   auto pick = [&](auto kc, auto ki) -> int { return inc ? launch(ki) : launch(kc); };
   if (W <= 4)
-    rc = batch ? pick(ilutp_pipeline_kernel<128, 4, false>, ilutp_pipeline_kernel<128, 4, true>)
-               : pick(ilutp_pipeline_kernel<128, 1, false>, ilutp_pipeline_kernel<128, 1, true>);
+    rc = batch ? pick(ilutp_pipeline_kernel<128, 4, false, false>, ilutp_pipeline_kernel<128, 4, true, false>)
+               : pick(ilutp_pipeline_kernel<128, 1, false, false>, ilutp_pipeline_kernel<128, 1, true, false>);
   else if (W <= 6)
-    rc = batch ? pick(ilutp_pipeline_kernel<192, 4, false>, ilutp_pipeline_kernel<192, 4, true>)
-               : pick(ilutp_pipeline_kernel<192, 1, false>, ilutp_pipeline_kernel<192, 1, true>);
+    rc = batch ? pick(ilutp_pipeline_kernel<192, 4, false, false>, ilutp_pipeline_kernel<192, 4, true, false>)
+               : pick(ilutp_pipeline_kernel<192, 1, false, false>, ilutp_pipeline_kernel<192, 1, true, false>);
   else if (W <= 8)
-    rc = batch ? pick(ilutp_pipeline_kernel<256, 4, false>, ilutp_pipeline_kernel<256, 4, true>)
-               : pick(ilutp_pipeline_kernel<256, 1, false>, ilutp_pipeline_kernel<256, 1, true>);
+    rc = batch ? pick(ilutp_pipeline_kernel<256, 4, false, false>, ilutp_pipeline_kernel<256, 4, true, false>)
+               : pick(ilutp_pipeline_kernel<256, 1, false, false>, ilutp_pipeline_kernel<256, 1, true, false>);
   else if (W <= 16)
-    rc = pick(ilutp_pipeline_kernel<512, 1, false>, ilutp_pipeline_kernel<512, 1, true>);
+    rc = pick(ilutp_pipeline_kernel<512, 1, false, false>, ilutp_pipeline_kernel<512, 1, true, false>);
   else
-    rc = pick(ilutp_pipeline_kernel<1024, 1, false>, ilutp_pipeline_kernel<1024, 1, true>);
+    rc = pick(ilutp_pipeline_kernel<1024, 1, false, false>, ilutp_pipeline_kernel<1024, 1, true, false>);
   if (rc) return rc;
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;

@@ -66,6 +66,8 @@ struct FactorArgs {
   int warps;         // warps (columns in flight) per system
   int hot_nap;       // ns the next column's owner naps between frontier polls
   unsigned nap_step; // ns per column of distance for the other warps' naps
+  int cps;           // CTAs per system (> 1: multi-CTA mode for large systems)
+  int32_t* gctl;     // [B*2] global control words in multi-CTA mode
   unsigned long long* probe;  // optional per-column phase clocks [n*6] (tuning)
 };
 // state[3b+0] codes
