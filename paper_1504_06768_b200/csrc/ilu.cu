@@ -702,8 +702,20 @@ static int launch_ilutp_multi(const FactorArgs& a, size_t smem, cudaStream_t st)
   // every CTA of a system waits on the others: cooperative launch guarantees
   // they are co-resident
   FactorArgs aa = a;
+  {  // never ask for more co-resident CTAs than the device holds
+    int per_sm = 0, dev = 0, sms = 0;
+    RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * a.warps, smem));
+    RS_CUDA_TRY(cudaGetDevice(&dev));
+    RS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int cap = per_sm * sms;
+    if (a.B > cap) {
+      set_error("multi-CTA factorization: %d systems exceed %d co-resident CTAs", a.B, cap);
+      return RS_ERR_UNSUPPORTED;
+    }
+    if (aa.B * aa.cps > cap) aa.cps = cap / aa.B;
+  }
   void* args[] = {&aa};
-  RS_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3((unsigned)(a.B * a.cps)), dim3(32 * a.warps),
+  RS_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3((unsigned)(aa.B * aa.cps)), dim3(32 * a.warps),
                                           args, smem, st));
   ::rs::count_launch();
   ilutp_multi_finish_kernel<<<dim3(64, (unsigned)a.B), 256, 0, st>>>(a);
