@@ -312,3 +312,27 @@ def test_apply_column_stream_random_long_columns(cuda):
         ref = O.factorize_raw(m, 0.0, math.inf).solve(b[k * n:(k + 1) * n])
         assert bits_equal(xc[k * n:(k + 1) * n], ref)
         assert bits_equal(xr[k * n:(k + 1) * n], ref)
+
+
+@pytest.mark.parametrize("name,kw,d,p,cps,nsys", [("c2", {}, 1e-4, 300.0, 4, 1),
+                                                  ("c2", {}, 0.0, math.inf, 3, 1),
+                                                  ("c4", {"i": 77}, 0.0, math.inf, 2, 3)])
+def test_factorize_multi_cta_bit_exact(cuda, monkeypatch, name, kw, d, p, cps, nsys):
+    """Multi-CTA factorization (one system across several co-resident CTAs,
+    used by default for n >= 8192) forced onto systems the oracle factors in
+    seconds: factors and the apply equal the reference bit for bit."""
+    monkeypatch.setenv("RHOSOLVE_ILU_CPS", str(cps))
+    H, c = model(name, **kw)
+    Lo = O.shift(oracle_L(H, c))
+    fwd, _ = O.rcm(Lo)
+    m = O.permute(Lo, fwd)
+    fo = O.factorize_raw(m, d, p)
+    f = factor.factor_batch(from_host([_host(m)] * nsys), d, p)
+    b = np.random.default_rng(4).standard_normal(m.n * nsys) + 0.1j
+    x = factor.solve_lu(f, b)
+    for s in range(nsys):
+        lp, li, lx, up, ui, ux, pinv = f.system_raw(s)
+        assert bits_equal(lp, fo.Lp) and bits_equal(up, fo.Up) and bits_equal(pinv, fo.pinv)
+        assert bits_equal(li, fo.Li) and bits_equal(ui, fo.Ui)
+        assert bits_equal(lx, fo.Lx) and bits_equal(ux, fo.Ux)
+        assert bits_equal(x[s * m.n:(s + 1) * m.n], fo.solve(b[s * m.n:(s + 1) * m.n]))

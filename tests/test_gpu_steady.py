@@ -103,3 +103,16 @@ def test_sharded_path_single_gpu_kerr_kerr(cuda):
     ref = O.inverse_power(oracle_L(H, c), 64, tol=1e-12, inner="direct", seed=3)
     assert res.residual <= 1e-10
     assert O.trace_distance(res.rho, ref["rho"]) <= 1e-6
+
+
+def test_c3_solve_direct(cuda):
+    """complete LU of the trace-modified optomechanics
+    Liouvillian (n = 57,600, fill ~184; multi-CTA factorization) -- the
+    reference needs 200-250 s for it."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c3.npz"))
+    H, c = model("c3")
+    L = liouville.build_liouvillian(H, c)
+    res = steady.solve_direct(L, ordering_name="rcm")
+    assert res.residual <= 1e-10
+    assert O.trace_distance(res.rho, g["power_bicgstab_rho"]) <= 1e-6
