@@ -35,6 +35,14 @@ def run(A, d, p, label):
 
 
 def main():
+    for name in ("c2", "c1"):
+        cc = configs.CONFIGS[name]
+        Lc = liouville.build_liouvillian(*cc["build"]())
+        shc = liouville.shift(Lc)
+        fc, ic = ordering.rcm_device(shc.matrix)
+        run(ordering.permute(shc.matrix, fc, ic), cc["d"], cc["p"], f"{name} ILUTP")
+    if os.environ.get("ONLY_SMALL"):
+        return
     c = configs.CONFIGS["c3"]
     L = liouville.build_liouvillian(*c["build"]())
     sh = liouville.shift(L)
