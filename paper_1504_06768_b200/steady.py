@@ -88,7 +88,14 @@ _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="rhosolve-rng")
 
 
 def _start_vectors(n, seeds):
-    return np.concatenate([start_vector(n, s) for s in seeds])
+    """The batch's start vectors drawn straight into pinned host memory, so
+    the upload is one asynchronous DMA."""
+    seeds = list(seeds)
+    out = torch.empty(len(seeds) * n, dtype=torch.complex128, pin_memory=True)
+    view = out.numpy()
+    for i, sd in enumerate(seeds):
+        view[i * n:(i + 1) * n] = start_vector(n, sd)
+    return out
 
 
 def _require_plain(L):
@@ -269,7 +276,7 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
         f = factor.factor_batch(mat, float(d), float(p), raise_on_fail=raise_errors)
         mode = _lib.INV_GMRES if solver == "gmres" else _lib.INV_BICGSTAB
     t2 = _sync()
-    x0 = torch.from_numpy(x0_future.result()).to(mat.values.device)
+    x0 = x0_future.result().to(mat.values.device, non_blocking=True)
     if not f.ok:  # some system of the batch failed to factor
         return None, f, None, None, label, (t0, t1, t2, _sync())
     x, st = _solve(mode, mat, plain, f, x0, tol, max_iter, restart_m, inner == "iterative",
