@@ -115,8 +115,9 @@ int rs_sell_build(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp,
 int rs_pivot_recip(int32_t nsys, int32_t n, const int32_t* Up, const rs_complex* Ux,
                    int64_t capU, rs_complex* rdiag, void* stream);
 
-/* 1 when systems of order n run the column-oriented sweeps (the sweep vector
- * and the factor staging ring fit one CTA's shared memory), else 0. */
+/* 1 when systems of order n run the column-oriented sweeps (the factor
+ * staging ring fits one CTA's shared memory; the sweep vector is kept there
+ * too when it fits, else in global memory), else 0. */
 int rs_col_sweep_supported(int32_t n);
 
 /* Column stream of one triangle of the raw CSC factors (rs_factorize) for

@@ -228,7 +228,10 @@ int rs_sell_build(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp,
   return sell_build(nsys, n, upper ? 1 : 0, rp, ci, C2(v), sptr, sci, M2(sv), total, S(stream));
 }
 
-int rs_col_sweep_supported(int32_t n) { return rs::col_ring_size(n, 1) > 0 ? 1 : 0; }
+int rs_col_sweep_supported(int32_t n) {
+  int yg = 0;
+  return (n > 0 && rs::col_plan(n, 1, &yg) > 0) ? 1 : 0;
+}
 
 int rs_pivot_recip(int32_t nsys, int32_t n, const int32_t* Up, const rs_complex* Ux,
                    int64_t capU, rs_complex* rdiag, void* stream) {
@@ -271,12 +274,16 @@ int rs_lu_solve_cols(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t
   a.pinv = pinv;
   a.rhs = C2(b);
   a.xout = M2(x);
-  a.ring_R = col_ring_size(n, nsys);
-  if (a.ring_R <= 0) {
-    set_error("lu_solve_cols: n=%d does not fit the column sweeps", n);
-    return RS_ERR_UNSUPPORTED;
+  a.ring_R = col_plan(n, nsys, &a.col_y_global);
+  cudaStream_t st = S(stream);
+  double2* work = nullptr;
+  if (a.col_y_global) {  // sweep vectors (+ dummy slot) in global memory
+    RS_CUDA_TRY(cudaMallocAsync(&work, sizeof(double2) * 2 * (size_t)n * nsys, st));
+    a.work = work;
   }
-  return launch_lu_solve(a, S(stream));
+  const int rc = launch_lu_solve(a, st);
+  if (work) cudaFreeAsync(work, st);
+  return rc;
 }
 
 int rs_lu_solve(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t* L_rp,
@@ -433,7 +440,7 @@ int rs_steady_solve(const rs_solver_args* p, void* stream) {
     a.Usv = C2(p->Us_val);
     a.Usm = p->Us_meta;
     a.Usr = C2(p->Us_rd);
-    a.ring_R = col_ring_size(a.n, a.B);
+    a.ring_R = col_plan(a.n, a.B, &a.col_y_global);
   }
   RS_CHECK_ARG(a.ring_R > 0 || a.Lrp != nullptr || p->Ls_rowoff == nullptr,
                "row-oriented factors required: n too large for the column sweeps");

@@ -109,6 +109,32 @@ __device__ __forceinline__ void sts2(unsigned a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// Where the sweep vector lives: shared memory (32-bit addresses) when it
+// fits the CTA, else global memory (the consumer warp is its only reader and
+// writer during a sweep, so L1 serves its re-reads; __syncwarp orders lanes).
+template <typename AT>
+struct YMem;
+template <>
+struct YMem<unsigned> {
+  __device__ static unsigned base(double2* y) { return saddr(y); }
+  __device__ static double2 ld(unsigned a) { return lds2(a); }
+  __device__ static void st(unsigned a, double2 v) { sts2(a, v); }
+};
+template <>
+struct YMem<unsigned long long> {
+  __device__ static unsigned long long base(double2* y) {
+    return reinterpret_cast<unsigned long long>(y);
+  }
+  __device__ static double2 ld(unsigned long long a) {
+    double2 v;
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(a));
+    return v;
+  }
+  __device__ static void st(unsigned long long a, double2 v) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(a), "d"(v.x), "d"(v.y) : "memory");
+  }
+};
+
 // All threads of the CTA: reset the ring before a sweep.
 __device__ __forceinline__ void col_ring_reset(const ColRing& g) {
   for (int s = threadIdx.x; s < g.S; s += blockDim.x) g.seq[s] = -1;
@@ -194,8 +220,9 @@ __device__ __forceinline__ void col_ring_produce(const ColRing& g, const ColStre
 }
 
 // One staged stream row in registers.
+template <typename AT>
 struct ColRow {
-  unsigned a0, a1;  // shared addresses of this lane's two y entries (dummy slot for padding)
+  AT a0, a1;        // addresses of this lane's two y entries (dummy slot for padding)
   double2 v0, v1;   // this lane's two factor entries
   double2 rd;       // recipc(U_cc) (U first rows)
   int cont;         // continues the previous column
@@ -222,18 +249,18 @@ __device__ __forceinline__ void col_row_raw(const ColRing& g, int r, ColRaw& x) 
   x.v1 = g.val[CW * slot + 32 + lane];
   if (UPPER) x.rd = g.rd[slot];
 }
-__device__ __forceinline__ void col_row_addr(const ColRaw& w, unsigned yb, unsigned dummy,
-                                             ColRow& x) {
+template <typename AT>
+__device__ __forceinline__ void col_row_addr(const ColRaw& w, AT yb, AT dummy, ColRow<AT>& x) {
   x.cont = w.seq & 1;
-  x.a0 = w.i0 >= 0 ? yb + 16u * w.i0 : dummy;
-  x.a1 = w.i1 >= 0 ? yb + 16u * w.i1 : dummy;
+  x.a0 = w.i0 >= 0 ? yb + (AT)16 * (AT)w.i0 : dummy;
+  x.a1 = w.i1 >= 0 ? yb + (AT)16 * (AT)w.i1 : dummy;
   x.v0 = w.v0;
   x.v1 = w.v1;
   x.rd = w.rd;
 }
-template <bool UPPER>
-__device__ __forceinline__ void col_row_load(const ColRing& g, int r, unsigned yb, unsigned dummy,
-                                             ColRow& x) {
+template <bool UPPER, typename AT>
+__device__ __forceinline__ void col_row_load(const ColRing& g, int r, AT yb, AT dummy,
+                                             ColRow<AT>& x) {
   ColRaw w;
   col_row_raw<UPPER>(g, r, w);
   col_row_addr(w, yb, dummy, x);
@@ -256,16 +283,17 @@ __device__ __forceinline__ int col_ring_ready(const ColRing& g, int r, int rows)
 // One consumer step: apply row r (cur) and stage row r+1 (nxt).  Order:
 // issue the y loads of row r, issue the raw ring loads of row r+1, do row
 // r's math and stores, then derive row r+1's addresses.
-template <bool UPPER>
-__device__ __forceinline__ void col_step(const ColRing& g, int r, int rows, unsigned yb,
-                                         unsigned dummy, int& c, double2& xc, int& ready,
-                                         const ColRow& cur, ColRow& nxt, long long* tt) {
+template <bool UPPER, typename AT>
+__device__ __forceinline__ void col_step(const ColRing& g, int r, int rows, AT yb, AT dummy,
+                                         int& c, double2& xc, int& ready,
+                                         const ColRow<AT>& cur, ColRow<AT>& nxt, long long* tt) {
+  using M = YMem<AT>;
   const int lane = threadIdx.x & 31;
   if (tt) tt[3 * r] = clock64();
   // first row of a column: xc = y[c'] (U: times recipc(U_cc), stored back)
   const int cn = cur.cont ? c : c + (UPPER ? -1 : 1);
-  double2 xn = lds2(yb + 16u * cn);
-  const double2 y0 = lds2(cur.a0), y1 = lds2(cur.a1);
+  double2 xn = M::ld(yb + (AT)16 * (AT)cn);
+  const double2 y0 = M::ld(cur.a0), y1 = M::ld(cur.a1);
   const bool more = r + 1 < rows;
   ColRaw w;
   if (more) {
@@ -276,9 +304,9 @@ __device__ __forceinline__ void col_step(const ColRing& g, int r, int rows, unsi
   if (UPPER) xn = cmul_plain(xn, cur.rd);
   xc = cur.cont ? xc : xn;
   c = cn;
-  if (UPPER && lane == 0 && !cur.cont) sts2(yb + 16u * cn, xc);
-  sts2(cur.a0, csub(y0, cmul_plain(cur.v0, xc)));
-  sts2(cur.a1, csub(y1, cmul_plain(cur.v1, xc)));
+  if (UPPER && lane == 0 && !cur.cont) M::st(yb + (AT)16 * (AT)cn, xc);
+  M::st(cur.a0, csub(y0, cmul_plain(cur.v0, xc)));
+  M::st(cur.a1, csub(y1, cmul_plain(cur.v1, xc)));
   __syncwarp();
   if (more) col_row_addr(w, yb, dummy, nxt);
   if (tt) tt[3 * r + 2] = clock64();
@@ -287,27 +315,28 @@ __device__ __forceinline__ void col_step(const ColRing& g, int r, int rows, unsi
 
 // Consumer warp: the whole sweep, in place on y (shared memory, with one
 // dummy slot after y[n-1] absorbing padding updates).
-template <bool UPPER>
+template <bool UPPER, typename AT>
 __device__ __forceinline__ void col_consume(int n, int rows, const ColRing& g, double2* y) {
   const int lane = threadIdx.x & 31;
-  const unsigned yb = saddr(y), dummy = yb + 16u * n;
+  const AT yb = YMem<AT>::base(y), dummy = yb + (AT)16 * (AT)n;
   long long* const tt = (!UPPER && blockIdx.x == 0 && lane == 0) ? g_col_times : nullptr;
   int c = UPPER ? n : -1;
   double2 xc = make_double2(0.0, 0.0);
   if (rows <= 0) return;
   int ready = col_ring_ready(g, 0, rows);
-  ColRow A, B;
-  col_row_load<UPPER>(g, 0, yb, dummy, A);
+  ColRow<AT> A, B;
+  col_row_load<UPPER, AT>(g, 0, yb, dummy, A);
   for (int r = 0; r < rows; r += 2) {  // unrolled by two: no register moves
-    col_step<UPPER>(g, r, rows, yb, dummy, c, xc, ready, A, B, tt);
+    col_step<UPPER, AT>(g, r, rows, yb, dummy, c, xc, ready, A, B, tt);
     if (r + 1 >= rows) break;
-    col_step<UPPER>(g, r + 1, rows, yb, dummy, c, xc, ready, B, A, tt);
+    col_step<UPPER, AT>(g, r + 1, rows, yb, dummy, c, xc, ready, B, A, tt);
   }
 }
 
 // CTA-level in-place M^{-1} sweeps on y (shared memory): warp 0 consumes,
 // warps 1..P produce.  Must be called by all threads (contains
 // __syncthreads).
+template <typename AT>
 __device__ __forceinline__ void col_lu_sweeps(int n, const ColStream& Ls, const ColStream& Us,
                                               const ColRing& g, double2* y) {
   const int wid = threadIdx.x >> 5;
@@ -315,12 +344,12 @@ __device__ __forceinline__ void col_lu_sweeps(int n, const ColStream& Ls, const 
   const int P = max(1, min(nw - 1, 8));
   col_ring_reset(g);
   __syncthreads();
-  if (wid == 0) col_consume<false>(n, Ls.rows, g, y);
+  if (wid == 0) col_consume<false, AT>(n, Ls.rows, g, y);
   else if (wid <= P) col_ring_produce(g, Ls, false, wid - 1, P);
   __syncthreads();
   col_ring_reset(g);
   __syncthreads();
-  if (wid == 0) col_consume<true>(n, Us.rows, g, y);
+  if (wid == 0) col_consume<true, AT>(n, Us.rows, g, y);
   else if (wid <= P) col_ring_produce(g, Us, true, wid - 1, P);
   __syncthreads();
 }

@@ -73,7 +73,8 @@ __device__ __noinline__ void csc_psolve(const SolverArgs* a, const double2* in, 
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a->n;
   const int64_t b = blockIdx.x;
-  double2* P = reinterpret_cast<double2*>(smem);
+  const bool yg = a->col_y_global != 0;  // sweep vector in global memory (large n)
+  double2* P = yg ? a->ywork + b * a->ywork_stride : reinterpret_cast<double2*>(smem);
   const int32_t* pinv = a->pinv + b * n;
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) P[pinv[i]] = in[i];
@@ -90,7 +91,9 @@ __device__ __noinline__ void csc_psolve(const SolverArgs* a, const double2* in, 
   Us.meta = a->Usm + u0;
   Us.rd = a->Usr + u0;
   Us.rows = a->Uso[b * n + n] - u0;
-  cta::col_lu_sweeps(n, Ls, Us, cta::col_ring_at(smem + cta::col_y_bytes(n), a->ring_R), P);
+  const cta::ColRing ring = cta::col_ring_at(smem + (yg ? 0 : cta::col_y_bytes(n)), a->ring_R);
+  if (yg) cta::col_lu_sweeps<unsigned long long>(n, Ls, Us, ring, P);
+  else cta::col_lu_sweeps<unsigned>(n, Ls, Us, ring, P);
   for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[i];
   __syncthreads();
 }
@@ -656,8 +659,9 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  size_t smem = a.ring_R > 0 ? cta::col_y_bytes(a.n) + cta::col_ring_bytes(a.ring_R)
-                             : (a.y_in_smem ? 32 * (size_t)a.n : 0);
+  size_t smem = a.ring_R > 0
+                    ? (a.col_y_global ? 0 : cta::col_y_bytes(a.n)) + cta::col_ring_bytes(a.ring_R)
+                    : (a.y_in_smem ? 32 * (size_t)a.n : 0);
   if (smem + 2048 > (size_t)max_smem) {
     set_error("steady solver: n=%d needs %zu B of shared memory", a.n, smem);
     return RS_ERR_UNSUPPORTED;
@@ -665,6 +669,8 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
   RS_CUDA_TRY(cudaFuncSetAttribute(steady_solver_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SolverArgs la = a;
+  la.ywork = a.work;  // slot 0 of each system's workspace (y, then y2 = dummy)
+  la.ywork_stride = a.work_stride;
   SolverArgs* dev_args = nullptr;
   if (la.ring_R > 0) {  // the out-of-line column sweeps read the arguments from here
     RS_CUDA_TRY(cudaMallocAsync(&dev_args, sizeof(SolverArgs), st));
@@ -827,14 +833,26 @@ int col_ring_size(int32_t n, int B) {
   return 0;
 }
 
+int col_plan(int32_t n, int B, int* y_global) {
+  const int S = col_ring_size(n, B);
+  if (S > 0) {
+    *y_global = 0;
+    return S;
+  }
+  // the sweep vector stays in global memory; the ring alone in shared
+  *y_global = 1;
+  return B > 148 ? 16 : 64;
+}
+
 int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
   if (a.B == 0 || a.n == 0) return RS_OK;
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int y_smem = 32 * (size_t)a.n + 2048 <= (size_t)max_smem;
-  size_t smem = a.ring_R > 0 ? cta::col_y_bytes(a.n) + cta::col_ring_bytes(a.ring_R)
-                             : (y_smem ? 32 * (size_t)a.n : 0);
+  size_t smem = a.ring_R > 0
+                    ? (a.col_y_global ? 0 : cta::col_y_bytes(a.n)) + cta::col_ring_bytes(a.ring_R)
+                    : (y_smem ? 32 * (size_t)a.n : 0);
   if (a.ring_R <= 0 && !y_smem && !a.work) {
     set_error("lu_solve: n=%d needs global scratch", a.n);
     return RS_ERR_UNSUPPORTED;
@@ -843,6 +861,8 @@ int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
                                    (int)smem));
   // column sweeps: 1 consumer + 4 producer warps; row sweeps: 16 warps
   SolverArgs la = a;
+  la.ywork = a.work;  // 2 n per system: y, then the dummy slot
+  la.ywork_stride = 2 * (int64_t)a.n;
   SolverArgs* dev_args = nullptr;
   if (la.ring_R > 0) {
     RS_CUDA_TRY(cudaMallocAsync(&dev_args, sizeof(SolverArgs), st));

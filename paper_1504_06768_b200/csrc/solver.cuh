@@ -79,12 +79,18 @@ struct SolverArgs {
   const int32_t* Usm;
   const double2* Usr;
   int32_t ring_R;  // > 0: column sweeps with a ring of ring_R 64-entry slots
+  int32_t col_y_global;    // column sweeps with the sweep vector in global memory
+  double2* ywork;          // global sweep vectors (set by the launcher)
+  int64_t ywork_stride;
   const SolverArgs* self;  // device copy of these arguments (set by the launcher)
 };
 
 // Ring size for the column sweeps of systems of order n in a launch of B
 // CTAs (0 = not supported: the sweep vector and ring do not fit).
 int col_ring_size(int32_t n, int B);
+// ring slots for the column sweeps; *y_global = 1 when the sweep vector
+// must stay in global memory (it does not fit next to the ring)
+int col_plan(int32_t n, int B, int* y_global);
 // column streams of one triangle (pass 1: idx == null -> rowoff + *total)
 int col_stream_build(int B, int32_t n, int upper, const int32_t* cp, const int32_t* ci,
                      const double2* cv, int64_t cap, const double2* rdiag, int32_t* rowoff,

@@ -57,6 +57,9 @@ def main(cfg, count=1):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        main(sys.argv[1])
+        raise SystemExit
     main("c1")
     main("c2")
     main("c4", 1)
