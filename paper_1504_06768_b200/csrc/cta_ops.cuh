@@ -58,46 +58,97 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return s;
 }
 
+// Deterministic CTA sums whose rounding does not depend on the CTA size:
+// elements are accumulated in the order of a 512-thread CTA (virtual thread
+// v takes i = v, v+512, ...; shuffle tree per virtual warp; virtual warps
+// summed 0..15 in order), each physical thread of a 128/256/512-thread CTA
+// playing 4/2/1 virtual threads.  A lone-system solve (256 threads) and a
+// batch (128 threads) therefore run the same arithmetic as a 512-thread CTA.
+constexpr int RED_T = 512;
+
+template <int K, int V, class F>
+__device__ __forceinline__ void vsum_impl(int n, F f, double (&out)[K], double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  double acc[V][K];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[j][k] = 0.0;
+    for (int i = threadIdx.x + j * blockDim.x; i < n; i += RED_T) f(i, acc[j]);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      for (int o = 16; o; o >>= 1) acc[j][k] = __dadd_rn(acc[j][k], __shfl_xor_sync(FULL, acc[j][k], o));
+  }
+  __syncthreads();  // protect red from a previous use
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+#pragma unroll
+      for (int k = 0; k < K; ++k) red[k * 32 + wid + j * nw] = acc[j][k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = red[k * 32];
+    for (int w = 1; w < RED_T / 32; ++w) s = __dadd_rn(s, red[k * 32 + w]);
+    out[k] = s;
+  }
+}
+
+template <int K, class F>
+__device__ __forceinline__ void vsum(int n, F f, double (&out)[K], double* red) {
+  if (blockDim.x >= RED_T) vsum_impl<K, 1>(n, f, out, red);
+  else if (blockDim.x * 2 >= RED_T) vsum_impl<K, 2>(n, f, out, red);
+  else vsum_impl<K, 4>(n, f, out, red);
+}
+
 // vdot(a, b) = sum conj(a_i) b_i  (numpy.vdot convention)
 __device__ __forceinline__ double2 vdot(int n, const double2* a, const double2* b,
                                         double* red) {
-  double acc[2] = {0.0, 0.0};
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double2 x = a[i], y = b[i];
-    acc[0] = __fma_rn(x.x, y.x, __fma_rn(x.y, y.y, acc[0]));
-    acc[1] = __fma_rn(x.x, y.y, __fma_rn(-x.y, y.x, acc[1]));
-  }
-  block_sum<2>(acc, red);
-  return make_double2(acc[0], acc[1]);
+  double out[2];
+  vsum<2>(
+      n,
+      [&](int i, double (&acc)[2]) {
+        const double2 x = a[i], y = b[i];
+        acc[0] = __fma_rn(x.x, y.x, __fma_rn(x.y, y.y, acc[0]));
+        acc[1] = __fma_rn(x.x, y.y, __fma_rn(-x.y, y.x, acc[1]));
+      },
+      out, red);
+  return make_double2(out[0], out[1]);
 }
 
 __device__ __forceinline__ double nrm2(int n, const double2* a, double* red) {
-  double acc[1] = {0.0};
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double2 x = a[i];
-    acc[0] = __fma_rn(x.x, x.x, __fma_rn(x.y, x.y, acc[0]));
-  }
-  block_sum<1>(acc, red);
-  return sqrt(acc[0]);
+  double out[1];
+  vsum<1>(
+      n,
+      [&](int i, double (&acc)[1]) {
+        const double2 x = a[i];
+        acc[0] = __fma_rn(x.x, x.x, __fma_rn(x.y, x.y, acc[0]));
+      },
+      out, red);
+  return sqrt(out[0]);
 }
 
 // ||b - A x||_2 without materialising the residual.
 __device__ __forceinline__ double resid_nrm2(int n, const int32_t* rp, const int32_t* ci,
                                              const double2* v, const double2* x,
                                              const double2* b, double* red) {
-  double acc[1] = {0.0};
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int p0 = rp[i], p1 = rp[i + 1];
-    double2 s = make_double2(0.0, 0.0);
-    if (p0 < p1) {
-      s = cmul_plain(v[p0], x[ci[p0]]);
-      for (int p = p0 + 1; p < p1; ++p) s = cadd(s, cmul_plain(v[p], x[ci[p]]));
-    }
-    const double2 r = csub(b[i], s);
-    acc[0] = __fma_rn(r.x, r.x, __fma_rn(r.y, r.y, acc[0]));
-  }
-  block_sum<1>(acc, red);
-  return sqrt(acc[0]);
+  double out[1];
+  vsum<1>(
+      n,
+      [&](int i, double (&acc)[1]) {
+        const int p0 = rp[i], p1 = rp[i + 1];
+        double2 s = make_double2(0.0, 0.0);
+        if (p0 < p1) {
+          s = cmul_plain(v[p0], x[ci[p0]]);
+          for (int p = p0 + 1; p < p1; ++p) s = cadd(s, cmul_plain(v[p], x[ci[p]]));
+        }
+        const double2 r = csub(b[i], s);
+        acc[0] = __fma_rn(r.x, r.x, __fma_rn(r.y, r.y, acc[0]));
+      },
+      out, red);
+  return sqrt(out[0]);
 }
 
 // y = A x, row-sequential (bit-exact with csr_matvec).  rp/ci local.

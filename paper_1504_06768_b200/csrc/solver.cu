@@ -457,7 +457,11 @@ __device__ IterOut gmres(const Ctx& C, const double2* b, const Vecs& W, double t
 
 }  // namespace
 
-__global__ void __launch_bounds__(512, 1) steady_solver_kernel(SolverArgs a) {
+// MAXT = 512: batches (128-thread CTAs, four per SM, 128 registers);
+// MAXT = 256: a lone system -- 255 registers, so the out-of-line
+// column-sweep consumer runs without spills (it spilled in the loop at 128).
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) steady_solver_kernel(SolverArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[32 * 4];
   const int b = blockIdx.x;
@@ -610,13 +614,15 @@ __global__ void __launch_bounds__(512, 1) steady_solver_kernel(SolverArgs a) {
       const double aov = cabs(ov);
       ph = make_double2(ov.x / aov, ov.y / aov);
     }
-    double acc[1] = {0.0};
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double2 al = ovnz ? cmul(y[i], ph) : y[i];
-      const double2 d = csub(al, xo[i]);
-      acc[0] = __fma_rn(d.x, d.x, __fma_rn(d.y, d.y, acc[0]));
-    }
-    cta::block_sum<1>(acc, red);
+    double acc[1];
+    cta::vsum<1>(
+        n,
+        [&](int i, double (&s)[1]) {
+          const double2 al = ovnz ? cmul(y[i], ph) : y[i];
+          const double2 d = csub(al, xo[i]);
+          s[0] = __fma_rn(d.x, d.x, __fma_rn(d.y, d.y, s[0]));
+        },
+        acc, red);
     const double diff = sqrt(acc[0]);
     // resid_inf = max |L_plain,perm y|
     double mx = 0.0;
@@ -666,8 +672,9 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
     set_error("steady solver: n=%d needs %zu B of shared memory", a.n, smem);
     return RS_ERR_UNSUPPORTED;
   }
-  RS_CUDA_TRY(cudaFuncSetAttribute(steady_solver_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const bool lone = a.threads <= 256 && a.B <= 148;
+  auto kern = lone ? steady_solver_kernel<256> : steady_solver_kernel<512>;
+  RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SolverArgs la = a;
   la.ywork = a.work;  // slot 0 of each system's workspace (y, then y2 = dummy)
   la.ywork_stride = a.work_stride;
@@ -677,7 +684,7 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
     RS_CUDA_TRY(cudaMemcpyAsync(dev_args, &la, sizeof(SolverArgs), cudaMemcpyHostToDevice, st));
     la.self = dev_args;
   }
-  steady_solver_kernel<<<a.B, a.threads, smem, st>>>(la); ::rs::count_launch();
+  kern<<<a.B, a.threads, smem, st>>>(la); ::rs::count_launch();
   if (dev_args) cudaFreeAsync(dev_args, st);
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;

@@ -130,8 +130,9 @@ def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0
     if not threads:
         # one CTA per system: big batches use 4-warp CTAs so four systems stay
         # resident per SM (one wave for the 512-instance sweep); a lone system
-        # gets 16 warps
-        threads = 128 if B > 148 else 512
+        # gets 8 warps and the 255-register kernel (the column-sweep consumer
+        # then runs without spills)
+        threads = 128 if B > 148 else 256
     x = torch.empty(B * n, dtype=torch.complex128, device=dev)
     stats = torch.zeros(B * _STATS_DT.itemsize, dtype=torch.uint8, device=dev)
     a = _lib.SolverArgs()
