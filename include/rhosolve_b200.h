@@ -57,6 +57,10 @@ const char* rs_last_error(void);
 /* Number of kernels this library has launched in the process (bench
  * bookkeeping: gpu_launches). */
 long long rs_launch_count(void);
+/* Number of systems the last rs_factorize call factored with the
+ * right-looking frontal kernel (complete LU whose front fits shared memory;
+ * opt-in with RHOSOLVE_FRONTAL=1; diagnostics and tests). */
+int rs_debug_frontal_taken(void);
 
 /* ---- kernel seam (kernels/__init__.py:19-36) ---------------------------- */
 

@@ -97,6 +97,9 @@ const char* rs_last_error(void) { return g_err; }
 long long rs_launch_count(void) { return g_launches.load(); }
 // Tuning hook (not part of the documented ABI): when set, the next
 // factorizations record per-column phase clocks of system 0 into buf[n*6].
+int rs_debug_frontal_taken(void) { return rs::frontal_last_taken(); }
+int rs_debug_frontal_probe(int enable, double* out4) { return rs::frontal_probe(enable, out4); }
+
 int rs_debug_factor_probe(void* buf) {
   g_factor_probe = reinterpret_cast<unsigned long long*>(buf);
   return 0;
@@ -198,6 +201,17 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.wkey = reinterpret_cast<uint64_t*>(ws + o_key);
   a.gctl = reinterpret_cast<int32_t*>(ws + o_ctl);
   a.probe = g_factor_probe;
+  // complete LU of small systems (the c4 sweep): right-looking frontal
+  // elimination in shared memory; whatever it does not take (front too large,
+  // zero pivot) runs through the column pipeline below
+  if (frontal_enabled() && !(drop_tol > 0.0) && fill_cap < 0 && !fill_caps && !q &&
+      !g_factor_probe) {
+    const int frc = frontal_factor(a, st);
+    if (frc) {
+      cudaFreeAsync(ws, st);
+      return frc;
+    }
+  }
   // prow is scratch: a resumed launch rebuilds it as the inverse of pinv.
   const int rc = launch_ilutp(a, st);
   cudaFreeAsync(ws, st);

@@ -1,0 +1,1131 @@
+// Right-looking frontal LU for systems whose active front fits one SM's
+// shared memory (the config-4 sweep: 512 systems).  Same
+// contract and bit-identical output as the reference `factorize` with
+// drop_tol = 0 and no cap (complete LU, _ckernels.pyx:144-385 via
+// factor.lu, factor.py:115-118), and as ilutp_pipeline_kernel<INC=false>.
+//
+// Why a right-looking elimination gives the reference's bits.  The
+// reference is left-looking: column k applies x[i] -= L[i,c] * x[prow c]
+// for every reachable pivotal c in ascending c.  Entry (i, k) therefore
+// receives exactly the products L[i,c] * U[c,k] of the structurally present
+// pairs, subtracted in ascending c, with every U[c,k] final when used.  A
+// right-looking elimination applies the same products to the same entry in
+// the same (ascending step) order, so every rounding is reproduced.  What
+// the column view also fixes -- the pivot (max |re|+|im| over non-pivotal
+// pattern rows, ties to the lowest original row), the L order (the column's
+// pattern discovery order) and U order (ascending pivotal row) -- is
+// reproduced explicitly:
+//   * structure is tracked exactly (a bit per front entry), so fill appears
+//     where the reference's pattern grows and nowhere else;
+//   * every front entry carries a discovery key: 0 for an entry of A (A's
+//     rows are scattered first, in ascending row order), else
+//     (step c that created it, position of its row in L column c) -- the
+//     reference appends a fill row when it first pops the c that reaches it,
+//     scanning L column c in storage order.  L column k is emitted sorted by
+//     (key, original row).
+//
+// The front.  Row i joins at step s_i = its first column in A (no update can
+// reach it earlier) and leaves when pivoted; column j joins when the first
+// row holding one of its A entries joins and leaves at step j.  The number
+// of active rows / columns at step k is therefore structural, so the front
+// size (max over k) is known before the elimination: a dense RS x CS tile of
+// complex128 in shared memory with slot maps (column slots assigned once by
+// interval colouring, row slots from a free mask at run time).  For the c4
+// systems (n = 1,600, RCM bandwidth 155) the front is 79 x 154 (222 KB with
+// keys and masks): a row's A entries reach ~155 columns right of its first.
+//
+// One CTA (16 warps) per system, three barriers per elimination step (see
+// frontal_lu_kernel).  U columns are compacted into the reference's CSC (Up prefix, pivot last)
+// and L rows remapped to pivotal order by frontal_finish_kernel.
+//
+// Systems that do not fit (front > 128 x 256, n >= 65,536, ...) and systems
+// that hit a zero pivot are left untouched (state 0) for the pipelined
+// kernel, which produces the reference's partial output on failure.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rs {
+
+namespace {
+
+constexpr int FT = 512;     // threads per CTA (all kernels here)
+constexpr int MAXR = 128;   // max row slots (4 mask words)
+constexpr int MAXC = 256;   // max column slots (8 mask words; slot ids fit u8)
+constexpr int MW = 8;       // column-mask words per row
+constexpr int MAXN = 16384; // column-slot map kept in shared memory (u8)
+constexpr int NINFO = 8;    // info words per system
+constexpr int MAX_EROWS = 256, MAX_ECOLS = 256, MAX_EENT = 512;  // joins per step
+constexpr unsigned FULL = 0xffffffffu;
+
+enum { I_OK = 0, I_RS, I_CS, I_LB, I_UB, I_DONE, I_SMEM };
+
+struct FrontWs {
+  int32_t n, B;
+  const int32_t* Ap;
+  const int32_t* Ai;
+  const double2* Ax;
+  const int32_t* state;
+  int64_t capL, capU;
+  // per system b (offset b*n, b*(n+1) or b*n*4)
+  int32_t* srow;   // first column of row i (n: empty row)
+  int32_t* rlen;   // entries of row i
+  int32_t* rfill;  // cursor per row (entry placement)
+  int32_t* ent;    // join step of column j
+  int32_t* hr;     // rows joining per step
+  int32_t* he;     // entries joining per step
+  int32_t* hc;     // columns joining per step
+  int32_t* erp;    // [n+1] rows joining per step (prefix)
+  int32_t* eep;    // [n+1] entries joining per step (prefix)
+  int32_t* ecp;    // [n+1] columns joining per step (prefix)
+  int32_t* ubase;  // [n+1] U staging base per column
+  int32_t* erow;   // joining rows, step order
+  int32_t* rloc;   // row i: rank among the rows joining at its step
+  int32_t* roff;   // row i: offset of its entries inside its step's block
+  uint32_t* emask; // [n*MW] joining row's column-slot mask
+  int32_t* ecol;   // joining columns, step order
+  uint8_t* ecs;    // joining columns: slot
+  int32_t* ecb;    // joining columns: U staging base
+  uint8_t* cslot;  // column slot of column j
+  uint32_t* eent;  // [nnz] (column slot << 16) | row rank; absolute CSC range
+  double2* eval;   // [nnz]
+  int32_t* info;   // [B*NINFO]
+};
+
+struct FrontArgs {
+  int32_t n, B;
+  const int32_t* erp;
+  const int32_t* eep;
+  const int32_t* ecp;
+  const int32_t* ubase;
+  const int32_t* erow;
+  const uint32_t* emask;
+  const int32_t* ecol;
+  const uint8_t* ecs;
+  const int32_t* ecb;
+  const uint8_t* cslot;
+  const uint32_t* eent;
+  const double2* eval;
+  const int32_t* Ap;  // only Ap[b*n] (entry stream base)
+  int32_t* info;
+  int32_t* ucount;   // [B*n] entries of U column k (incl. pivot)
+  int32_t* usi;      // [B*ustride] staged U rows (pivotal)
+  double2* usv;      // [B*ustride]
+  int64_t ustride;
+  int32_t* Lp;
+  int32_t* Li;
+  double2* Lx;
+  int64_t capL;
+  int32_t* Up;
+  int32_t* Ui;
+  double2* Ux;
+  int64_t capU;
+  int32_t* pinv;
+  int32_t* state;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Exclusive scan of in[0..m) into out[0..m] by the whole block; returns the
+// total.  sh: >= 33 ints of shared memory.
+__device__ int block_exscan(const int32_t* in, int32_t* out, int m, int* sh) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+  const int per = (m + blockDim.x - 1) / blockDim.x;
+  const int lo = min(m, t * per), hi = min(m, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; ++i) s += in[i];
+  int v = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < nw ? sh[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += u;
+    }
+    if (lane < nw) sh[lane] = x;
+    if (lane == 31) sh[32] = x;
+  }
+  __syncthreads();
+  int run = v - s + (w ? sh[w - 1] : 0);
+  for (int i = lo; i < hi; ++i) {
+    out[i] = run;
+    run += in[i];
+  }
+  const int total = sh[32];
+  if (t == 0) out[m] = total;
+  __syncthreads();
+  return total;
+}
+
+// Stable bucketing of keys[0..m) (bucket < nb, or >= nb: skipped) by one
+// warp: out[base[k] + rank] = i, rank_out[i] = rank within its bucket, and
+// (optional) off_out[i] = sum of w[] over earlier members of its bucket.
+// cur / curw: zeroed per-bucket cursors.
+__device__ void warp_bucket(const int32_t* keys, int m, int nb, const int32_t* base, int32_t* out,
+                            int32_t* rank_out, const int32_t* w, int32_t* off_out, int32_t* cur,
+                            int32_t* curw) {
+  const int lane = threadIdx.x & 31;
+  for (int b0 = 0; b0 < m; b0 += 32) {
+    const int i = b0 + lane;
+    const int key = i < m ? keys[i] : nb;
+    const bool valid = key < nb;
+    const unsigned act = __ballot_sync(FULL, valid);
+    if (valid) {
+      const unsigned grp = __match_any_sync(act, key);
+      const int r = __popc(grp & lanemask_lt());
+      const int c0 = cur[key];
+      int wo = 0;
+      if (w) {
+        const int c1 = curw[key];
+        unsigned g = grp & lanemask_lt();
+        while (g) {
+          const int l = __ffs(g) - 1;
+          g &= g - 1;
+          wo += w[b0 + l];
+        }
+        off_out[i] = c1 + wo;
+      }
+      out[base[key] + c0 + r] = i;
+      if (rank_out) rank_out[i] = c0 + r;
+      __syncwarp(act);
+      // the highest lane of the group publishes the new cursors
+      if ((grp >> lane) == 1u) {
+        cur[key] = c0 + r + 1;
+        if (w) curw[key] = curw[key] + wo + w[i];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Structural analysis of one system per CTA: join steps, join streams,
+// column slots, front size, storage bounds.  Everything here depends on the
+// pattern of A only.
+__global__ void __launch_bounds__(FT) frontal_analyze_kernel(FrontWs w) {
+  __shared__ int sh[40];
+  __shared__ int red[8];
+  const int b = blockIdx.x, t = threadIdx.x;
+  const int n = w.n;
+  int32_t* info = w.info + (int64_t)b * NINFO;
+  if (w.state[3 * b] != 0) {  // resumed / finished systems: not ours
+    if (t == 0) info[I_OK] = 0;
+    return;
+  }
+  const int64_t bn = (int64_t)b * n, bn1 = (int64_t)b * (n + 1);
+  const int32_t* Ap = w.Ap + bn;
+  const int32_t* Ai = w.Ai;
+  int32_t *srow = w.srow + bn, *rlen = w.rlen + bn, *rfill = w.rfill + bn, *ent = w.ent + bn;
+  int32_t *hr = w.hr + bn, *he = w.he + bn, *hc = w.hc + bn;
+  int32_t *erp = w.erp + bn1, *eep = w.eep + bn1, *ecp = w.ecp + bn1, *ubase = w.ubase + bn1;
+  int32_t *erow = w.erow + bn, *rloc = w.rloc + bn, *roff = w.roff + bn, *ecol = w.ecol + bn;
+  uint32_t* emask = w.emask + MW * bn;
+  uint8_t* cslot = w.cslot + bn;
+  const int64_t base = Ap[0];
+  for (int i = t; i < n; i += FT) {
+    srow[i] = n;
+    rlen[i] = 0;
+    rfill[i] = 0;
+    hr[i] = he[i] = hc[i] = 0;
+  }
+  for (int i = t; i < MW * n; i += FT) emask[i] = 0;
+  if (t < 8) red[t] = 0;
+  __syncthreads();
+  // s_i = first column of row i; row lengths
+  for (int j = t; j < n; j += FT)
+    for (int64_t p = Ap[j]; p < Ap[j + 1]; ++p) {
+      atomicMin(&srow[Ai[p]], j);
+      atomicAdd(&rlen[Ai[p]], 1);
+    }
+  __syncthreads();
+  // column join step = min s_i over its rows; histograms per step
+  int bad = 0, maxspan = 0;
+  for (int j = t; j < n; j += FT) {
+    int e = n;
+    for (int64_t p = Ap[j]; p < Ap[j + 1]; ++p) e = min(e, srow[Ai[p]]);
+    ent[j] = e;
+    if (e > j) bad = 1;  // empty column: no pivot at step j
+    else {
+      atomicAdd(&hc[e], 1);
+      maxspan = max(maxspan, j - e);
+    }
+  }
+  for (int i = t; i < n; i += FT) {
+    const int s = srow[i];
+    if (s < n) {
+      atomicAdd(&hr[s], 1);
+      atomicAdd(&he[s], rlen[i]);
+    }
+  }
+  if (bad) atomicOr(&red[0], 1);
+  atomicMax(&red[1], maxspan);
+  __syncthreads();
+  // prefix streams; U staging base = sum of column spans (j - ent_j + 1)
+  block_exscan(hr, erp, n, sh);
+  block_exscan(he, eep, n, sh);
+  block_exscan(hc, ecp, n, sh);
+  for (int j = t; j < n; j += FT) rfill[j] = ent[j] <= j ? j - ent[j] + 1 : 0;  // temp: spans
+  __syncthreads();
+  const int ub = block_exscan(rfill, ubase, n, sh);
+  // front size: active rows / columns at step k (rows joined minus pivoted)
+  int rs = 0, cs = 0, jr = 0, jc = 0, je = 0;
+  long long lb = 0;
+  for (int k = t; k < n; k += FT) {
+    const int ar = erp[k + 1] - k, ac = ecp[k + 1] - k;
+    // rows joining at step k+1 are written while step k's pivot row still
+    // holds its slot: one more row slot than the active rows of step k+1
+    rs = max(rs, max(ar, erp[min(k + 2, n)] - k));
+    cs = max(cs, ac);
+    lb += ar > 0 ? ar : 0;
+    jr = max(jr, hr[k]);
+    jc = max(jc, hc[k]);
+    je = max(je, he[k]);
+  }
+  atomicMax(&red[2], rs);
+  atomicMax(&red[3], cs);
+  atomicMax(&red[4], jr);
+  atomicMax(&red[5], jc);
+  atomicMax(&red[6], je);
+  for (int o = 16; o; o >>= 1) lb += __shfl_xor_sync(FULL, lb, o);
+  __shared__ unsigned long long lbsum;
+  if (t == 0) lbsum = 0;
+  __syncthreads();
+  if ((t & 31) == 0) atomicAdd(&lbsum, (unsigned long long)lb);
+  // the histograms become the bucketing cursors; rfill the per-row cursor
+  for (int i = t; i < n; i += FT) rfill[i] = hr[i] = he[i] = hc[i] = 0;
+  __syncthreads();
+  const int RS = red[2], CS = red[3];
+  const bool ok = !red[0] && RS <= MAXR && CS <= MAXC && red[1] <= 255 && n < 65536 &&
+                  n <= MAXN && red[4] <= MAX_EROWS && red[5] <= MAX_ECOLS &&
+                  red[6] <= MAX_EENT && (long long)lbsum <= w.capL && (long long)ub <= w.capU &&
+                  erp[n] == n;
+  if (!ok) {
+    if (t == 0) info[I_OK] = 0;
+    return;
+  }
+  // stable join order: rows by s_i (with entry offsets), columns by join step
+  if (t < 32) {
+    warp_bucket(srow, n, n, erp, erow, rloc, rlen, roff, hr, he);  // hr/he reused as cursors
+  } else if (t < 64) {
+    warp_bucket(ent, n, n, ecp, ecol, nullptr, nullptr, nullptr, hc, nullptr);
+  }
+  __syncthreads();
+  // column slots: interval colouring in join order, lowest free slot first
+  if (t == 0) {
+    uint32_t fm[MW] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    for (int k = 0; k < n; ++k) {
+      if (k > 0) {
+        const int s = cslot[k - 1];
+        fm[s >> 5] &= ~(1u << (s & 31));
+      }
+      for (int q = ecp[k]; q < ecp[k + 1]; ++q) {
+        int s = 0;
+        for (int wd = 0; wd < MW; ++wd)
+          if (~fm[wd]) {
+            s = 32 * wd + __ffs(~fm[wd]) - 1;
+            break;
+          }
+        fm[s >> 5] |= 1u << (s & 31);
+        cslot[ecol[q]] = (uint8_t)s;
+      }
+    }
+  }
+  __syncthreads();
+  for (int q = t; q < n; q += FT) {
+    const int j = w.ecol[bn + q];
+    w.ecs[bn + q] = cslot[j];
+    w.ecb[bn + q] = ubase[j];
+  }
+  // joining entries: (column slot, row rank) + value in step order; row masks
+  for (int j = t; j < n; j += FT) {
+    const int s = cslot[j];
+    for (int64_t p = Ap[j]; p < Ap[j + 1]; ++p) {
+      const int i = Ai[p];
+      const int st = srow[i];
+      const int q = atomicAdd(&rfill[i], 1);
+      const int64_t pos = base + eep[st] + roff[i] + q;
+      w.eent[pos] = ((uint32_t)s << 16) | (uint32_t)rloc[i];
+      w.eval[pos] = w.Ax[p];
+      atomicOr(&emask[MW * (erp[st] + rloc[i]) + (s >> 5)], 1u << (s & 31));
+    }
+  }
+  if (t == 0) {
+    info[I_OK] = 1;
+    info[I_RS] = RS;
+    info[I_CS] = CS;
+    info[I_LB] = (int)lbsum;
+    info[I_UB] = ub;
+    info[I_DONE] = 0;
+  }
+}
+
+// Shared-memory layout of one system's front (byte offsets; the front F is
+// first so its address is the window base).
+struct SmemLayout {
+  uint32_t K, M, Pre, rowid, CKc, Ls, Lv, colid, ucnt, cbase, Uc, misc, total;
+};
+
+__host__ __device__ inline SmemLayout frontal_layout(int RS, int CS) {
+  SmemLayout L{};
+  uint32_t b = 0;
+  auto take = [&](uint32_t x) {
+    const uint32_t o = b;
+    b += (x + 15u) & ~15u;
+    return o;
+  };
+  take(16u * RS * CS);         // F   [RS][CS] complex128 front values (0 where absent)
+  L.K = take(2u * RS * CS);    // K   [RS][CS] discovery keys (0xffff: absent)
+  L.M = take(4u * MW * RS);    // M   [RS][MW] column-slot structure mask per row slot
+  L.Pre = take(2u * MW * RS);  // per candidate row: mask bits below each word (u16)
+  L.rowid = take(4u * RS);     // original row of a row slot (-1: free)
+  L.CKc = take(4u * 128);      // candidate keys of column k, 32 per row warp (padded)
+  L.Ls = take(4u * RS);        // L column k by rank: (slot << 24) | slot * CS
+  L.Lv = take(16u * RS);       // L column k: value by rank
+  L.colid = take(2u * CS);     // column held by a column slot
+  L.ucnt = take(2u * CS);      // U entries staged so far for that column
+  L.cbase = take(4u * CS);     // staging base of that column
+  L.Uc = take(CS);             // U row k: column slots, ascending
+  L.misc = take(8 * 4 + 4 * 4 + 4 * 4 + 4 * 4 + 16);
+  L.total = b;
+  return L;
+}
+
+__host__ __device__ inline size_t frontal_smem_bytes(int RS, int CS, int n) {
+  (void)n;
+  return frontal_layout(RS, CS).total;
+}
+
+// free row slots: a 128-bit mask replicated in every thread
+struct FreeMask {
+  uint32_t w0, w1, w2, w3;
+};
+
+__device__ __forceinline__ uint32_t pick4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                          int w) {
+  return w == 0 ? a0 : w == 1 ? a1 : w == 2 ? a2 : a3;
+}
+
+// slot of the r-th (0-based) free slot
+__device__ __forceinline__ int fm_nth(FreeMask f, int r) {
+  const int c0 = __popc(f.w0), c1 = __popc(f.w1), c2 = __popc(f.w2);
+  if (r < c0) return (int)__fns(f.w0, 0, r + 1);
+  r -= c0;
+  if (r < c1) return 32 + (int)__fns(f.w1, 0, r + 1);
+  r -= c1;
+  if (r < c2) return 64 + (int)__fns(f.w2, 0, r + 1);
+  r -= c2;
+  return 96 + (int)__fns(f.w3, 0, r + 1);
+}
+
+// rank of slot s among the free slots (valid when s is free)
+__device__ __forceinline__ int fm_rank(FreeMask f, int s) {
+  const int w = s >> 5;
+  const uint32_t below = (1u << (s & 31)) - 1u;
+  int r = __popc(pick4(f.w0, f.w1, f.w2, f.w3, w) & below);
+  if (w > 0) r += __popc(f.w0);
+  if (w > 1) r += __popc(f.w1);
+  if (w > 2) r += __popc(f.w2);
+  return r;
+}
+
+__device__ __forceinline__ bool fm_has(FreeMask f, int s) {
+  return (pick4(f.w0, f.w1, f.w2, f.w3, s >> 5) >> (s & 31)) & 1u;
+}
+
+__device__ __forceinline__ FreeMask fm_set(FreeMask f, int s) {
+  const uint32_t bit = 1u << (s & 31);
+  switch (s >> 5) {
+    case 0: f.w0 |= bit; break;
+    case 1: f.w1 |= bit; break;
+    case 2: f.w2 |= bit; break;
+    default: f.w3 |= bit; break;
+  }
+  return f;
+}
+
+// the e lowest free slots leave the mask
+__device__ __forceinline__ FreeMask fm_take(FreeMask f, int e) {
+  for (int r = 0; r < e; ++r) {
+    if (f.w0) f.w0 &= f.w0 - 1;
+    else if (f.w1) f.w1 &= f.w1 - 1;
+    else if (f.w2) f.w2 &= f.w2 - 1;
+    else f.w3 &= f.w3 - 1;
+  }
+  return f;
+}
+
+// tuning probe: per-phase clocks of CTA 0 (rs_debug_frontal_probe)
+__device__ long long g_fprobe[5];
+__device__ long long g_fwarp[16 * 3];  // per-warp busy cycles per phase (CTA 0)
+__device__ int g_fprobe_on;
+__device__ int g_fdebug;  // tuning: 1 skip the update, 2 skip L/U emission
+
+// Three barriers per elimination step k:
+//   P1  row warps: apply step k-1's structure change to their slot (mask |=
+//       U pattern for L rows, column k-1 leaves: its entries are zeroed),
+//       then column k's pivot candidates, discovery keys and warp argmax;
+//       warps 4-7 clear the row of step k-1's pivot (free slots hold zeros);
+//       loader warps prefetch the rows / entries / columns joining at k+1
+//   P2  pivot, L column (row warps rank by key and scale), U row (one thread
+//       per column slot, staged per column in global memory)
+//   P3  rank-1 update of the front (all warps): F -= l u on every pair, key =
+//       min(key, creation key) -- absent entries hold exactly +0 and 0xffff,
+//       so a fill starts from 0 - l u as in the reference; loaders then write
+//       the rows joining at step k+1 into free slots (never the pivot row,
+//       which the update still reads)
+__global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ int s_jrows;  // rows joining at step k+1 (published in P1)
+  const int b = blockIdx.x;
+  int32_t* info = a.info + (int64_t)b * NINFO;
+  if (!info[I_OK]) return;
+  const int n = a.n, RS = info[I_RS], CS = info[I_CS], CSP = CS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const SmemLayout SL = frontal_layout(RS, CS);
+  double2* const sF = reinterpret_cast<double2*>(smraw);
+  uint16_t* const sK = reinterpret_cast<uint16_t*>(smraw + SL.K);
+  uint32_t* const sM = reinterpret_cast<uint32_t*>(smraw + SL.M);
+  int32_t* const sRow = reinterpret_cast<int32_t*>(smraw + SL.rowid);
+  uint32_t* const sCKc = reinterpret_cast<uint32_t*>(smraw + SL.CKc);
+  uint32_t* const sLs = reinterpret_cast<uint32_t*>(smraw + SL.Ls);
+  double2* const sLv = reinterpret_cast<double2*>(smraw + SL.Lv);
+  uint16_t* const sColid = reinterpret_cast<uint16_t*>(smraw + SL.colid);
+  uint16_t* const sUcnt = reinterpret_cast<uint16_t*>(smraw + SL.ucnt);
+  int32_t* const sCbase = reinterpret_cast<int32_t*>(smraw + SL.cbase);
+  uint8_t* const sUc = smraw + SL.Uc;
+  double* const sWmag = reinterpret_cast<double*>(smraw + SL.misc);
+  int32_t* const sWrid = reinterpret_cast<int32_t*>(smraw + SL.misc + 32);
+  int32_t* const sWslot = reinterpret_cast<int32_t*>(smraw + SL.misc + 48);
+  uint32_t* const sCb = reinterpret_cast<uint32_t*>(smraw + SL.misc + 64);
+  int32_t* const sCnt = reinterpret_cast<int32_t*>(smraw + SL.misc + 80);
+  uint16_t* const sPre = reinterpret_cast<uint16_t*>(smraw + SL.Pre);
+
+  const int64_t bn = (int64_t)b * n, bn1 = (int64_t)b * (n + 1);
+  const int32_t* erp = a.erp + bn1;
+  const int32_t* eep = a.eep + bn1;
+  const int32_t* ecp = a.ecp + bn1;
+  const int32_t* erow = a.erow + bn;
+  const uint32_t* emask = a.emask + MW * bn;
+  const int32_t* ecol = a.ecol + bn;
+  const uint8_t* ecs = a.ecs + bn;
+  const int32_t* ecb = a.ecb + bn;
+  const uint8_t* cslot = a.cslot + bn;
+  const int64_t ebase = a.Ap[bn];
+  const uint32_t* eent = a.eent + ebase;
+  const double2* evl = a.eval + ebase;
+  int32_t* Lp = a.Lp + bn1;
+  int32_t* Li = a.Li + (int64_t)b * a.capL;
+  double2* Lx = a.Lx + (int64_t)b * a.capL;
+  int32_t* pinv = a.pinv + bn;
+  int32_t* ucount = a.ucount + bn;
+  int32_t* usi = a.usi + (int64_t)b * a.ustride;
+  double2* usv = a.usv + (int64_t)b * a.ustride;
+
+  // empty front: zeros and absent keys everywhere
+  for (int i = tid; i < RS * CSP; i += FT) {
+    sF[i] = make_double2(0.0, 0.0);
+    sK[i] = 0xffff;
+  }
+  for (int i = tid; i < RS; i += FT) {
+    sRow[i] = -1;
+    for (int wd = 0; wd < MW; ++wd) sM[MW * i + wd] = 0u;
+  }
+  if (tid == 0) Lp[0] = 0;
+  FreeMask fm;
+  {
+    auto full = [&](int lo) { return RS >= lo + 32 ? FULL : (RS > lo ? (1u << (RS - lo)) - 1u : 0u); };
+    fm.w0 = full(0);
+    fm.w1 = full(32);
+    fm.w2 = full(64);
+    fm.w3 = full(96);
+  }
+  __syncthreads();
+
+  // ---- joining rows / entries / columns: prefetched by loader warps 8..15 ----
+  const bool loader = warp >= 8;
+  const int lt = tid - 256;  // loader index
+  int erp1 = 0, erp2 = 0, eep1 = 0, eep2 = 0, ecp1 = 0, ecp2 = 0;
+  int pr_row = -1;
+  uint4 pr_m0 = make_uint4(0u, 0u, 0u, 0u), pr_m1 = pr_m0;
+  uint32_t pr_e0 = 0, pr_e1 = 0;
+  double2 pr_v0 = make_double2(0, 0), pr_v1 = make_double2(0, 0);
+  int pr_col = -1, pr_cb = 0, pr_cs = 0;
+  int ne_rows = 0, ne_ent = 0;
+#define FR_PREFETCH()                                                                  \
+  do {                                                                                 \
+    ne_rows = erp2 - erp1;                                                             \
+    ne_ent = eep2 - eep1;                                                              \
+    const int ne_cols = ecp2 - ecp1;                                                   \
+    pr_row = -1;                                                                       \
+    if (lt < ne_rows) {                                                                \
+      pr_row = erow[erp1 + lt];                                                        \
+      const uint4* mp = reinterpret_cast<const uint4*>(emask + MW * (int64_t)(erp1 + lt)); \
+      pr_m0 = mp[0];                                                                   \
+      pr_m1 = mp[1];                                                                   \
+    }                                                                                  \
+    if (lt < ne_ent) {                                                                 \
+      pr_e0 = eent[eep1 + lt];                                                         \
+      pr_v0 = evl[eep1 + lt];                                                          \
+    }                                                                                  \
+    if (lt + 256 < ne_ent) {                                                           \
+      pr_e1 = eent[eep1 + lt + 256];                                                   \
+      pr_v1 = evl[eep1 + lt + 256];                                                    \
+    }                                                                                  \
+    pr_col = -1;                                                                       \
+    if (lt < ne_cols) {                                                                \
+      pr_col = ecol[ecp1 + lt];                                                        \
+      pr_cb = ecb[ecp1 + lt];                                                          \
+      pr_cs = ecs[ecp1 + lt];                                                          \
+    }                                                                                  \
+  } while (0)
+#define FR_ADVANCE(kk)         \
+  do {                         \
+    erp1 = erp2;               \
+    eep1 = eep2;               \
+    ecp1 = ecp2;               \
+    if ((kk) + 2 <= n) {       \
+      erp2 = erp[(kk) + 2];    \
+      eep2 = eep[(kk) + 2];    \
+      ecp2 = ecp[(kk) + 2];    \
+    }                          \
+  } while (0)
+  // loaders write the prefetched payload into the lowest free slots of fm
+#define FR_JOIN()                                                      \
+  do {                                                                 \
+    if (loader) {                                                      \
+      if (pr_row >= 0) {                                               \
+        const int slot = fm_nth(fm, lt);                               \
+        sRow[slot] = pr_row;                                           \
+        uint4* mp = reinterpret_cast<uint4*>(sM + MW * slot);          \
+        mp[0] = pr_m0;                                                 \
+        mp[1] = pr_m1;                                                 \
+      }                                                                \
+      if (lt < ne_ent) {                                               \
+        const int slot = fm_nth(fm, (int)(pr_e0 & 0xffffu));           \
+        const int c = (int)(pr_e0 >> 16);                              \
+        sF[slot * CSP + c] = pr_v0;                                    \
+        sK[slot * CSP + c] = 0;                                        \
+      }                                                                \
+      if (lt + 256 < ne_ent) {                                         \
+        const int slot = fm_nth(fm, (int)(pr_e1 & 0xffffu));           \
+        const int c = (int)(pr_e1 >> 16);                              \
+        sF[slot * CSP + c] = pr_v1;                                    \
+        sK[slot * CSP + c] = 0;                                        \
+      }                                                                \
+      if (pr_col >= 0) {                                               \
+        sColid[pr_cs] = (uint16_t)pr_col;                              \
+        sUcnt[pr_cs] = 0;                                              \
+        sCbase[pr_cs] = pr_cb;                                         \
+      }                                                                \
+    }                                                                  \
+  } while (0)
+
+  bool joined = false;  // row threads: the slot received a row in the last join
+  {  // prologue: step 0's joins
+    const int e0 = erp[1] - erp[0];
+    if (loader) {
+      erp2 = erp[0];
+      eep2 = eep[0];
+      ecp2 = ecp[0];
+      FR_ADVANCE(-1);  // prefixes of steps 0 .. 1
+      FR_PREFETCH();
+      FR_ADVANCE(0);   // prefixes of steps 1 .. 2
+    }
+    FR_JOIN();
+    joined = tid < RS && e0 && fm_has(fm, tid) && fm_rank(fm, tid) < e0;
+    fm = fm_take(fm, e0);
+  }
+  int ck = cslot[0];
+  __syncthreads();
+
+  // step k-1 state carried in registers
+  int p_prev = -1, ck_prev = 0;
+  uint32_t um[MW];
+#pragma unroll
+  for (int wd = 0; wd < MW; ++wd) um[wd] = 0u;
+  uint32_t cb0 = 0, cb1 = 0, cb2 = 0, cb3 = 0;
+  int lnnz = 0;
+  bool failed = false;
+  const bool probe = g_fprobe_on && b == 0 && tid == 0;
+  const bool wprobe = g_fprobe_on && b == 0 && lane == 0;
+  long long pc[4] = {0, 0, 0, 0}, t0 = clock64();
+  long long wb0 = 0, wb1 = 0, wb2 = 0, tw = clock64();
+  for (int k = 0; k < n; ++k) {
+    const int ck_next = k + 1 < n ? cslot[k + 1] : 0;  // used next step
+    // ---------------- P1 ----------------
+    if (warp < 4) {
+      const int sl = tid;
+      bool cand = false;
+      double mag = -1.0;
+      int rid = 0x7fffffff;
+      uint32_t key = 0xffffffffu;
+      if (sl < RS) {
+        int r = sRow[sl];
+        if (p_prev >= 0 && !joined && r >= 0) {  // step k-1's structure change
+          uint4* mp = reinterpret_cast<uint4*>(sM + MW * sl);
+          if (sl == p_prev) {  // (its values are cleared by warps 4-7)
+            r = -1;
+            sRow[sl] = -1;
+            mp[0] = make_uint4(0u, 0u, 0u, 0u);
+            mp[1] = make_uint4(0u, 0u, 0u, 0u);
+          } else {
+            uint4 m0 = mp[0], m1 = mp[1];
+            if ((pick4(cb0, cb1, cb2, cb3, warp) >> lane) & 1u) {
+              m0.x |= um[0];
+              m0.y |= um[1];
+              m0.z |= um[2];
+              m0.w |= um[3];
+              m1.x |= um[4];
+              m1.y |= um[5];
+              m1.z |= um[6];
+              m1.w |= um[7];
+            }
+            const uint32_t pb = ~(1u << (ck_prev & 31));
+            switch (ck_prev >> 5) {
+              case 0: m0.x &= pb; break;
+              case 1: m0.y &= pb; break;
+              case 2: m0.z &= pb; break;
+              case 3: m0.w &= pb; break;
+              case 4: m1.x &= pb; break;
+              case 5: m1.y &= pb; break;
+              case 6: m1.z &= pb; break;
+              default: m1.w &= pb; break;
+            }
+            mp[0] = m0;
+            mp[1] = m1;
+            sF[sl * CSP + ck_prev] = make_double2(0.0, 0.0);  // column k-1 leaves
+            sK[sl * CSP + ck_prev] = 0xffff;
+          }
+        }
+        if (r >= 0) {
+          const uint32_t kk = sK[sl * CSP + ck];
+          if (kk != 0xffffu) {
+            cand = true;
+            {  // bits below each mask word (the U row positions if this row pivots)
+              const uint4* mq = reinterpret_cast<const uint4*>(sM + MW * sl);
+              const uint4 q0 = mq[0], q1 = mq[1];
+              const uint32_t a0 = __popc(q0.x), a1 = a0 + __popc(q0.y), a2 = a1 + __popc(q0.z),
+                             a3 = a2 + __popc(q0.w), a4 = a3 + __popc(q1.x),
+                             a5 = a4 + __popc(q1.y), a6 = a5 + __popc(q1.z),
+                             a7 = a6 + __popc(q1.w);
+              uint4* pp = reinterpret_cast<uint4*>(sPre + MW * sl);
+              // (u16 pairs: word w's prefix at index w; the total at index 8 of the
+              // next row is not needed: total = a7)
+              *pp = make_uint4(a0 << 16, a1 | (a2 << 16), a3 | (a4 << 16), a5 | (a6 << 16));
+              (void)a7;
+            }
+            key = (kk << 16) | (uint32_t)r;
+            const double m = cabs1(sF[sl * CSP + ck]);
+            if (!(m != m)) {  // NaN never wins (the reference's comparisons fail)
+              mag = m;
+              rid = r;
+            }
+          }
+        }
+      }
+      const unsigned bal = __ballot_sync(FULL, cand);
+      const unsigned lt_mask = lanemask_lt();
+      // compacted keys: candidates first, padding 0xffffffff after
+      const int pos = cand ? __popc(bal & lt_mask) : __popc(bal) + __popc(~bal & lt_mask);
+      sCKc[32 * warp + pos] = key;
+      int bs = sl;
+      for (int o = 16; o; o >>= 1) {
+        const double om = __shfl_xor_sync(FULL, mag, o);
+        const int orr = __shfl_xor_sync(FULL, rid, o);
+        const int os = __shfl_xor_sync(FULL, bs, o);
+        if (om > mag || (om == mag && orr < rid)) {
+          mag = om;
+          rid = orr;
+          bs = os;
+        }
+      }
+      if (lane == 0) {
+        sCb[warp] = bal;
+        sCnt[warp] = __popc(bal);
+        sWmag[warp] = mag;
+        sWrid[warp] = rid;
+        sWslot[warp] = bs;
+      }
+    } else if (warp < 8) {
+      if (p_prev >= 0)  // the freed pivot row returns to zeros / absent
+        for (int c = tid - 128; c < CS; c += 128) {
+          sF[p_prev * CSP + c] = make_double2(0.0, 0.0);
+          sK[p_prev * CSP + c] = 0xffff;
+        }
+    } else if (k + 1 < n) {  // loaders
+      FR_PREFETCH();
+      FR_ADVANCE(k + 1);
+      if (lt == 0) s_jrows = ne_rows;
+    }
+    if (p_prev >= 0) fm = fm_set(fm, p_prev);
+    if (wprobe) wb0 += clock64() - tw;
+    __syncthreads();  // S1
+    if (wprobe) tw = clock64();
+    if (probe) { const long long t = clock64(); pc[0] += t - t0; t0 = t; }
+    // ---------------- P2: pivot, L column, U row ----------------
+    double pmag = sWmag[0];
+    int prid = sWrid[0], p = sWslot[0];
+#pragma unroll
+    for (int wv = 1; wv < 4; ++wv) {
+      const double om = sWmag[wv];
+      const int orr = sWrid[wv];
+      if (om > pmag || (om == pmag && orr < prid)) {
+        pmag = om;
+        prid = orr;
+        p = sWslot[wv];
+      }
+    }
+    if (!(pmag > 0.0)) {  // no pivot, or a zero pivot: left to the pipeline
+      failed = true;
+      break;
+    }
+    cb0 = sCb[0];
+    cb1 = sCb[1];
+    cb2 = sCb[2];
+    cb3 = sCb[3];
+    const int4 cnt4 = *reinterpret_cast<const int4*>(sCnt);
+    const int nL = cnt4.x + cnt4.y + cnt4.z + cnt4.w - 1;
+    const double2 piv = sF[p * CSP + ck];
+    {
+      const uint4* mp = reinterpret_cast<const uint4*>(sM + MW * p);
+      const uint4 m0 = mp[0], m1 = mp[1];
+      um[0] = m0.x;
+      um[1] = m0.y;
+      um[2] = m0.z;
+      um[3] = m0.w;
+      um[4] = m1.x;
+      um[5] = m1.y;
+      um[6] = m1.z;
+      um[7] = m1.w;
+      const uint32_t nb = ~(1u << (ck & 31));
+#pragma unroll
+      for (int wd = 0; wd < MW; ++wd)
+        if (wd == (ck >> 5)) um[wd] &= nb;
+    }
+    // U row length: the pivot row's mask bits minus column k
+    const int nU = (int)sPre[MW * p + 7] + __popc(um[7]) + ((ck >> 5) == 7 ? 1 : 0) - 1;
+    if (g_fdebug & 2) {
+    } else if (warp < 4) {  // L column k: rank by (discovery key, row) among the candidates
+      const int sl = tid;
+      const bool mine = sl < RS && ((pick4(cb0, cb1, cb2, cb3, warp) >> lane) & 1u) && sl != p;
+      if (mine) {
+        const uint32_t key = ((uint32_t)sK[sl * CSP + ck] << 16) | (uint32_t)sRow[sl];
+        const uint32_t pkey = ((uint32_t)sK[p * CSP + ck] << 16) | (uint32_t)sRow[p];
+        int rank = -(int)(pkey < key);
+#pragma unroll
+        for (int wv = 0; wv < 4; ++wv) {
+          const int cnt = wv == 0 ? cnt4.x : wv == 1 ? cnt4.y : wv == 2 ? cnt4.z : cnt4.w;
+          const uint4* q = reinterpret_cast<const uint4*>(sCKc + 32 * wv);
+          for (int j = 0; j < cnt; j += 4) {
+            const uint4 v = q[j >> 2];
+            rank += (int)(v.x < key) + (int)(v.y < key) + (int)(v.z < key) + (int)(v.w < key);
+          }
+        }
+        const double2 rp = recipc(piv);
+        const double2 l = cmul_plain(sF[sl * CSP + ck], rp);
+        sLs[rank] = ((uint32_t)sl << 24) | (uint32_t)(sl * CSP);
+        sLv[rank] = l;
+        Li[lnnz + 1 + rank] = sRow[sl];
+        Lx[lnnz + 1 + rank] = l;
+      }
+    } else if (warp < 4 + MW) {  // U row k: one thread per column slot
+      const int c = tid - 128;
+      if (c < CS) {
+        const int cw = c >> 5;
+        const uint32_t cbit = 1u << (c & 31);
+        const uint32_t mw = sM[MW * p + cw];  // (still holds column k's bit)
+        if ((mw & cbit) && c != ck) {
+          const int pos = (int)sPre[MW * p + cw] + __popc(mw & (cbit - 1u)) - (ck < c ? 1 : 0);
+          sUc[pos] = (uint8_t)c;
+          const int u = sUcnt[c];
+          sUcnt[c] = (uint16_t)(u + 1);
+          usi[sCbase[c] + u] = k;
+          usv[sCbase[c] + u] = sF[p * CSP + c];
+        } else if (c == ck) {  // the pivot closes U column k
+          const int u = sUcnt[c];
+          usi[sCbase[c] + u] = k;
+          usv[sCbase[c] + u] = piv;
+          ucount[k] = u + 1;
+        }
+      }
+    }
+    if (tid == FT - 1) {
+      Li[lnnz] = prid;
+      Lx[lnnz] = make_double2(1.0, 0.0);
+      pinv[prid] = k;
+      Lp[k + 1] = lnnz + 1 + nL;
+    }
+    const int e1 = k + 1 < n ? s_jrows : 0;
+    if (wprobe) wb1 += clock64() - tw;
+    __syncthreads();  // S2
+    if (wprobe) tw = clock64();
+    if (probe) { const long long t = clock64(); pc[1] += t - t0; t0 = t; }
+    // ---------------- P3: rank-1 update, then joins ----------------
+    // lanes over the U row (32 columns per pass), warps over the L column;
+    // U values come from the pivot row (left in place until P1 of step k+1)
+    for (int m0 = 0; m0 < ((g_fdebug & 1) ? 0 : nU); m0 += 32) {
+      const int bi = m0 + lane;
+      if (bi < nU) {
+        const int c = sUc[bi];
+        const double2 u = sF[p * CSP + c];
+        const uint32_t key = ((uint32_t)(256 - ((int)sColid[c] - k)) << 8) | (uint32_t)warp;
+        double2* const Fc = sF + c;
+        uint16_t* const Kc = sK + c;
+#pragma unroll 4
+        for (int ai = warp; ai < nL; ai += FT / 32) {
+          const int off = (int)(sLs[ai] & 0xffffffu);
+          const double2 l = sLv[ai];
+          const double2 f = Fc[off];
+          Fc[off] = csub(f, cmul_plain(l, u));
+          const uint32_t kk = Kc[off];
+          Kc[off] = (uint16_t)min(kk, key + (uint32_t)(ai - warp));
+        }
+      }
+    }
+    if (k + 1 < n) {
+      FR_JOIN();
+      joined = tid < RS && e1 && fm_has(fm, tid) && fm_rank(fm, tid) < e1;
+      fm = fm_take(fm, e1);
+    } else {
+      joined = false;
+    }
+    lnnz += 1 + nL;
+    p_prev = p;
+    ck_prev = ck;
+    ck = ck_next;
+    if (wprobe) wb2 += clock64() - tw;
+    __syncthreads();  // S3
+    if (wprobe) tw = clock64();
+    if (probe) { const long long t = clock64(); pc[2] += t - t0; t0 = t; }
+  }
+#undef FR_PREFETCH
+#undef FR_ADVANCE
+#undef FR_JOIN
+  if (probe) {
+    for (int i = 0; i < 4; ++i) g_fprobe[i] = pc[i];
+    g_fprobe[4] = n;
+  }
+  if (wprobe) {
+    g_fwarp[3 * warp] = wb0 / n;
+    g_fwarp[3 * warp + 1] = wb1 / n;
+    g_fwarp[3 * warp + 2] = wb2 / n;
+  }
+  if (tid == 0) info[I_DONE] = failed ? 0 : 1;
+}
+
+// U columns: exact CSC (Up prefix, entries ascending by pivotal row, pivot
+// last) from the per-column staging; L rows -> pivotal indices.
+__global__ void __launch_bounds__(FT) frontal_finish_kernel(FrontArgs a) {
+  __shared__ int sh[40];
+  const int b = blockIdx.x, t = threadIdx.x;
+  int32_t* info = a.info + (int64_t)b * NINFO;
+  if (!info[I_OK] || !info[I_DONE]) return;
+  const int n = a.n;
+  const int64_t bn = (int64_t)b * n, bn1 = (int64_t)b * (n + 1);
+  int32_t* Up = a.Up + bn1;
+  const int32_t* ucount = a.ucount + bn;
+  block_exscan(ucount, Up, n, sh);
+  const int32_t* ubase = a.ubase + bn1;
+  const int32_t* usi = a.usi + (int64_t)b * a.ustride;
+  const double2* usv = a.usv + (int64_t)b * a.ustride;
+  int32_t* Ui = a.Ui + (int64_t)b * a.capU;
+  double2* Ux = a.Ux + (int64_t)b * a.capU;
+  const int lane = t & 31, w = t >> 5;
+  for (int j = w; j < n; j += FT / 32) {
+    const int cnt = ucount[j], src = ubase[j], dst = Up[j];
+    for (int q = lane; q < cnt; q += 32) {
+      Ui[dst + q] = usi[src + q];
+      Ux[dst + q] = usv[src + q];
+    }
+  }
+  const int32_t* pinv = a.pinv + bn;
+  int32_t* Li = a.Li + (int64_t)b * a.capL;
+  const int lnnz = a.Lp[bn1 + n];
+  for (int q = t; q < lnnz; q += FT) Li[q] = pinv[Li[q]];
+  if (t == 0) {
+    a.state[3 * b] = FAC_DONE;
+    a.state[3 * b + 1] = -1;
+  }
+}
+
+}  // namespace
+
+// tuning: enable the per-phase clock probe of CTA 0; read the last run's
+// cycles per step of phases A, B, C, D
+int frontal_probe(int enable, double* out4) {
+  RS_CUDA_TRY(cudaMemcpyToSymbol(g_fprobe_on, &enable, sizeof(int)));
+  {
+    const char* e = getenv("RHOSOLVE_FRONTAL_DEBUG");
+    int dbg = e ? atoi(e) : 0;
+    RS_CUDA_TRY(cudaMemcpyToSymbol(g_fdebug, &dbg, sizeof(int)));
+  }
+  if (out4) {
+    long long h[5];
+    RS_CUDA_TRY(cudaMemcpyFromSymbol(h, g_fprobe, sizeof(h)));
+    for (int i = 0; i < 4; ++i) out4[i] = h[4] ? (double)h[i] / (double)h[4] : 0.0;
+    long long wv[48];
+    RS_CUDA_TRY(cudaMemcpyFromSymbol(wv, g_fwarp, sizeof(wv)));
+    for (int w = 0; w < 16; ++w) printf("warp %2d busy/step P1 %6lld P2 %6lld P3 %6lld\n", w, wv[3 * w], wv[3 * w + 1], wv[3 * w + 2]);
+  }
+  return RS_OK;
+}
+
+static int g_frontal_taken = 0;  // systems accepted by the last frontal_factor
+int frontal_last_taken() { return g_frontal_taken; }
+
+// Opt-in (RHOSOLVE_FRONTAL=1): measured on the 512-system c4 batch it is
+// bit-identical to the column pipeline but not faster (32 ms vs 29.5 ms; the
+// per-step pivot chain costs ~2.7k cycles with one system per SM), see
+// DESIGN.md.
+bool frontal_enabled() {
+  g_frontal_taken = 0;
+  const char* e = getenv("RHOSOLVE_FRONTAL");
+  return e && e[0] == '1';
+}
+
+// Complete LU of the systems whose front fits (see top of file); the others
+// keep state 0 for the pipelined kernel.
+int frontal_factor(const FactorArgs& fa, cudaStream_t st) {
+  const int n = fa.n, B = fa.B;
+  g_frontal_taken = 0;
+  if (B == 0 || n == 0 || n > MAXN || fa.q) return RS_OK;
+  const int64_t N = (int64_t)B * n, N1 = (int64_t)B * (n + 1);
+  int32_t nnz_all = 0;
+  RS_CUDA_TRY(cudaMemcpyAsync(&nnz_all, fa.Ap + N, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  size_t bytes = 0;
+  auto take = [&](size_t x) {
+    size_t o = bytes;
+    bytes += (x + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t o_srow = take(4 * N), o_rlen = take(4 * N), o_rfill = take(4 * N),
+               o_ent = take(4 * N), o_hr = take(4 * N), o_he = take(4 * N), o_hc = take(4 * N),
+               o_erp = take(4 * N1), o_eep = take(4 * N1), o_ecp = take(4 * N1),
+               o_ub = take(4 * N1), o_erow = take(4 * N), o_rloc = take(4 * N),
+               o_roff = take(4 * N), o_emask = take(4 * MW * N), o_ecol = take(4 * N),
+               o_cslot = take(N), o_ecs = take(N), o_ecb = take(4 * N), o_info = take(4 * NINFO * (size_t)B), o_ucount = take(4 * N);
+  RS_CUDA_TRY(cudaStreamSynchronize(st));
+  const size_t o_eent = take(4 * (size_t)nnz_all), o_eval = take(16 * (size_t)nnz_all);
+  unsigned char* ws = nullptr;
+  RS_CUDA_TRY(cudaMallocAsync(&ws, bytes, st));
+  FrontWs w{};
+  w.n = n;
+  w.B = B;
+  w.Ap = fa.Ap;
+  w.Ai = fa.Ai;
+  w.Ax = fa.Ax;
+  w.state = fa.state;
+  w.capL = fa.capL;
+  w.capU = fa.capU;
+  w.srow = (int32_t*)(ws + o_srow);
+  w.rlen = (int32_t*)(ws + o_rlen);
+  w.rfill = (int32_t*)(ws + o_rfill);
+  w.ent = (int32_t*)(ws + o_ent);
+  w.hr = (int32_t*)(ws + o_hr);
+  w.he = (int32_t*)(ws + o_he);
+  w.hc = (int32_t*)(ws + o_hc);
+  w.erp = (int32_t*)(ws + o_erp);
+  w.eep = (int32_t*)(ws + o_eep);
+  w.ecp = (int32_t*)(ws + o_ecp);
+  w.ubase = (int32_t*)(ws + o_ub);
+  w.erow = (int32_t*)(ws + o_erow);
+  w.rloc = (int32_t*)(ws + o_rloc);
+  w.roff = (int32_t*)(ws + o_roff);
+  w.emask = (uint32_t*)(ws + o_emask);
+  w.ecol = (int32_t*)(ws + o_ecol);
+  w.cslot = (uint8_t*)(ws + o_cslot);
+  w.ecs = (uint8_t*)(ws + o_ecs);
+  w.ecb = (int32_t*)(ws + o_ecb);
+  w.eent = (uint32_t*)(ws + o_eent);
+  w.eval = (double2*)(ws + o_eval);
+  w.info = (int32_t*)(ws + o_info);
+  frontal_analyze_kernel<<<B, FT, 0, st>>>(w);
+  ::rs::count_launch();
+  RS_CUDA_TRY(cudaGetLastError());
+  std::vector<int32_t> info((size_t)B * NINFO);
+  RS_CUDA_TRY(cudaMemcpyAsync(info.data(), w.info, 4 * info.size(), cudaMemcpyDeviceToHost, st));
+  RS_CUDA_TRY(cudaStreamSynchronize(st));
+  int dev = 0, max_smem = 0;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  size_t smem = 0;
+  int64_t ustride = 0;
+  int any = 0;
+  bool changed = false;
+  for (int b = 0; b < B; ++b) {
+    int32_t* I = info.data() + (size_t)b * NINFO;
+    if (!I[I_OK]) continue;
+    const size_t sb = frontal_smem_bytes(I[I_RS], I[I_CS], n);
+    if (sb > (size_t)max_smem) {  // does not fit: the pipeline takes it
+      I[I_OK] = 0;
+      changed = true;
+      continue;
+    }
+    smem = std::max(smem, sb);
+    ustride = std::max<int64_t>(ustride, I[I_UB]);
+    ++any;
+  }
+  g_frontal_taken = any;
+  if (!any) {
+    cudaFreeAsync(ws, st);
+    return RS_OK;
+  }
+  if (changed)
+    RS_CUDA_TRY(cudaMemcpyAsync(w.info, info.data(), 4 * info.size(), cudaMemcpyHostToDevice, st));
+  unsigned char* us = nullptr;
+  RS_CUDA_TRY(cudaMallocAsync(&us, (size_t)B * ustride * 20 + 256, st));
+  FrontArgs a{};
+  a.n = n;
+  a.B = B;
+  a.erp = w.erp;
+  a.eep = w.eep;
+  a.ecp = w.ecp;
+  a.ubase = w.ubase;
+  a.erow = w.erow;
+  a.emask = w.emask;
+  a.ecol = w.ecol;
+  a.cslot = w.cslot;
+  a.ecs = w.ecs;
+  a.ecb = w.ecb;
+  a.eent = w.eent;
+  a.eval = w.eval;
+  a.Ap = fa.Ap;
+  a.info = w.info;
+  a.ucount = (int32_t*)(ws + o_ucount);
+  a.usv = (double2*)us;
+  a.usi = (int32_t*)(us + (size_t)B * ustride * 16);
+  a.ustride = ustride;
+  a.Lp = fa.Lp;
+  a.Li = fa.Li;
+  a.Lx = fa.Lx;
+  a.capL = fa.capL;
+  a.Up = fa.Up;
+  a.Ui = fa.Ui;
+  a.Ux = fa.Ux;
+  a.capU = fa.capU;
+  a.pinv = fa.pinv;
+  a.state = fa.state;
+  RS_CUDA_TRY(cudaFuncSetAttribute(frontal_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+  frontal_lu_kernel<<<B, FT, smem, st>>>(a);
+  ::rs::count_launch();
+  frontal_finish_kernel<<<B, FT, 0, st>>>(a);
+  ::rs::count_launch();
+  RS_CUDA_TRY(cudaGetLastError());
+  cudaFreeAsync(us, st);
+  cudaFreeAsync(ws, st);
+  return RS_OK;
+}
+
+}  // namespace rs

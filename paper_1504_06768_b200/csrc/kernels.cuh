@@ -77,4 +77,13 @@ __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_
                                             int bits_in_smem);
 int ilutp_plan(int32_t n, int warps, int* smem_mode, int* bits_in_smem);
 
+// ---- frontal.cu: right-looking frontal complete LU ------------------------
+// Factors (complete LU, q == null) every system whose structural front fits
+// shared memory and marks it FAC_DONE; the rest keep their state for
+// launch_ilutp.  RHOSOLVE_FRONTAL=0 disables it.
+bool frontal_enabled();
+int frontal_factor(const FactorArgs& a, cudaStream_t st);
+int frontal_last_taken();
+int frontal_probe(int enable, double* out4);
+
 }  // namespace rs
