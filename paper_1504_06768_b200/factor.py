@@ -19,10 +19,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from .sparse import DeviceCSR
+from .sparse import CSRMatrix, DeviceCSR, Permutation, write_matrix_market
 
 __all__ = ["LUFactors", "lu", "ilutp", "solve_lu", "condest", "SingularMatrixError",
-           "PreconditionerBreakdownError", "factor_batch"]
+           "PreconditionerBreakdownError", "factor_batch", "export_factors"]
 
 
 class SingularMatrixError(ValueError):
@@ -56,6 +56,40 @@ class LUFactors:
     @property
     def fill_factor(self):
         return float(self.fill_factors[0])
+
+    def _host_csr(self, b, upper):
+        """factor._csc_to_csr_matrix (factor.py:59-67): system b's L (unit
+        diagonal) or U (with pivots) as a host CSR, rows in ascending column
+        order (stable by the column scan)."""
+        lp, li, lx, up, ui, ux, _ = self.system_raw(b)
+        cp, ci, cx = (up, ui, ux) if upper else (lp, li, lx)
+        n = self.n
+        order = np.argsort(ci, kind="stable")
+        cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(cp))[order]
+        rp = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(np.bincount(ci[order], minlength=n), out=rp[1:])
+        return CSRMatrix(n, n, rp, cols, cx[order])
+
+    @property
+    def L(self):
+        """Host CSR L of system 0 (LUFactors.L, factor.py:27-56)."""
+        return self._host_csr(0, False)
+
+    @property
+    def U(self):
+        """Host CSR U of system 0 (LUFactors.U)."""
+        return self._host_csr(0, True)
+
+    @property
+    def row_perm(self):
+        """Permutation(pinv) of system 0 (LUFactors.row_perm)."""
+        return Permutation(self.pinv[: self.n].cpu().numpy().astype(np.int64))
+
+    @property
+    def col_perm(self):
+        """Column pre-ordering (identity: "cmd" column orderings are not on the
+        GPU path)."""
+        return Permutation.identity(self.n)
 
     def system_raw(self, b):
         """Host copy of system b's raw CSC factors (reference layout, int64)."""
@@ -284,3 +318,13 @@ def condest(f):
     e = torch.ones(f.nsys * f.n, dtype=torch.complex128, device=f.pinv.device)
     x = solve_lu_device(f, e).reshape(f.nsys, f.n).abs().amax(1).cpu().numpy()
     return float(x[0]) if f.nsys == 1 else x
+
+
+def export_factors(f, prefix):
+    """Write L/U as Matrix Market files and the permutations as
+    newline-delimited integer lists: <prefix>_L.mtx, _U.mtx, _rowperm.txt,
+    _colperm.txt (factor.py:160-167); system 0 of a batch."""
+    write_matrix_market(f.L, f"{prefix}_L.mtx")
+    write_matrix_market(f.U, f"{prefix}_U.mtx")
+    f.row_perm.save(f"{prefix}_rowperm.txt")
+    f.col_perm.save(f"{prefix}_colperm.txt")

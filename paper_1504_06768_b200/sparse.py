@@ -24,7 +24,9 @@ import torch
 
 __all__ = ["CSRMatrix", "Permutation", "DeviceCSR", "PinnedBatchCSR", "identity", "kron",
            "transpose", "conjugate", "adjoint", "add", "matmul", "from_host", "pin_batch",
-           "as_host_csr"]
+           "as_host_csr", "write_matrix_market", "read_matrix_market"]
+
+_MM_HEADER = "%%MatrixMarket matrix coordinate complex general"
 
 
 class CSRMatrix:
@@ -82,6 +84,10 @@ class CSRMatrix:
     def to_coo(self):
         return self.row_ids(), self.col_idx.copy(), self.values.copy()
 
+    def diagonal_stored_count(self):
+        """How many diagonal positions are explicitly stored (sparse.py:127-131)."""
+        return int(np.count_nonzero(self.row_ids() == self.col_idx))
+
     def __repr__(self):
         return f"CSRMatrix({self.nrows}x{self.ncols}, nnz={self.nnz})"
 
@@ -98,6 +104,11 @@ class Permutation:
             inverse = np.empty_like(self.forward)
             inverse[self.forward] = np.arange(len(self.forward))
         self.inverse = np.ascontiguousarray(inverse, dtype=np.int64)
+        n = len(self.forward)
+        if (len(self.inverse) != n
+                or not np.array_equal(np.sort(self.forward), np.arange(n))
+                or not np.array_equal(self.inverse[self.forward], np.arange(n))):
+            raise ValueError("not a bijection with matching inverse")
 
     @classmethod
     def identity(cls, n):
@@ -116,6 +127,22 @@ class Permutation:
 
     def is_identity(self):
         return bool(np.array_equal(self.forward, np.arange(len(self.forward))))
+
+    def save(self, path):
+        """Newline-delimited forward map (sparse.py:179-183)."""
+        with open(path, "w", encoding="ascii") as fh:
+            fh.write("\n".join(str(int(i)) for i in self.forward))
+            fh.write("\n")
+
+    @classmethod
+    def load(cls, path):
+        """Inverse of save (sparse.py:185-189)."""
+        with open(path, encoding="ascii") as fh:
+            vals = [int(line) for line in fh if line.strip()]
+        return cls(np.array(vals, dtype=np.int64))
+
+    def __repr__(self):
+        return f"Permutation(n={len(self.forward)})"
 
 
 def identity(n):
@@ -179,9 +206,14 @@ def matmul(a, b):
 
 
 def as_host_csr(m):
-    """Accept our CSRMatrix or the reference SparseComplexMatrix (duck-typed)."""
+    """Accept our CSRMatrix, a single-system DeviceCSR, a system object with
+    .matrix, or the reference SparseComplexMatrix (duck-typed)."""
     if isinstance(m, CSRMatrix):
         return m
+    if not hasattr(m, "row_ptr") and hasattr(m, "matrix"):
+        m = m.matrix
+    if isinstance(m, DeviceCSR):
+        return m.to_host()
     return CSRMatrix(m.nrows, m.ncols, m.row_ptr, m.col_idx, m.values)
 
 
@@ -298,3 +330,61 @@ def from_host(mats, device=None):
         torch.from_numpy(rp.astype(np.int32)).to(dev),
         torch.from_numpy(np.concatenate([m.col_idx for m in mats]).astype(np.int32)).to(dev),
         torch.from_numpy(np.concatenate([m.values for m in mats])).to(dev))
+
+
+def write_matrix_market(a, path, comment=None):
+    """Matrix Market coordinate complex general, 1-based indices, values with
+    17 significant digits -- the reference writer's bytes (sparse.py:302-312).
+    Accepts a host CSRMatrix, a single-system DeviceCSR or any object with
+    nrows/ncols/row_ptr/col_idx/values."""
+    a = as_host_csr(a)
+    rows, cols, vals = a.to_coo()
+    lines = [_MM_HEADER]
+    if comment:
+        lines += [f"% {line}" for line in comment.splitlines()]
+    lines.append(f"{a.nrows} {a.ncols} {a.nnz}")
+    re, im = vals.real.tolist(), vals.imag.tolist()
+    lines += [f"{r + 1} {c + 1} {x:.17g} {y:.17g}"
+              for r, c, x, y in zip(rows.tolist(), cols.tolist(), re, im)]
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+
+def read_matrix_market(path):
+    """Reader for coordinate general complex / real / integer Matrix Market
+    files (sparse.py:315-351): duplicates summed, nothing pruned."""
+    with open(path, encoding="ascii") as fh:
+        header = fh.readline().strip()
+        fields = header.lower().split()
+        if (len(fields) < 5 or fields[0] != "%%matrixmarket"
+                or fields[1] != "matrix" or fields[2] != "coordinate"):
+            raise ValueError(f"unsupported Matrix Market header: {header}")
+        kind, symmetry = fields[3], fields[4]
+        if symmetry != "general":
+            raise ValueError(f"unsupported symmetry: {symmetry}")
+        if kind not in ("complex", "real", "integer"):
+            raise ValueError(f"unsupported field type: {kind}")
+        line = fh.readline()
+        while line.startswith("%") or not line.strip():
+            line = fh.readline()
+        nrows, ncols, nnz = (int(t) for t in line.split())
+        rows = np.empty(nnz, dtype=np.int64)
+        cols = np.empty(nnz, dtype=np.int64)
+        vals = np.empty(nnz, dtype=np.complex128)
+        got = 0
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("%"):
+                continue
+            parts = line.split()
+            if got >= nnz:
+                got += 1
+                break
+            rows[got] = int(parts[0]) - 1
+            cols[got] = int(parts[1]) - 1
+            vals[got] = (complex(float(parts[2]), float(parts[3])) if kind == "complex"
+                         else float(parts[2]))
+            got += 1
+        if got != nnz:
+            raise ValueError(f"expected {nnz} entries, found {got}")
+    return CSRMatrix.from_coo(nrows, ncols, rows, cols, vals, prune=False)
