@@ -46,6 +46,7 @@ extern "C" {
 #define RS_ERR_NONFINITE -5
 #define RS_ERR_OVERFLOW -6
 #define RS_ERR_UNSUPPORTED -7
+#define RS_ERR_STRUCT_SINGULAR -8
 
 typedef struct rs_complex {
   double re;
@@ -57,6 +58,28 @@ const char* rs_last_error(void);
 /* Number of kernels this library has launched in the process (bench
  * bookkeeping: gpu_launches). */
 long long rs_launch_count(void);
+/* ---- 'cmd' ordering (host-native; steady._prepare, steady.py:95-107) -----
+ * Both take HOST arrays: the CSR of a square matrix (int64 row_ptr[n+1] /
+ * col_idx, complex128 values), as the reference's SparseComplexMatrix holds
+ * it.  The algorithms are greedy and sequential, so they run on the host
+ * once per structure; the elimination they order runs on the GPU. */
+
+/* Replaces ordering.weighted_mbm (ordering.py:121-218): forward[r] = the
+ * position row r moves to (a zero-free structural diagonal); weight-guided
+ * column BFS from the largest |a_ij| (numpy complex abs = hypot), greedy
+ * largest-|value| matching, completed by BFS augmenting paths.  Returns
+ * RS_ERR_STRUCT_SINGULAR (StructurallySingularError) when no perfect
+ * matching exists. */
+int rs_weighted_mbm_host(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                         const rs_complex* values, int64_t* forward);
+
+/* Replaces ordering.col_min_degree (ordering.py:221-282): exact greedy
+ * minimum degree on the column-intersection graph (quotient form), ties to
+ * the lowest column; order[k] = the k-th eliminated column
+ * (Permutation.from_order(order)). */
+int rs_col_min_degree_host(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                           int64_t* order);
+
 /* Number of systems the last rs_factorize call factored with the
  * right-looking frontal kernel (complete LU whose front fits shared memory;
  * opt-in with RHOSOLVE_FRONTAL=1; diagnostics and tests). */
@@ -198,6 +221,15 @@ int rs_rcm(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
 int rs_permute(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
                const rs_complex* v, const int32_t* forward, const int32_t* inverse,
                int32_t* out_rp, int32_t* out_ci, rs_complex* out_v, void* stream);
+
+/* sparse.permute(a, row_perm, col_perm) with distinct permutations
+ * (sparse.py:276-282): B[rf[i], cf[j]] = A[i, j], given rf^-1 (row_inverse)
+ * and cf (col_forward), per system.  The 'cmd' path uses it for the MBM row
+ * permutation and the minimum-degree column order. */
+int rs_permute_rows_cols(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+                         const rs_complex* v, const int32_t* row_inverse,
+                         const int32_t* col_forward, int32_t* out_rp, int32_t* out_ci,
+                         rs_complex* out_v, void* stream);
 
 /* gather != 0: out[i] = x[forward[i]] (solution unpermute, steady.py:249-250);
  * gather == 0: out[forward[i]] = x[i] (rhs permute, steady.py:89-94). */

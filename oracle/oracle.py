@@ -250,8 +250,9 @@ class Factors:
         return y
 
 
-def factorize_raw(A, drop_tol, fill_limit):
-    """factor._factor (factor.py:70-112) -> Factors, or raises Breakdown."""
+def factorize_raw(A, drop_tol, fill_limit, q=None):
+    """factor._factor (factor.py:70-112) -> Factors, or raises Breakdown.
+    q: elimination column order (col_perm.inverse, factor.py:78)."""
     n = A.n
     at = transpose(A)
     incomplete = drop_tol > 0.0 or not math.isinf(fill_limit)
@@ -261,7 +262,8 @@ def factorize_raw(A, drop_tol, fill_limit):
         np.maximum.at(rn, A.rows(), np.abs(A.v.real) + np.abs(A.v.imag))
     cap = -1 if math.isinf(fill_limit) else int(math.ceil(fill_limit * A.nnz / n))
     out = _Factors()
-    if _lib().orc_factorize(n, _p(at.rp), _p(at.ci), _p(at.v), None, float(drop_tol), cap,
+    qa = None if q is None else _i64(q)
+    if _lib().orc_factorize(n, _p(at.rp), _p(at.ci), _p(at.v), _p(qa), float(drop_tol), cap,
                             _p(rn), ctypes.byref(out)) != 0:
         raise MemoryError
     try:

@@ -26,7 +26,9 @@ ERRORS = {
     -5: "non-finite values",
     -6: "capacity overflow",
     -7: "unsupported",
+    -8: "structurally singular",
 }
+RS_ERR_STRUCT_SINGULAR = -8
 
 # rs_solve_mode
 INV_DIRECT, INV_BICGSTAB, INV_GMRES, LIN_DIRECT, LIN_BICGSTAB, LIN_GMRES = range(6)
@@ -89,7 +91,10 @@ _SIGS = {
     "rs_trace_modify": [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                         ctypes.POINTER(_i64), _vp],
     "rs_rcm": [_i32, _i32, _vp, _vp, _vp, _vp, _vp],
+    "rs_weighted_mbm_host": [_i64, _vp, _vp, _vp, _vp],
+    "rs_col_min_degree_host": [_i64, _vp, _vp, _vp],
     "rs_permute": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "rs_permute_rows_cols": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "rs_permute_vector": [_i32, _i32, _vp, _vp, _vp, _i32, _vp],
     "rs_transpose": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "rs_row_norms": [_i32, _i32, _vp, _vp, _vp, _vp],
@@ -102,7 +107,7 @@ _SIGS = {
                          _vp],
 }
 
-EXPORTED = tuple(_SIGS) + ("rs_last_error", "rs_launch_count")
+EXPORTED = tuple(_SIGS) + ("rs_last_error", "rs_launch_count", "rs_debug_frontal_taken")
 
 _lib = None
 
@@ -125,6 +130,8 @@ def load():
     lib.rs_last_error.restype = ctypes.c_char_p
     lib.rs_launch_count.argtypes = []
     lib.rs_launch_count.restype = ctypes.c_longlong
+    lib.rs_debug_frontal_taken.argtypes = []
+    lib.rs_debug_frontal_taken.restype = _i32
     _lib = lib
     return lib
 

@@ -98,6 +98,26 @@ long long rs_launch_count(void) { return g_launches.load(); }
 // Tuning hook (not part of the documented ABI): when set, the next
 // factorizations record per-column phase clocks of system 0 into buf[n*6].
 int rs_debug_frontal_taken(void) { return rs::frontal_last_taken(); }
+
+int rs_weighted_mbm_host(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                         const rs_complex* values, int64_t* forward) {
+  RS_CHECK_ARG(n >= 0, "negative size");
+  RS_CHECK_ARG(!n || (row_ptr && col_idx && values && forward), "null array");
+  if (rs::weighted_mbm_host(n, row_ptr, col_idx, reinterpret_cast<const double2*>(values),
+                            forward)) {
+    rs::set_error("matrix is structurally singular: no zero-free diagonal");
+    return RS_ERR_STRUCT_SINGULAR;
+  }
+  return RS_OK;
+}
+
+int rs_col_min_degree_host(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                           int64_t* order) {
+  RS_CHECK_ARG(n >= 0, "negative size");
+  RS_CHECK_ARG(!n || (row_ptr && col_idx && order), "null array");
+  rs::col_min_degree_host(n, row_ptr, col_idx, order);
+  return RS_OK;
+}
 int rs_debug_frontal_probe(int enable, double* out4) { return rs::frontal_probe(enable, out4); }
 
 int rs_debug_factor_probe(void* buf) {
@@ -380,6 +400,15 @@ int rs_permute(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, co
   if (!nsys || !n) return RS_OK;
   return csr_permute(nsys, n, rp, ci, C2(v), forward, inverse, out_rp, out_ci, M2(out_v),
                      S(stream));
+}
+
+int rs_permute_rows_cols(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
+                         const rs_complex* v, const int32_t* row_inverse,
+                         const int32_t* col_forward, int32_t* out_rp, int32_t* out_ci,
+                         rs_complex* out_v, void* stream) {
+  if (!nsys || !n) return RS_OK;
+  return csr_permute(nsys, n, rp, ci, C2(v), col_forward, row_inverse, out_rp, out_ci,
+                     M2(out_v), S(stream));
 }
 
 int rs_permute_vector(int32_t nsys, int32_t n, const rs_complex* x, const int32_t* forward,

@@ -75,6 +75,7 @@ __device__ __forceinline__ int warp_lane() { return threadIdx.x & 31; }
 #define RS_ERR_NONFINITE -5
 #define RS_ERR_OVERFLOW -6
 #define RS_ERR_UNSUPPORTED -7
+#define RS_ERR_STRUCT_SINGULAR -8
 
 namespace rs {
 void set_error(const char* fmt, ...);

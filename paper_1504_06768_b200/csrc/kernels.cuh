@@ -77,6 +77,11 @@ __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_
                                             int bits_in_smem);
 int ilutp_plan(int32_t n, int warps, int* smem_mode, int* bits_in_smem);
 
+// ---- cmd_order.cu: host-native 'cmd' ordering ---------------------------
+int weighted_mbm_host(int64_t n, const int64_t* rp, const int64_t* ci, const double2* v,
+                      int64_t* forward);
+void col_min_degree_host(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* order);
+
 // ---- frontal.cu: right-looking frontal complete LU ------------------------
 // Factors (complete LU, q == null) every system whose structural front fits
 // shared memory and marks it FAC_DONE; the rest keep their state for

@@ -45,7 +45,8 @@ class LUFactors:
 
     __slots__ = ("n", "nsys", "raw", "capL", "capU", "pinv", "L_rp", "L_ci", "L_v", "U_rp",
                  "U_ci", "U_v", "rdiag", "fill_factors", "complete", "drop_tol",
-                 "fill_limit", "fail", "lnnz", "unnz", "ok", "csc", "Ls", "Us")
+                 "fill_limit", "fail", "lnnz", "unnz", "ok", "csc", "Ls", "Us", "colp",
+                 "colp_dev")
 
     def ensure_rows(self):
         """Build the row-oriented factor copy (row sweeps, exports) once."""
@@ -87,9 +88,9 @@ class LUFactors:
 
     @property
     def col_perm(self):
-        """Column pre-ordering (identity: "cmd" column orderings are not on the
-        GPU path)."""
-        return Permutation.identity(self.n)
+        """Column pre-ordering (LUFactors.col_perm): the 'cmd' minimum-degree
+        order when one was given, else the identity."""
+        return self.colp if self.colp is not None else Permutation.identity(self.n)
 
     def system_raw(self, b):
         """Host copy of system b's raw CSC factors (reference layout, int64)."""
@@ -196,6 +197,7 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
     # larger systems use the row-oriented copy
     f.csc = bool(_lib.load().rs_col_sweep_supported(n))
     f.Ls = f.Us = None
+    f.colp = f.colp_dev = None
     if f.ok:
         f.rdiag = torch.empty(B * n, dtype=torch.complex128, device=dev)
         _lib.call("rs_pivot_recip", B, n, _lib.ptr(Up), _lib.ptr(Ux), capU,
@@ -262,16 +264,26 @@ def _mat(a):
     return a.matrix if hasattr(a, "matrix") else a
 
 
-def _check_colperm(col_perm, n):
-    if col_perm is not None and not col_perm.is_identity():
-        raise NotImplementedError("column pre-orderings ('cmd') are outside the GPU path")
+def _with_colperm(M, col_perm, drop_tol, fill_limit):
+    """factor._factor's column pre-ordering (factor.py:76-78): the reference
+    eliminates column q[k] at step k (q = col_perm.inverse); factoring the
+    column-permuted matrix A[:, q] in natural order gives the same factors
+    bit for bit, and solve_lu scatters x[q] = y back."""
+    if col_perm is None or col_perm.is_identity():
+        return factor_batch(M, drop_tol, fill_limit)
+    if len(col_perm) != M.n:
+        raise ValueError("column permutation length does not match matrix")
+    from . import ordering
+    cf = torch.from_numpy(np.tile(col_perm.forward, M.nsys).astype(np.int32)).to(
+        M.values.device)
+    f = factor_batch(ordering.permute_rows_cols(M, None, cf), drop_tol, fill_limit)
+    f.colp, f.colp_dev = col_perm, cf
+    return f
 
 
 def lu(a, col_perm=None):
     """Complete sparse LU with partial pivoting (factor.py:115-118)."""
-    M = _mat(a)
-    _check_colperm(col_perm, M.n)
-    return factor_batch(M, 0.0, math.inf)
+    return _with_colperm(_mat(a), col_perm, 0.0, math.inf)
 
 
 def ilutp(a, d=1e-4, p=300.0, col_perm=None):
@@ -280,13 +292,21 @@ def ilutp(a, d=1e-4, p=300.0, col_perm=None):
         raise ValueError("drop tolerance d must be >= 0")
     if not p >= 1:
         raise ValueError("fill limit p must be >= 1")
-    M = _mat(a)
-    _check_colperm(col_perm, M.n)
-    return factor_batch(M, float(d), float(p))
+    return _with_colperm(_mat(a), col_perm, float(d), float(p))
 
 
 def solve_lu_device(f, b):
     """x = M^{-1} b on the device for every system (b: nsys*n complex128)."""
+    x = _solve_lu_rows(f, b)
+    if f.colp_dev is not None:  # x[q] = y (factor.py:147-148)
+        y = torch.empty_like(x)
+        _lib.call("rs_permute_vector", f.nsys, f.n, _lib.ptr(x), _lib.ptr(f.colp_dev),
+                  _lib.ptr(y), 1, _lib.stream_ptr())
+        return y
+    return x
+
+
+def _solve_lu_rows(f, b):
     x = torch.empty_like(b)
     if f.csc:
         (lo, li, lv, lm, _), (uo, ui, uv, um, ur) = f.Ls, f.Us

@@ -105,11 +105,13 @@ def _require_plain(L):
 
 
 def _prepare(system, ordering_name, plain=None):
-    """steady._prepare for "natural" / "rcm" (steady.py:74-94) on the device.
-    Returns (matrix, rhs, plain_ordered, forward, label)."""
+    """steady._prepare (steady.py:74-108) on the device.  Returns (matrix,
+    rhs, plain_ordered, forward, label, x0_gather): the solution is x[forward]
+    (None: unchanged); x0_gather maps a start vector drawn in the reference's
+    coordinates into the working ones (None: the same)."""
     m = system.matrix
     if ordering_name == "natural":
-        return m, system.rhs, plain, None, "natural"
+        return m, system.rhs, plain, None, "natural", None
     if ordering_name == "rcm":
         fwd, inv = ordering.rcm_device(m)
         pm = ordering.permute(m, fwd, inv)
@@ -117,10 +119,23 @@ def _prepare(system, ordering_name, plain=None):
         if system.rhs is not None:
             prhs = ordering.permute_vector(system.rhs, fwd, m.nsys, m.n, gather=False)
         pp = ordering.permute(plain, fwd, inv) if plain is not None else None
-        return pm, prhs, pp, fwd, "rcm"
+        return pm, prhs, pp, fwd, "rcm", None
     if ordering_name == "cmd":
-        raise NotImplementedError("the 'cmd' ordering (MBM + column minimum degree) is "
-                                  "outside the GPU hot path")
+        # MBM rows (when the diagonal is not fully stored) and the minimum-
+        # degree column order, both host-native (csrc/cmd_order.cu).  The
+        # reference keeps x in original coordinates and applies the column
+        # order inside factor/solve_lu; here the columns of the working matrix
+        # are permuted instead (identical factors), so the iterate lives in
+        # elimination order: x0 is gathered into it and the solution gathered
+        # back (x[j] = y[colp.forward[j]]).
+        (rf, ri, cf, ci), label = ordering.cmd_plan(m)
+        pm = ordering.permute_rows_cols(m, ri, cf)
+        prhs = None
+        if system.rhs is not None:
+            prhs = (ordering.permute_vector(system.rhs, rf, m.nsys, m.n, gather=False)
+                    if rf is not None else system.rhs)
+        pp = ordering.permute_rows_cols(plain, None, cf) if plain is not None else None
+        return pm, prhs, pp, cf, label, ci
     raise ValueError(f"unknown ordering {ordering_name!r}")
 
 
@@ -196,7 +211,7 @@ def solve_direct(L, ordering_name="natural", w=None):
     L = _require_plain(L)
     t0 = _sync()
     modified = liouville.build_modified(L, w)
-    mat, rhs, _, fwd, label = _prepare(modified, ordering_name)
+    mat, rhs, _, fwd, label, _ = _prepare(modified, ordering_name)
     t1 = _sync()
     f = factor.lu(mat)
     t2 = _sync()
@@ -218,7 +233,7 @@ def solve_iterative(L, ordering_name="natural", solver="gmres", d=1e-4, p=300.0,
     _check_ops(tol, max_iter, restart_m)
     t0 = _sync()
     modified = liouville.build_modified(L, w)
-    mat, rhs, _, fwd, label = _prepare(modified, ordering_name)
+    mat, rhs, _, fwd, label, _ = _prepare(modified, ordering_name)
     t1 = _sync()
     f = factor.ilutp(mat, d=d, p=p)
     t2 = _sync()
@@ -262,7 +277,7 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
     # are generated on a host thread while the GPU orders and factors
     x0_future = _POOL.submit(_start_vectors, L.n, list(seeds))
     shifted = liouville.shift(L, sigma)
-    mat, _, plain, fwd, label = _prepare(shifted, ordering_name, plain=L.matrix)
+    mat, _, plain, fwd, label, x0_map = _prepare(shifted, ordering_name, plain=L.matrix)
     if plain is None:
         plain = L.matrix
     t1 = _sync()
@@ -278,6 +293,8 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
         mode = _lib.INV_GMRES if solver == "gmres" else _lib.INV_BICGSTAB
     t2 = _sync()
     x0 = x0_future.result().to(mat.values.device, non_blocking=True)
+    if x0_map is not None:
+        x0 = ordering.permute_vector(x0, x0_map, mat.nsys, mat.n, gather=True)
     if not f.ok:  # some system of the batch failed to factor
         return None, f, None, None, label, (t0, t1, t2, _sync())
     x, st = _solve(mode, mat, plain, f, x0, tol, max_iter, restart_m, inner == "iterative",
@@ -351,7 +368,7 @@ def solve_batch(L, method="bicgstab", ordering_name="natural", d=1e-4, p=300.0, 
     L = _require_plain(L)
     t0 = _sync()
     modified = liouville.build_modified(L, w)
-    mat, rhs, _, fwd, label = _prepare(modified, ordering_name)
+    mat, rhs, _, fwd, label, _ = _prepare(modified, ordering_name)
     t1 = _sync()
     if method == "direct":
         f = factor.factor_batch(mat, 0.0, float("inf"))
