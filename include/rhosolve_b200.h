@@ -82,7 +82,8 @@ int rs_col_min_degree_host(int64_t n, const int64_t* row_ptr, const int64_t* col
 
 /* Number of systems the last rs_factorize call factored with the
  * right-looking frontal kernel (complete LU whose front fits shared memory;
- * opt-in with RHOSOLVE_FRONTAL=1; diagnostics and tests). */
+ * batches of <= 2 waves by default, RHOSOLVE_FRONTAL=1/0 forces it on/off;
+ * diagnostics and tests). */
 int rs_debug_frontal_taken(void);
 
 /* ---- kernel seam (kernels/__init__.py:19-36) ---------------------------- */

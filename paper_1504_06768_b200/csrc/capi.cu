@@ -224,7 +224,7 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   // complete LU of small systems (the c4 sweep): right-looking frontal
   // elimination in shared memory; whatever it does not take (front too large,
   // zero pivot) runs through the column pipeline below
-  if (frontal_enabled() && !(drop_tol > 0.0) && fill_cap < 0 && !fill_caps && !q &&
+  if (frontal_enabled(nsys) && !(drop_tol > 0.0) && fill_cap < 0 && !fill_caps && !q &&
       !g_factor_probe) {
     const int frc = frontal_factor(a, st);
     if (frc) {

@@ -416,16 +416,30 @@ __device__ __forceinline__ uint32_t pick4(uint32_t a0, uint32_t a1, uint32_t a2,
   return w == 0 ? a0 : w == 1 ? a1 : w == 2 ? a2 : a3;
 }
 
-// slot of the r-th (0-based) free slot
-__device__ __forceinline__ int fm_nth(FreeMask f, int r) {
-  const int c0 = __popc(f.w0), c1 = __popc(f.w1), c2 = __popc(f.w2);
-  if (r < c0) return (int)__fns(f.w0, 0, r + 1);
-  r -= c0;
-  if (r < c1) return 32 + (int)__fns(f.w1, 0, r + 1);
-  r -= c1;
-  if (r < c2) return 64 + (int)__fns(f.w2, 0, r + 1);
-  r -= c2;
-  return 96 + (int)__fns(f.w3, 0, r + 1);
+// slot of the r-th (0-based) free slot (compact code: joins are rare)
+__device__ __noinline__ int fm_nth(FreeMask f, int r) {
+  uint32_t w = f.w0;
+  int base = 0;
+  int c = __popc(w);
+  if (r >= c) {
+    r -= c;
+    w = f.w1;
+    base = 32;
+    c = __popc(w);
+    if (r >= c) {
+      r -= c;
+      w = f.w2;
+      base = 64;
+      c = __popc(w);
+      if (r >= c) {
+        r -= c;
+        w = f.w3;
+        base = 96;
+      }
+    }
+  }
+  for (; r > 0; --r) w &= w - 1;
+  return base + __ffs(w) - 1;
 }
 
 // rank of slot s among the free slots (valid when s is free)
@@ -484,6 +498,7 @@ __device__ int g_fdebug;  // tuning: 1 skip the update, 2 skip L/U emission
 //       so a fill starts from 0 - l u as in the reference; loaders then write
 //       the rows joining at step k+1 into free slots (never the pivot row,
 //       which the update still reads)
+template <bool PROBE>
 __global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int s_jrows;  // rows joining at step k+1 (published in P1)
@@ -657,10 +672,12 @@ __global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
   uint32_t cb0 = 0, cb1 = 0, cb2 = 0, cb3 = 0;
   int lnnz = 0;
   bool failed = false;
-  const bool probe = g_fprobe_on && b == 0 && tid == 0;
-  const bool wprobe = g_fprobe_on && b == 0 && lane == 0;
+  const bool probe = PROBE && g_fprobe_on && b == 0 && tid == 0;
+  const bool wprobe = PROBE && g_fprobe_on && b == 0 && lane == 0;
+  const int dbg = PROBE ? g_fdebug : 0;
   long long pc[4] = {0, 0, 0, 0}, t0 = clock64();
   long long wb0 = 0, wb1 = 0, wb2 = 0, tw = clock64();
+#pragma unroll 1
   for (int k = 0; k < n; ++k) {
     const int ck_next = k + 1 < n ? cslot[k + 1] : 0;  // used next step
     // ---------------- P1 ----------------
@@ -815,7 +832,7 @@ __global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
     }
     // U row length: the pivot row's mask bits minus column k
     const int nU = (int)sPre[MW * p + 7] + __popc(um[7]) + ((ck >> 5) == 7 ? 1 : 0) - 1;
-    if (g_fdebug & 2) {
+    if (dbg & 2) {
     } else if (warp < 4) {  // L column k: rank by (discovery key, row) among the candidates
       const int sl = tid;
       const bool mine = sl < RS && ((pick4(cb0, cb1, cb2, cb3, warp) >> lane) & 1u) && sl != p;
@@ -823,7 +840,7 @@ __global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
         const uint32_t key = ((uint32_t)sK[sl * CSP + ck] << 16) | (uint32_t)sRow[sl];
         const uint32_t pkey = ((uint32_t)sK[p * CSP + ck] << 16) | (uint32_t)sRow[p];
         int rank = -(int)(pkey < key);
-#pragma unroll
+#pragma unroll 1
         for (int wv = 0; wv < 4; ++wv) {
           const int cnt = wv == 0 ? cnt4.x : wv == 1 ? cnt4.y : wv == 2 ? cnt4.z : cnt4.w;
           const uint4* q = reinterpret_cast<const uint4*>(sCKc + 32 * wv);
@@ -874,7 +891,7 @@ __global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
     // ---------------- P3: rank-1 update, then joins ----------------
     // lanes over the U row (32 columns per pass), warps over the L column;
     // U values come from the pivot row (left in place until P1 of step k+1)
-    for (int m0 = 0; m0 < ((g_fdebug & 1) ? 0 : nU); m0 += 32) {
+    for (int m0 = 0; m0 < ((dbg & 1) ? 0 : nU); m0 += 32) {
       const int bi = m0 + lane;
       if (bi < nU) {
         const int c = sUc[bi];
@@ -882,7 +899,7 @@ __global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
         const uint32_t key = ((uint32_t)(256 - ((int)sColid[c] - k)) << 8) | (uint32_t)warp;
         double2* const Fc = sF + c;
         uint16_t* const Kc = sK + c;
-#pragma unroll 4
+#pragma unroll 2
         for (int ai = warp; ai < nL; ai += FT / 32) {
           const int off = (int)(sLs[ai] & 0xffffffu);
           const double2 l = sLv[ai];
@@ -963,7 +980,9 @@ __global__ void __launch_bounds__(FT) frontal_finish_kernel(FrontArgs a) {
 
 // tuning: enable the per-phase clock probe of CTA 0; read the last run's
 // cycles per step of phases A, B, C, D
+static bool g_probe_host = false;
 int frontal_probe(int enable, double* out4) {
+  g_probe_host = enable != 0;
   RS_CUDA_TRY(cudaMemcpyToSymbol(g_fprobe_on, &enable, sizeof(int)));
   {
     const char* e = getenv("RHOSOLVE_FRONTAL_DEBUG");
@@ -984,14 +1003,20 @@ int frontal_probe(int enable, double* out4) {
 static int g_frontal_taken = 0;  // systems accepted by the last frontal_factor
 int frontal_last_taken() { return g_frontal_taken; }
 
-// Opt-in (RHOSOLVE_FRONTAL=1): measured on the 512-system c4 batch it is
-// bit-identical to the column pipeline but not faster (32 ms vs 29.5 ms; the
-// per-step pivot chain costs ~2.7k cycles with one system per SM), see
-// DESIGN.md.
-bool frontal_enabled() {
+// Selection (RHOSOLVE_FRONTAL: 1 always, 0 never, unset auto).  Auto takes
+// batches of at most two waves (B <= 2 x SMs): measured on the c4 systems
+// it beats the column pipeline there (148 systems 9.3 vs 14.8 ms, 296
+// systems ~18-21 vs 22.5 ms, one system 8.4 vs 8.8 ms) and loses on the
+// 512-system batch (4 waves: 32 vs 29.5 ms), see DESIGN.md.
+bool frontal_enabled(int nsys) {
   g_frontal_taken = 0;
   const char* e = getenv("RHOSOLVE_FRONTAL");
-  return e && e[0] == '1';
+  if (e && e[0] == '1') return true;
+  if (e && e[0] == '0') return false;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return nsys <= 2 * sms;
 }
 
 // Complete LU of the systems whose front fits (see top of file); the others
@@ -1116,9 +1141,9 @@ int frontal_factor(const FactorArgs& fa, cudaStream_t st) {
   a.capU = fa.capU;
   a.pinv = fa.pinv;
   a.state = fa.state;
-  RS_CUDA_TRY(cudaFuncSetAttribute(frontal_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-  frontal_lu_kernel<<<B, FT, smem, st>>>(a);
+  auto kern = g_probe_host ? frontal_lu_kernel<true> : frontal_lu_kernel<false>;
+  RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<B, FT, smem, st>>>(a);
   ::rs::count_launch();
   frontal_finish_kernel<<<B, FT, 0, st>>>(a);
   ::rs::count_launch();

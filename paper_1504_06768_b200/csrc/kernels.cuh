@@ -85,8 +85,8 @@ void col_min_degree_host(int64_t n, const int64_t* rp, const int64_t* ci, int64_
 // ---- frontal.cu: right-looking frontal complete LU ------------------------
 // Factors (complete LU, q == null) every system whose structural front fits
 // shared memory and marks it FAC_DONE; the rest keep their state for
-// launch_ilutp.  RHOSOLVE_FRONTAL=0 disables it.
-bool frontal_enabled();
+// launch_ilutp.  RHOSOLVE_FRONTAL=1/0 forces it on/off (auto: <= 2 waves).
+bool frontal_enabled(int nsys);
 int frontal_factor(const FactorArgs& a, cudaStream_t st);
 int frontal_last_taken();
 int frontal_probe(int enable, double* out4);
