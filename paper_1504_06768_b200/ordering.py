@@ -15,7 +15,7 @@ import torch
 from . import _lib
 from .sparse import DeviceCSR, Permutation, as_host_csr
 
-__all__ = ["rcm", "rcm_device", "permute", "permute_rows_cols", "permute_vector", "BandProfile",
+__all__ = ["rcm", "rcm_device", "shared_structure", "permute", "permute_rows_cols", "permute_vector", "BandProfile",
            "band_profile", "weighted_mbm", "col_min_degree", "StructurallySingularError",
            "cmd_plan"]
 
@@ -29,10 +29,39 @@ def _mat(a):
     return a.matrix if hasattr(a, "matrix") else a
 
 
+def shared_structure(M):
+    """True when every system of a batch stores exactly system 0's pattern
+    (same row extents and column indices; values may differ) -- the config-4
+    sweep, whose instances differ only in a detuning."""
+    if M.nsys <= 1:
+        return False
+    nnz = M.nnz
+    if nnz % M.nsys:
+        return False
+    per = nnz // M.nsys
+    rp = M.row_ptr[:-1].view(M.nsys, M.n)
+    off = rp - rp[:, :1]
+    same = torch.logical_and(
+        (rp[:, 0] == torch.arange(M.nsys, device=rp.device, dtype=rp.dtype) * per).all(),
+        (off == off[0]).all())
+    same = torch.logical_and(same, (M.col_idx.view(M.nsys, per) == M.col_idx[:per]).all())
+    return bool(same.item())
+
+
 def rcm_device(a):
-    """(forward, inverse) int32 device tensors, nsys*n long (local indices)."""
+    """(forward, inverse) int32 device tensors, nsys*n long (local indices).
+    RCM depends on the pattern only, so a batch whose systems share system
+    0's pattern is ordered once and the permutation replicated (the same
+    bits as ordering every system)."""
     M = _mat(a)
     dev = M.values.device
+    if shared_structure(M):
+        per = M.nnz // M.nsys
+        fwd = torch.empty(M.n, dtype=torch.int32, device=dev)
+        inv = torch.empty_like(fwd)
+        _lib.call("rs_rcm", 1, M.n, _lib.ptr(M.row_ptr), _lib.ptr(M.col_idx[:per]),
+                  _lib.ptr(fwd), _lib.ptr(inv), _lib.stream_ptr())
+        return fwd.repeat(M.nsys), inv.repeat(M.nsys)
     fwd = torch.empty(M.nsys * M.n, dtype=torch.int32, device=dev)
     inv = torch.empty_like(fwd)
     _lib.call("rs_rcm", M.nsys, M.n, _lib.ptr(M.row_ptr), _lib.ptr(M.col_idx), _lib.ptr(fwd),

@@ -86,6 +86,9 @@ def _rand_csr(rng, n, density, long_rows=(), empty_rows=()):
     (6000, 1, 0.0015, (17, 4000), (0, 5, 5999)),  # rows longer than a staging chunk
     (1600, 5, 0.005, (1599,), (0,)),   # CTAs straddling system boundaries
     (1, 3, 1.0, (), ()),
+    # more 32-row groups than resident warps: each warp of the streamed
+    # kernel walks several groups, groups straddle systems (n odd)
+    (997, 100, 0.006, (500,), (0, 31, 32, 996)),
 ])
 def test_spmv_random_batches_bit_exact(cuda, n, nsys, density, long_rows, empty_rows):
     rng = np.random.default_rng(n + nsys)
@@ -198,12 +201,24 @@ def test_rcm_random_corpus_bit_exact(cuda):
     assert k == 30
 
 
-def test_rcm_batch_equals_single(cuda):
+@pytest.mark.parametrize("mixed", [False, True])
+def test_rcm_batch_equals_single(cuda, mixed):
+    """Shared-pattern batches (the c4 sweep) are ordered once; a batch mixing
+    patterns (a trace-modified system) is ordered per system.  Both give
+    every system the reference's permutation."""
     mats = [_host(O.shift(oracle_L(*model("c4", i=i)))) for i in (0, 100, 511)]
-    fwd, inv = ordering.rcm_device(from_host(mats))
+    if mixed:
+        Lo = oracle_L(*model("c4", i=7))
+        mo, _, _ = O.build_modified(Lo, 40, O.default_weight(Lo))
+        mats.insert(1, _host(mo))
+    A = from_host(mats)
+    assert ordering.shared_structure(A) == (not mixed)
+    fwd, inv = ordering.rcm_device(A)
     for b, m in enumerate(mats):
-        f1, _ = O.rcm(O.CSR(m.nrows, m.ncols, m.row_ptr, m.col_idx, m.values))
-        assert bits_equal(fwd[b * m.nrows:(b + 1) * m.nrows].cpu().numpy().astype(np.int64), f1)
+        f1, i1 = O.rcm(O.CSR(m.nrows, m.ncols, m.row_ptr, m.col_idx, m.values))
+        sl = slice(b * m.nrows, (b + 1) * m.nrows)
+        assert bits_equal(fwd[sl].cpu().numpy().astype(np.int64), f1)
+        assert bits_equal(inv[sl].cpu().numpy().astype(np.int64), i1)
 
 
 def test_vector_kernels(cuda):
