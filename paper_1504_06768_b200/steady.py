@@ -74,7 +74,10 @@ assert _STATS_DT.itemsize == _lib.STATS_BYTES
 
 
 def _sync():
-    torch.cuda.synchronize()
+    """Stage boundary for the *_time fields: the current stream only, so work
+    queued on the side stream (start-vector upload, plain-matrix permute)
+    keeps overlapping the next stage."""
+    torch.cuda.current_stream().synchronize()
     return time.perf_counter()
 
 
@@ -98,17 +101,42 @@ def _start_vectors(n, seeds):
     return out
 
 
+_SIDE = {}
+
+
+def _side_stream(device):
+    """A second stream per device for copies and kernels that only the
+    solve needs, so they overlap the factorization."""
+    st = _SIDE.get(device)
+    if st is None:
+        st = _SIDE[device] = torch.cuda.Stream(device=device)
+    return st
+
+
+def _upload_start_vectors(n, seeds, device, stream):
+    """Draw the start vectors (host thread) and upload them on `stream` as
+    soon as they exist, overlapping the factorization; the caller makes its
+    stream wait for `stream` before the solve."""
+    host = _start_vectors(n, seeds)
+    with torch.cuda.stream(stream):
+        dev = host.to(device, non_blocking=True)
+    return dev, host
+
+
 def _require_plain(L):
     if L.variant != "plain":
         raise ValueError(f"expected the plain variant, got {L.variant!r}")
     return liouville.on_device(L)
 
 
-def _prepare(system, ordering_name, plain=None):
+def _prepare(system, ordering_name, plain=None, side=None):
     """steady._prepare (steady.py:74-108) on the device.  Returns (matrix,
     rhs, plain_ordered, forward, label, x0_gather): the solution is x[forward]
     (None: unchanged); x0_gather maps a start vector drawn in the reference's
-    coordinates into the working ones (None: the same)."""
+    coordinates into the working ones (None: the same).  `side`: a stream on
+    which the plain matrix (read only by the solve) is permuted, overlapping
+    the factorization; the caller makes its stream wait for `side` before
+    the solve."""
     m = system.matrix
     if ordering_name == "natural":
         return m, system.rhs, plain, None, "natural", None
@@ -118,7 +146,19 @@ def _prepare(system, ordering_name, plain=None):
         prhs = None
         if system.rhs is not None:
             prhs = ordering.permute_vector(system.rhs, fwd, m.nsys, m.n, gather=False)
-        pp = ordering.permute(plain, fwd, inv) if plain is not None else None
+        pp = None
+        if plain is not None:
+            if side is None:
+                pp = ordering.permute(plain, fwd, inv)
+            else:
+                main = torch.cuda.current_stream(m.values.device)
+                side.wait_stream(main)
+                with torch.cuda.stream(side):
+                    pp = ordering.permute(plain, fwd, inv)
+                    for t in (pp.row_ptr, pp.col_idx, pp.values):
+                        t.record_stream(main)
+                    for t in (fwd, inv, plain.row_ptr, plain.col_idx, plain.values):
+                        t.record_stream(side)
         return pm, prhs, pp, fwd, "rcm", None
     if ordering_name == "cmd":
         # MBM rows (when the diagonal is not fully stored) and the minimum-
@@ -275,9 +315,12 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
     t0 = _sync()
     # the seeded start vectors (numpy PCG64, drawn exactly as steady.py:171-174)
     # are generated on a host thread while the GPU orders and factors
-    x0_future = _POOL.submit(_start_vectors, L.n, list(seeds))
+    device = L.matrix.values.device
+    side = _side_stream(device)
+    x0_future = _POOL.submit(_upload_start_vectors, L.n, list(seeds), device, side)
     shifted = liouville.shift(L, sigma)
-    mat, _, plain, fwd, label, x0_map = _prepare(shifted, ordering_name, plain=L.matrix)
+    mat, _, plain, fwd, label, x0_map = _prepare(shifted, ordering_name, plain=L.matrix,
+                                                 side=side)
     if plain is None:
         plain = L.matrix
     t1 = _sync()
@@ -292,7 +335,10 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
         f = factor.factor_batch(mat, float(d), float(p), raise_on_fail=raise_errors)
         mode = _lib.INV_GMRES if solver == "gmres" else _lib.INV_BICGSTAB
     t2 = _sync()
-    x0 = x0_future.result().to(mat.values.device, non_blocking=True)
+    x0, _host = x0_future.result()
+    main = torch.cuda.current_stream(device)
+    main.wait_stream(side)  # the start vectors and the permuted plain matrix
+    x0.record_stream(main)
     if x0_map is not None:
         x0 = ordering.permute_vector(x0, x0_map, mat.nsys, mat.n, gather=True)
     if not f.ok:  # some system of the batch failed to factor
