@@ -238,10 +238,12 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def measured_traffic(cfg, kernel):
+def measured_traffic(cfg, kernel, systems=None):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
     (profiles/*_traffic_<cfg>.json, written by tools/ncu_traffic.py from an
-    `ncu --set full` run of the same workload): (bytes, source) or None."""
+    `ncu --set full` run of the same workload): (bytes, source) or None.
+    An entry captured on a batch of `systems` systems is scaled to this
+    run's batch (the per-GPU shard at N > 1)."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_traffic_{cfg}.json")),
                        reverse=True):
@@ -251,7 +253,13 @@ def measured_traffic(cfg, kernel):
         except (OSError, ValueError):
             continue
         if kernel in d:
-            return float(d[kernel]["dram_bytes_per_launch"]), os.path.relpath(path, ROOT)
+            e = d[kernel]
+            v = float(e["dram_bytes_per_launch"])
+            src = os.path.relpath(path, ROOT)
+            if systems and e.get("systems") and e["systems"] != systems:
+                v *= systems / e["systems"]
+                src += f" (captured on {e['systems']} systems, scaled to {systems})"
+            return v, src
     return None
 
 
@@ -317,10 +325,14 @@ def kernel_timings(L, skw, torch, seeds):
                   _lib.ptr(state), _lib.stream_ptr())
 
     nLU = int(np.sum(f.lnnz) + np.sum(f.unnz))
+    fact_s = timed(run_fact, reps=3)
+    frontal = _lib.load().rs_debug_frontal_taken() == B  # rs_factorize's own choice
     out["factorize"] = {
-        "seconds": timed(run_fact, reps=3), "bytes": 20 * nnz + 20 * nLU + 8 * B * (n + 1),
-        "kernel": "ilutp_pipeline_kernel",
-        "note": f"{B} system(s), column-pipelined left-looking {'LU' if d == 0 else 'ILUTP'}"}
+        "seconds": fact_s, "bytes": 20 * nnz + 20 * nLU + 8 * B * (n + 1),
+        "kernel": "frontal_lu_kernel" if frontal else "ilutp_pipeline_kernel",
+        "note": (f"{B} system(s), right-looking frontal complete LU (analysis + elimination "
+                 "+ finish)" if frontal else
+                 f"{B} system(s), column-pipelined left-looking {'LU' if d == 0 else 'ILUTP'}")}
     x = torch.randn(B * n, dtype=torch.complex128, device="cuda")
     y = torch.empty_like(x)
 
@@ -500,7 +512,7 @@ def run_gpu(args):
     step_s = total / args.steps
     dom = max(("factorize", "solver"), key=lambda k: kt[k]["seconds"])
     ach = kernels[dom]["achieved_gbs"]
-    traffic = measured_traffic(cfg, kt[dom]["kernel"])
+    traffic = measured_traffic(cfg, kt[dom]["kernel"], L.nsys)
     roof = {"bound": "hbm", "kernel": kt[dom]["kernel"], "achieved": ach, "peak": peak,
             "unit": "GB/s", "frac": ach / peak,
             "traffic": traffic[0] if traffic else None,
