@@ -756,23 +756,24 @@ __global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
       // compacted keys: candidates first, padding 0xffffffff after
       const int pos = cand ? __popc(bal & lt_mask) : __popc(bal) + __popc(~bal & lt_mask);
       sCKc[32 * warp + pos] = key;
-      int bs = sl;
-      for (int o = 16; o; o >>= 1) {
-        const double om = __shfl_xor_sync(FULL, mag, o);
-        const int orr = __shfl_xor_sync(FULL, rid, o);
-        const int os = __shfl_xor_sync(FULL, bs, o);
-        if (om > mag || (om == mag && orr < rid)) {
-          mag = om;
-          rid = orr;
-          bs = os;
-        }
-      }
+      // warp argmax of (mag, -row) with three redux.sync instead of a
+      // five-level shuffle tree: non-negative doubles order like their bit
+      // patterns; "no candidate" (-1) maps to key 0 like a zero magnitude,
+      // and either way a best magnitude of 0 fails the pivot test in P2
+      const unsigned long long km =
+          mag >= 0.0 ? (unsigned long long)__double_as_longlong(mag) : 0ull;
+      const unsigned khi = (unsigned)(km >> 32), klo = (unsigned)km;
+      const unsigned mh = __reduce_max_sync(FULL, khi);
+      const unsigned ml = __reduce_max_sync(FULL, khi == mh ? klo : 0u);
+      const bool top = khi == mh && klo == ml;
+      const unsigned br = __reduce_min_sync(FULL, top ? (unsigned)rid : 0xffffffffu);
+      const unsigned wm = __ballot_sync(FULL, top && (unsigned)rid == br);
       if (lane == 0) {
         sCb[warp] = bal;
         sCnt[warp] = __popc(bal);
-        sWmag[warp] = mag;
-        sWrid[warp] = rid;
-        sWslot[warp] = bs;
+        sWmag[warp] = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+        sWrid[warp] = (int)br;
+        sWslot[warp] = 32 * warp + __ffs(wm) - 1;
       }
     } else if (warp < 8) {
       if (p_prev >= 0)  // the freed pivot row returns to zeros / absent
@@ -839,16 +840,19 @@ __global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
       if (mine) {
         const uint32_t key = ((uint32_t)sK[sl * CSP + ck] << 16) | (uint32_t)sRow[sl];
         const uint32_t pkey = ((uint32_t)sK[p * CSP + ck] << 16) | (uint32_t)sRow[p];
+        // all 128 compacted keys (non-candidates hold 0xffffffff, never
+        // below a key): 32 independent broadcast loads, no count-dependent
+        // loop, so they issue back to back
         int rank = -(int)(pkey < key);
-#pragma unroll 1
-        for (int wv = 0; wv < 4; ++wv) {
-          const int cnt = wv == 0 ? cnt4.x : wv == 1 ? cnt4.y : wv == 2 ? cnt4.z : cnt4.w;
-          const uint4* q = reinterpret_cast<const uint4*>(sCKc + 32 * wv);
-          for (int j = 0; j < cnt; j += 4) {
-            const uint4 v = q[j >> 2];
-            rank += (int)(v.x < key) + (int)(v.y < key) + (int)(v.z < key) + (int)(v.w < key);
-          }
+        const uint4* q = reinterpret_cast<const uint4*>(sCKc);
+        int r0 = 0, r1 = 0;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const uint4 v = q[j], u = q[j + 1];
+          r0 += (int)(v.x < key) + (int)(v.y < key) + (int)(v.z < key) + (int)(v.w < key);
+          r1 += (int)(u.x < key) + (int)(u.y < key) + (int)(u.z < key) + (int)(u.w < key);
         }
+        rank += r0 + r1;
         const double2 rp = recipc(piv);
         const double2 l = cmul_plain(sF[sl * CSP + ck], rp);
         sLs[rank] = ((uint32_t)sl << 24) | (uint32_t)(sl * CSP);
