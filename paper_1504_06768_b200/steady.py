@@ -387,24 +387,34 @@ def inverse_power_batch(L, seeds, sigma=DEFAULT_SIGMA, tol=1e-14, inner="direct"
         threads)
     results = []
     method = "power-direct" if inner == "direct" else "power-doubly-iterative"
-    for b in range(L.nsys):
-        if out is None:
+    fills = np.asarray(f.fill_factors, dtype=np.float64).tolist()
+    if out is None:
+        for b in range(L.nsys):
             err = (f"zero pivot at elimination step {int(f.fail[b])}" if f.fail[b] >= 0
                    else None)
             results.append(SteadyStateResult(
                 rho=None, method=method, ordering=label, residual=float("nan"), iterations=0,
-                fill_factor=float(f.fill_factors[b]), condest=None, build_time=t1 - t0,
+                fill_factor=fills[b], condest=None, build_time=t1 - t0,
                 factor_time=t2 - t1, solve_time=0.0, seed=seeds[b], error=err))
-            continue
-        s = st[b]
-        err = None if s["status"] == _lib.SOLVE_OK else _STATUS_MSG[int(s["status"])][1]
+        return results
+    # per-system fields as Python lists once (structured-array element access
+    # per system costs more than the solve of a small system)
+    rho, resid = out
+    resid = resid.tolist()
+    status = st["status"].tolist()
+    outer = st["outer"].tolist()
+    it = inner == "iterative"
+    cond = st["condest"].tolist() if it else None
+    inner_tot = st["inner_total"].tolist() if it else None
+    bt, ft, stime = t1 - t0, t2 - t1, t3 - t2
+    for b in range(L.nsys):
+        err = None if status[b] == _lib.SOLVE_OK else _STATUS_MSG[int(status[b])][1]
         results.append(SteadyStateResult(
-            rho=out[0][b], method=method, ordering=label, residual=float(out[1][b]),
-            iterations=int(s["outer"]), fill_factor=float(f.fill_factors[b]),
-            condest=float(s["condest"]) if inner == "iterative" else None,
-            build_time=t1 - t0, factor_time=t2 - t1, solve_time=t3 - t2, seed=seeds[b],
-            inner_iterations=int(s["inner_total"]) if inner == "iterative" else None,
-            error=err))
+            rho=rho[b], method=method, ordering=label, residual=resid[b],
+            iterations=outer[b], fill_factor=fills[b],
+            condest=cond[b] if it else None,
+            build_time=bt, factor_time=ft, solve_time=stime, seed=seeds[b],
+            inner_iterations=inner_tot[b] if it else None, error=err))
     return results
 
 
