@@ -90,14 +90,35 @@ def start_vector(n, seed):
 _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="rhosolve-rng")
 
 
-def _start_vectors(n, seeds):
+_DRAW_POOL = ThreadPoolExecutor(max_workers=2, thread_name_prefix="rhosolve-draw")
+
+
+def _start_vectors(n, seeds, pin=True):
     """The batch's start vectors drawn straight into pinned host memory, so
-    the upload is one asynchronous DMA."""
+    the upload is one asynchronous DMA.  Same bits as start_vector: one
+    standard_normal(2n) call continues the PCG64 stream exactly as the
+    reference's two calls of n (real part first), and default_rng(seed) is
+    Generator(PCG64(seed)); large batches are split over two threads (the
+    normal draws release the GIL)."""
     seeds = list(seeds)
-    out = torch.empty(len(seeds) * n, dtype=torch.complex128, pin_memory=True)
-    view = out.numpy()
-    for i, sd in enumerate(seeds):
-        view[i * n:(i + 1) * n] = start_vector(n, sd)
+    out = torch.empty(len(seeds) * n, dtype=torch.complex128, pin_memory=pin)
+    view = out.numpy().reshape(len(seeds), n)
+
+    def part(lo, hi):
+        tmp = np.empty(2 * n)
+        for i in range(lo, hi):
+            np.random.Generator(np.random.PCG64(seeds[i])).standard_normal(2 * n, out=tmp)
+            view[i].real = tmp[:n]
+            view[i].imag = tmp[n:]
+
+    m = len(seeds)
+    if m >= 64:
+        h = m // 2
+        fut = _DRAW_POOL.submit(part, h, m)
+        part(0, h)
+        fut.result()
+    else:
+        part(0, m)
     return out
 
 

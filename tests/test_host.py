@@ -97,3 +97,13 @@ def test_shared_structure_detection():
     rp4 = torch.tensor([0, 1, 2, 3], dtype=torch.int32)         # other nnz
     ci4 = torch.tensor([0, 1, 2], dtype=torch.int32)
     assert not ordering.shared_structure(batch([rp1, rp4], [ci1, ci4]))
+
+
+@pytest.mark.parametrize("m", [1, 5, 100])
+def test_batch_start_vectors_match_reference_draw(m):
+    """The batched draw (one standard_normal(2n) per seed, two threads for
+    large batches) gives the reference's start_vector bits (steady.py:171-174)."""
+    seeds = list(range(2, 2 + m))
+    got = steady._start_vectors(1600, seeds, pin=False).numpy()
+    ref = np.concatenate([steady.start_vector(1600, s) for s in seeds])
+    assert bits_equal(got, ref)
