@@ -56,14 +56,16 @@ class LiouvillianSystem:
                 f"nsys={self.nsys}, nnz={self.matrix.nnz})")
 
 
-def on_device(L, device=None):
+def on_device(L, device=None, values_stream=None):
     """L with its matrix resident on the GPU: a host CSRMatrix, a list-built
     batch or a PinnedBatchCSR is uploaded (pinned batches asynchronously on
-    the current stream); a DeviceCSR passes through unchanged."""
+    the current stream, values on `values_stream` when given -- see
+    sparse.from_host); a DeviceCSR passes through unchanged."""
     if isinstance(L.matrix, DeviceCSR):
         return L
-    return LiouvillianSystem(from_host(L.matrix, device), L.hilbert_dim, L.variant,
-                             sigma=L.sigma, weight=L.weight, rhs=L.rhs)
+    return LiouvillianSystem(from_host(L.matrix, device, values_stream=values_stream),
+                             L.hilbert_dim, L.variant, sigma=L.sigma, weight=L.weight,
+                             rhs=L.rhs)
 
 
 def _dev_op(m, dev):

@@ -313,14 +313,26 @@ def pin_batch(mats):
     return PinnedBatchCSR(n, B, rp, ci, v)
 
 
-def from_host(mats, device=None):
+def from_host(mats, device=None, values_stream=None):
     """Upload one CSR, a list of equal-order CSRs (as a batch), or a
-    PinnedBatchCSR (asynchronous copies on the current stream) to the GPU."""
+    PinnedBatchCSR (asynchronous copies on the current stream) to the GPU.
+    values_stream (pinned batches): the values travel on that stream instead,
+    so structure-only work (RCM) can start as soon as row_ptr / col_idx have
+    landed; the caller makes its stream wait for values_stream before any
+    kernel reads the values."""
     dev = device or torch.device("cuda")
     if isinstance(mats, PinnedBatchCSR):
-        return DeviceCSR(mats.n, mats.nsys, mats.row_ptr.to(dev, non_blocking=True),
-                         mats.col_idx.to(dev, non_blocking=True),
-                         mats.values.to(dev, non_blocking=True))
+        rp = mats.row_ptr.to(dev, non_blocking=True)
+        ci = mats.col_idx.to(dev, non_blocking=True)
+        if values_stream is None:
+            v = mats.values.to(dev, non_blocking=True)
+        else:
+            main = torch.cuda.current_stream(dev)
+            values_stream.wait_stream(main)
+            with torch.cuda.stream(values_stream):
+                v = mats.values.to(dev, non_blocking=True)
+            v.record_stream(main)
+        return DeviceCSR(mats.n, mats.nsys, rp, ci, v)
     if not isinstance(mats, (list, tuple)):
         mats = [mats]
     mats, n, offs = _pack(mats)

@@ -25,6 +25,7 @@ import torch
 
 from . import _lib, factor, liouville, ordering
 from .liouville import DEFAULT_SIGMA
+from .sparse import DeviceCSR
 
 __all__ = ["SteadyStateResult", "solve_direct", "solve_iterative", "inverse_power",
            "inverse_power_batch", "solve_batch", "InnerSolverError", "PowerIterationError",
@@ -144,25 +145,27 @@ def _upload_start_vectors(n, seeds, device, stream):
     return dev, host
 
 
-def _require_plain(L):
+def _require_plain(L, values_stream=None):
     if L.variant != "plain":
         raise ValueError(f"expected the plain variant, got {L.variant!r}")
-    return liouville.on_device(L)
+    return liouville.on_device(L, values_stream=values_stream)
 
 
-def _prepare(system, ordering_name, plain=None, side=None):
+def _prepare(system, ordering_name, plain=None, side=None, rcm=None):
     """steady._prepare (steady.py:74-108) on the device.  Returns (matrix,
     rhs, plain_ordered, forward, label, x0_gather): the solution is x[forward]
     (None: unchanged); x0_gather maps a start vector drawn in the reference's
     coordinates into the working ones (None: the same).  `side`: a stream on
     which the plain matrix (read only by the solve) is permuted, overlapping
     the factorization; the caller makes its stream wait for `side` before
-    the solve."""
+    the solve.  rcm: (forward, inverse) already computed for this pattern
+    (RCM ignores the diagonal, so the plain matrix's ordering is the shifted
+    one's)."""
     m = system.matrix
     if ordering_name == "natural":
         return m, system.rhs, plain, None, "natural", None
     if ordering_name == "rcm":
-        fwd, inv = ordering.rcm_device(m)
+        fwd, inv = rcm if rcm is not None else ordering.rcm_device(m)
         pm = ordering.permute(m, fwd, inv)
         prhs = None
         if system.rhs is not None:
@@ -325,7 +328,13 @@ _STATUS_MSG = {
 
 def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, max_iter, seeds,
                 raise_errors, threads=0):
-    L = _require_plain(L)
+    m = L.matrix
+    device = (m.values.device if isinstance(m, DeviceCSR)
+              else torch.device("cuda", torch.cuda.current_device()))
+    side = _side_stream(device)
+    # host batches upload their values on the side stream: the RCM below
+    # needs only the pattern and overlaps that copy
+    L = _require_plain(L, values_stream=side)
     if inner not in ("direct", "iterative"):
         raise ValueError(f"unknown inner solve {inner!r}")
     if not tol > 0:
@@ -336,12 +345,14 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
     t0 = _sync()
     # the seeded start vectors (numpy PCG64, drawn exactly as steady.py:171-174)
     # are generated on a host thread while the GPU orders and factors
-    device = L.matrix.values.device
-    side = _side_stream(device)
     x0_future = _POOL.submit(_upload_start_vectors, L.n, list(seeds), device, side)
+    # RCM of the plain pattern = RCM of the shifted one (the graph drops
+    # self-loops, and shifting only adds diagonal entries: ordering.py:62-79)
+    rcm = ordering.rcm_device(L.matrix) if ordering_name == "rcm" else None
+    torch.cuda.current_stream(device).wait_stream(side)  # the values have landed
     shifted = liouville.shift(L, sigma)
     mat, _, plain, fwd, label, x0_map = _prepare(shifted, ordering_name, plain=L.matrix,
-                                                 side=side)
+                                                 side=side, rcm=rcm)
     if plain is None:
         plain = L.matrix
     t1 = _sync()

@@ -5,7 +5,7 @@ import pytest
 
 from oracle import oracle as O
 from paper_1504_06768_b200 import liouville, steady
-from tests.helpers import model, oracle_L
+from tests.helpers import bits_equal, model, oracle_L
 
 pytestmark = pytest.mark.gpu
 
@@ -77,6 +77,25 @@ def test_c4_batch_power_direct(cuda):
         ref = O.inverse_power(oracle_L(H, c), 40, tol=1e-12, inner="direct", seed=2 + i)
         assert r.error is None
         _check(r, ref)
+
+
+@pytest.mark.parametrize("ordering_name", ["rcm", "natural"])
+def test_c4_batch_from_pinned_host_buffers(cuda, ordering_name):
+    """The end-to-end path of bench.py: a PinnedBatchCSR (host) input, values
+    uploaded on the side stream while the pattern is RCM-ordered, gives the
+    same bits as the device-resident input."""
+    from paper_1504_06768_b200.sparse import pin_batch
+    idx = [0, 7, 300, 511]
+    L = liouville.build_liouvillian_batch([model("c4", i=i) for i in idx])
+    seeds = [2 + i for i in idx]
+    kw = dict(tol=1e-12, inner="direct", ordering_name=ordering_name)
+    dev = steady.inverse_power_batch(L, seeds, **kw)
+    pinned = pin_batch([L.matrix.system(b) for b in range(L.nsys)])
+    host = steady.inverse_power_batch(liouville.LiouvillianSystem(pinned, 40, "plain"), seeds, **kw)
+    for a, b in zip(dev, host):
+        assert a.error is None and b.error is None
+        assert bits_equal(a.rho, b.rho)
+        assert a.residual == b.residual
 
 
 @pytest.mark.slow
