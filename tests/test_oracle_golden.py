@@ -140,3 +140,15 @@ def test_c2_c3_reference_results_are_physical():
         assert float(g["power_bicgstab_residual"]) <= 1e-10
         assert abs(np.trace(rho) - 1) < 1e-12
         assert np.max(np.abs(rho - rho.conj().T)) < 1e-12
+
+
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c2", {}), ("c4", {"i": 0}), ("c4", {"i": 511})])
+def test_rcm_of_plain_equals_rcm_of_shifted(name, kw):
+    """The GPU path orders the plain pattern while the shifted values are
+    still uploading (steady._power_core): valid because the RCM graph drops
+    self-loops (ordering.py:62-79) and shifting only adds diagonal entries."""
+    H, c = model(name, **kw)
+    Lo = O.build_liouvillian(H.matrix, [x.matrix for x in c])
+    fp, ip = O.rcm(Lo)
+    fs, is_ = O.rcm(O.shift(Lo))
+    assert bits_equal(fp, fs) and bits_equal(ip, is_)
