@@ -82,7 +82,7 @@ int rs_col_min_degree_host(int64_t n, const int64_t* row_ptr, const int64_t* col
 
 /* Number of systems the last rs_factorize call factored with the
  * right-looking frontal kernel (complete LU whose front fits shared memory;
- * batches of <= 2 waves by default, RHOSOLVE_FRONTAL=1/0 forces it on/off;
+ * batches of <= 3 waves by default, RHOSOLVE_FRONTAL=1/0 forces it on/off;
  * diagnostics and tests). */
 int rs_debug_frontal_taken(void);
 

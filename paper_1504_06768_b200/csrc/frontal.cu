@@ -1008,10 +1008,11 @@ static int g_frontal_taken = 0;  // systems accepted by the last frontal_factor
 int frontal_last_taken() { return g_frontal_taken; }
 
 // Selection (RHOSOLVE_FRONTAL: 1 always, 0 never, unset auto).  Auto takes
-// batches of at most two waves (B <= 2 x SMs): measured on the c4 systems
-// it beats the column pipeline there (148 systems 9.3 vs 14.8 ms, 296
-// systems ~18-21 vs 22.5 ms, one system 8.4 vs 8.8 ms) and loses on the
-// 512-system batch (4 waves: 32 vs 29.5 ms), see DESIGN.md.
+// batches of at most three waves (B <= 3 x SMs): measured on the c4 systems
+// it beats the column pipeline there (148 systems 8.3 vs 14.8 ms, 256
+// systems 14.8 vs 22.6 ms, 444 systems 22.8 vs 26.4 ms, one system 8.4 vs
+// 8.8 ms); on the 512-system batch (a partial fourth wave) it is level
+// (typically 28.9 vs 29.5 ms, with slower outliers), see DESIGN.md.
 bool frontal_enabled(int nsys) {
   g_frontal_taken = 0;
   const char* e = getenv("RHOSOLVE_FRONTAL");
@@ -1020,7 +1021,7 @@ bool frontal_enabled(int nsys) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return nsys <= 2 * sms;
+  return nsys <= 3 * sms;
 }
 
 // Complete LU of the systems whose front fits (see top of file); the others

@@ -35,7 +35,7 @@ def main(count=512, reps=5, modes="101"):
         print("cycles/step P1 P2 P3:", [round(x) for x in ph[:3]])
         print(f"frontal={mode} taken={_lib.load().rs_debug_frontal_taken()} "
               f"median {1e3 * sorted(ts)[len(ts) // 2]:.2f} ms  min {1e3 * min(ts):.2f} ms "
-              f"fill {f.fill_factors[:2]}")
+              f"fill {f.fill_factors[:2]}  all ms {[round(1e3 * t, 1) for t in ts]}")
 
 
 if __name__ == "__main__":
