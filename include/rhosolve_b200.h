@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 1
+#define RS_ABI_VERSION 2
 
 #define RS_OK 0
 #define RS_ERR_ARG -1
@@ -178,6 +178,21 @@ int rs_lu_solve(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t* L_r
                 const int32_t* U_ci, const rs_complex* U_v, const rs_complex* rdiag,
                 const rs_complex* b, rs_complex* x, void* stream);
 
+/* In-place y <- L^{-1} y on the raw CSC L of rs_factorize (unit diagonal
+ * first, pivotal row indices).  Replaces lower_solve (_ckernels.pyx:53-67),
+ * the third function of the kernel seam; bit-identical.  cap = entries
+ * between consecutive systems' Li/Lx (any value when nsys == 1).  Stream-
+ * ordered: no allocation, no synchronisation. */
+int rs_lower_solve(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li,
+                   const rs_complex* Lx, int64_t cap, rs_complex* y, void* stream);
+
+/* In-place y <- U^{-1} y on the raw CSC U (pivot last in each column):
+ * x_c = y_c * recipc(U_cc), then the column scatter.  Replaces upper_solve
+ * (_ckernels.pyx:70-85), the fourth function of the kernel seam;
+ * bit-identical. */
+int rs_upper_solve(int32_t nsys, int32_t n, const int32_t* Up, const int32_t* Ui,
+                   const rs_complex* Ux, int64_t cap, rs_complex* y, void* stream);
+
 /* ---- superoperator (liouville.py) ---------------------------------------- */
 
 /* build_liouvillian (liouville.py:54-77), bit-identical structure and values.
@@ -261,11 +276,12 @@ enum rs_solve_mode {
 /* status codes written to rs_solve_stats.status */
 enum rs_solve_status {
   RS_SOLVE_OK = 0,
-  RS_SOLVE_INNER_BREAKDOWN = 1,   /* InnerSolverError, steady.py:509-512 */
-  RS_SOLVE_INNER_NONFINITE = 2,   /* InnerSolverError, steady.py:509-512 */
-  RS_SOLVE_INNER_NO_PROGRESS = 3, /* InnerSolverError, steady.py:513-514 */
-  RS_SOLVE_UNUSABLE_VECTOR = 4,   /* InnerSolverError, steady.py:525-526 */
-  RS_SOLVE_POWER_NOT_CONVERGED = 5 /* PowerIterationError, steady.py:537-539 */
+  RS_SOLVE_INNER_BREAKDOWN = 1,   /* InnerSolverError, steady.py:218-222 */
+  RS_SOLVE_INNER_NONFINITE = 2,   /* InnerSolverError, steady.py:218-222 */
+  RS_SOLVE_INNER_NO_PROGRESS = 3, /* InnerSolverError, steady.py:223-224 */
+  RS_SOLVE_UNUSABLE_VECTOR = 4,   /* InnerSolverError, steady.py:234-235 */
+  RS_SOLVE_POWER_NOT_CONVERGED = 5, /* PowerIterationError, steady.py:246-248 */
+  RS_SOLVE_SKIPPED = 6              /* masked out by rs_solver_args.skip */
 };
 
 typedef struct rs_solve_stats {
@@ -323,6 +339,24 @@ typedef struct rs_solver_args {
   const rs_complex* Us_val;
   const int32_t* Us_meta;
   const rs_complex* Us_rd;
+  /* optional column pre-ordering of the preconditioner (factor.py:76-78,
+   * 147-148): the factors are those of A[:, q] and every apply ends with
+   * x[q] = y, i.e. x[j] = y[colp[j]] with colp = col_perm.forward (device
+   * int32 [nsys*n], local indices).  NULL: identity.  A, P, rhs and x stay in
+   * the caller's (unpermuted) column coordinates, exactly as in the
+   * reference's krylov / steady drivers. */
+  const int32_t* colp;
+  /* optional per-system mask (device int32 [nsys]): systems with skip[b] != 0
+   * (e.g. a zero pivot in their factorization) are not solved; their stats
+   * report RS_SOLVE_SKIPPED and x is zeroed.  NULL: solve every system. */
+  const int32_t* skip;
+  /* optional residual history of system 0 in the linear modes -- the rows the
+   * reference's gmres/bicgstab write to their `trace` stream (krylov.py:62-64,
+   * 152, 228): trace[2k] = iteration, trace[2k+1] = monitored residual,
+   * k < min(*trace_count, trace_cap).  Device pointers; NULL: not recorded. */
+  double* trace;
+  int32_t* trace_count;
+  int32_t trace_cap;
 } rs_solver_args;
 
 /* One launch runs the whole solve of every system on the device. */

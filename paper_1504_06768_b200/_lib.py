@@ -34,7 +34,7 @@ RS_ERR_STRUCT_SINGULAR = -8
 INV_DIRECT, INV_BICGSTAB, INV_GMRES, LIN_DIRECT, LIN_BICGSTAB, LIN_GMRES = range(6)
 # rs_solve_status
 (SOLVE_OK, SOLVE_INNER_BREAKDOWN, SOLVE_INNER_NONFINITE, SOLVE_INNER_NO_PROGRESS,
- SOLVE_UNUSABLE_VECTOR, SOLVE_POWER_NOT_CONVERGED) = range(6)
+ SOLVE_UNUSABLE_VECTOR, SOLVE_POWER_NOT_CONVERGED, SOLVE_SKIPPED) = range(7)
 # factorize state codes
 FAC_RUNNING, FAC_DONE, FAC_ZERO_PIVOT, FAC_OVERFLOW = range(4)
 
@@ -64,7 +64,8 @@ class SolverArgs(ctypes.Structure):
                 ("max_outer", _i32), ("want_condest", _i32),
                 ("Ls_rowoff", _vp), ("Ls_idx", _vp), ("Ls_val", _vp), ("Ls_meta", _vp),
                 ("Us_rowoff", _vp), ("Us_idx", _vp), ("Us_val", _vp), ("Us_meta", _vp),
-                ("Us_rd", _vp)]
+                ("Us_rd", _vp), ("colp", _vp), ("skip", _vp),
+                ("trace", _vp), ("trace_count", _vp), ("trace_cap", _i32)]
 
 
 # name -> argtypes; every function returns int32 status
@@ -84,6 +85,8 @@ _SIGS = {
     "rs_lu_solve_cols": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp, _vp],
     "rs_lu_solve": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "rs_lower_solve": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp],
+    "rs_upper_solve": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp],
     "rs_liouvillian": [_i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
                        ctypes.POINTER(_f64), _vp, _vp, _vp, ctypes.POINTER(_i64), _vp],
     "rs_shift": [_i32, _i32, _vp, _vp, _vp, _f64, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp],

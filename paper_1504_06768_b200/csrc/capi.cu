@@ -125,6 +125,22 @@ int rs_debug_factor_probe(void* buf) {
   return 0;
 }
 
+int rs_lower_solve(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li,
+                   const rs_complex* Lx, int64_t cap, rs_complex* y, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0 && cap >= 0, "negative size");
+  if (!nsys || !n) return RS_OK;
+  RS_CHECK_ARG(Lp && Li && Lx && y, "null pointer");
+  return half_solve(0, nsys, n, Lp, Li, C2(Lx), cap, M2(y), S(stream));
+}
+
+int rs_upper_solve(int32_t nsys, int32_t n, const int32_t* Up, const int32_t* Ui,
+                   const rs_complex* Ux, int64_t cap, rs_complex* y, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0 && cap >= 0, "negative size");
+  if (!nsys || !n) return RS_OK;
+  RS_CHECK_ARG(Up && Ui && Ux && y, "null pointer");
+  return half_solve(1, nsys, n, Up, Ui, C2(Ux), cap, M2(y), S(stream));
+}
+
 int rs_csr_matvec(int32_t nsys, int32_t n, const int32_t* row_ptr, const int32_t* col_idx,
                   const rs_complex* values, const rs_complex* x, rs_complex* y, void* stream) {
   RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
@@ -469,6 +485,11 @@ int rs_steady_solve(const rs_solver_args* p, void* stream) {
   a.restart_m = p->restart_m;
   a.max_outer = p->max_outer > 0 ? p->max_outer : 50;
   a.want_condest = p->want_condest;
+  a.colp = p->colp;
+  a.skip = p->skip;
+  a.trace = p->trace;
+  a.trace_count = p->trace_count;
+  a.trace_cap = p->trace_cap;
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));

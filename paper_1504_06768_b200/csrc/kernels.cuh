@@ -77,6 +77,10 @@ __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_
                                             int bits_in_smem);
 int ilutp_plan(int32_t n, int warps, int* smem_mode, int* bits_in_smem);
 
+// ---- halfsolve.cu: in-place lower / upper solves on the raw CSC factors ----
+int half_solve(int upper, int B, int32_t n, const int32_t* cp, const int32_t* ci,
+               const double2* cx, int64_t cap, double2* y, cudaStream_t st);
+
 // ---- cmd_order.cu: host-native 'cmd' ordering ---------------------------
 int weighted_mbm_host(int64_t n, const int64_t* rp, const int64_t* ci, const double2* v,
                       int64_t* forward);
@@ -85,7 +89,7 @@ void col_min_degree_host(int64_t n, const int64_t* rp, const int64_t* ci, int64_
 // ---- frontal.cu: right-looking frontal complete LU ------------------------
 // Factors (complete LU, q == null) every system whose structural front fits
 // shared memory and marks it FAC_DONE; the rest keep their state for
-// launch_ilutp.  RHOSOLVE_FRONTAL=1/0 forces it on/off (auto: <= 2 waves).
+// launch_ilutp.  RHOSOLVE_FRONTAL=1/0 forces it on/off (auto: <= 3 waves).
 bool frontal_enabled(int nsys);
 int frontal_factor(const FactorArgs& a, cudaStream_t st);
 int frontal_last_taken();

@@ -47,7 +47,7 @@ struct Ctx {
   const int32_t *Arp, *Aci;
   const double2* Av;
   // preconditioner
-  const int32_t *Lrp, *Lci, *Urp, *Uci, *pinv;
+  const int32_t *Lrp, *Lci, *Urp, *Uci, *pinv, *colp;
   const double2 *Lv, *Uv, *rU;
   bool have_M;
   // column sweeps on the raw CSC factors (colsweep.cuh): the launch's
@@ -60,7 +60,22 @@ struct Ctx {
   double* red;
   double2* small;  // GMRES H/g/sn (global, per system)
   double* cs;
+  // residual history (krylov._trace_write, krylov.py:62-64); null: off
+  double* trace;
+  int32_t* trace_count;
+  int32_t trace_cap;
 };
+
+__device__ __forceinline__ void trace_write(const Ctx& C, int iteration, double residual) {
+  if (C.trace && threadIdx.x == 0) {
+    const int k = *C.trace_count;
+    if (k < C.trace_cap) {
+      C.trace[2 * k] = (double)iteration;
+      C.trace[2 * k + 1] = residual;
+    }
+    *C.trace_count = k + 1;
+  }
+}
 
 // out = M^{-1} in  (factor.solve_lu, factor.py:137-149: y[pinv] = b; L; U;
 // x[q] = y with q = identity on the natural/RCM path).  out may alias in.
@@ -94,7 +109,12 @@ __device__ __noinline__ void csc_psolve(const SolverArgs* a, const double2* in, 
   const cta::ColRing ring = cta::col_ring_at(smem + (yg ? 0 : cta::col_y_bytes(n)), a->ring_R);
   if (yg) cta::col_lu_sweeps<unsigned long long>(n, Ls, Us, ring, P);
   else cta::col_lu_sweeps<unsigned>(n, Ls, Us, ring, P);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[i];
+  // x[q] = y (factor.py:147-148) when the factors are column pre-ordered
+  const int32_t* colp = a->colp ? a->colp + b * n : nullptr;
+  if (colp)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[colp[i]];
+  else
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[i];
   __syncthreads();
 }
 
@@ -139,8 +159,11 @@ __device__ void psolve_body(const Ctx& C, const double2* in, double2* out) {
   __syncthreads();
   cta::upper_solve(n, C.Urp, C.Uci, C.Uv, C.rU, Q, P);
   __syncthreads();
-  if (out != P)
+  if (C.colp) {  // x[q] = y (factor.py:147-148); P is scratch, never the output
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[C.colp[i]];
+  } else if (out != P) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = P[i];
+  }
   __syncthreads();
 }
 
@@ -207,6 +230,7 @@ __device__ IterOut bicgstab(const Ctx& C, const double2* b, const Vecs& W, doubl
   int it = 0;
   while (it < max_iter) {
     const double rnorm = cta::nrm2(n, W.r, C.red);
+    trace_write(C, it, rnorm);
     if (rnorm <= target) {
       const double true_res = cta::resid_nrm2(n, C.Arp, C.Aci, C.Av, W.x, b, C.red);
       if (true_res <= tol * bnorm) {
@@ -401,6 +425,7 @@ __device__ IterOut gmres(const Ctx& C, const double2* b, const Vecs& W, double t
         __syncthreads();
         res = s_res;
         ++j;
+        trace_write(C, total, res);
         if (hnext == 0.0) {
           invariant = true;
           break;
@@ -468,6 +493,14 @@ __global__ void __launch_bounds__(MAXT, 1) steady_solver_kernel(SolverArgs a) {
   const int n = a.n;
   const int64_t bn = (int64_t)b * n;
   SolveStats* st = a.stats + b;
+  if (a.skip && a.skip[b]) {  // e.g. this system's factorization hit a zero pivot
+    for (int i = threadIdx.x; i < n; i += blockDim.x) a.xout[bn + i] = make_double2(0.0, 0.0);
+    if (threadIdx.x == 0) {
+      *st = SolveStats{};
+      st->status = SOLVE_SKIPPED;
+    }
+    return;
+  }
 
   Ctx C;
   C.n = n;
@@ -483,6 +516,12 @@ __global__ void __launch_bounds__(MAXT, 1) steady_solver_kernel(SolverArgs a) {
   C.Uv = a.Uv;
   C.rU = a.rU ? a.rU + bn : nullptr;
   C.pinv = a.pinv ? a.pinv + bn : nullptr;
+  C.colp = a.colp ? a.colp + bn : nullptr;
+  const bool tr = a.trace && b == 0 && a.mode >= MODE_LIN_DIRECT;
+  C.trace = tr ? a.trace : nullptr;
+  C.trace_count = a.trace_count;
+  C.trace_cap = a.trace_cap;
+  if (tr && threadIdx.x == 0) *a.trace_count = 0;
   C.red = red;
   double2* ws = a.work + (int64_t)b * a.work_stride;
   C.csc = a.ring_R > 0;
@@ -562,7 +601,7 @@ __global__ void __launch_bounds__(MAXT, 1) steady_solver_kernel(SolverArgs a) {
     return;
   }
 
-  // ---- inverse power, steady.py:518-541 -----------------------------------
+  // ---- inverse power, steady.py:211-245 -----------------------------------
   // start vector (drawn on the host, steady.py:171-174) normalised here
   {
     const double nx = cta::nrm2(n, in, red);
@@ -711,6 +750,8 @@ __global__ void __launch_bounds__(512) lu_solve_kernel(SolverArgs a, int y_in_sm
   C.Uv = a.Uv;
   C.rU = a.rU + bn;
   C.pinv = a.pinv + bn;
+  C.colp = a.colp ? a.colp + bn : nullptr;
+  C.trace = nullptr;
   C.csc = a.ring_R > 0;
   C.sa = a.self;  // device copy of the launch arguments
   if (C.csc) {
@@ -732,7 +773,9 @@ __global__ void pivot_recip_kernel(int B, int32_t n, const int32_t* __restrict__
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)B * n) return;
   const int64_t b = t / n, k = t % n;
-  rd[t] = recipc(Ux[b * capU + Up[b * (n + 1) + k + 1] - 1]);
+  const int32_t e = Up[b * (n + 1) + k + 1];
+  // a system whose factorization stopped early has no column k: leave 0
+  rd[t] = e > Up[b * (n + 1) + k] ? recipc(Ux[b * capU + e - 1]) : make_double2(0.0, 0.0);
 }
 
 int pivot_recip(int B, int32_t n, const int32_t* Up, const double2* Ux, int64_t capU,

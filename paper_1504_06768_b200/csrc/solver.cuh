@@ -15,11 +15,12 @@ enum SolveMode {
 
 enum SolveStatus {
   SOLVE_OK = 0,
-  SOLVE_INNER_BREAKDOWN = 1,    // steady.py:509-512
-  SOLVE_INNER_NONFINITE = 2,    // steady.py:509-512
-  SOLVE_INNER_NO_PROGRESS = 3,  // steady.py:513-514
-  SOLVE_UNUSABLE_VECTOR = 4,    // steady.py:525-526
-  SOLVE_POWER_NOT_CONVERGED = 5,  // steady.py:537-539
+  SOLVE_INNER_BREAKDOWN = 1,    // steady.py:218-222
+  SOLVE_INNER_NONFINITE = 2,    // steady.py:218-222
+  SOLVE_INNER_NO_PROGRESS = 3,  // steady.py:223-224
+  SOLVE_UNUSABLE_VECTOR = 4,    // steady.py:234-235
+  SOLVE_POWER_NOT_CONVERGED = 5,  // steady.py:246-248
+  SOLVE_SKIPPED = 6,            // masked out (SolverArgs::skip)
 };
 
 // Must match include/rhosolve_b200.h rs_solve_stats.
@@ -83,6 +84,11 @@ struct SolverArgs {
   double2* ywork;          // global sweep vectors (set by the launcher)
   int64_t ywork_stride;
   const SolverArgs* self;  // device copy of these arguments (set by the launcher)
+  const int32_t* colp;     // column pre-ordering: apply ends with x[j] = y[colp[j]] (null: identity)
+  const int32_t* skip;     // per-system mask: != 0 -> not solved (SOLVE_SKIPPED)
+  double* trace;           // (iteration, residual) pairs of system 0 (krylov.py:62-64)
+  int32_t* trace_count;
+  int32_t trace_cap;
 };
 
 // Ring size for the column sweeps of systems of order n in a launch of B

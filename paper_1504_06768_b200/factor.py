@@ -46,7 +46,7 @@ class LUFactors:
     __slots__ = ("n", "nsys", "raw", "capL", "capU", "pinv", "L_rp", "L_ci", "L_v", "U_rp",
                  "U_ci", "U_v", "rdiag", "fill_factors", "complete", "drop_tol",
                  "fill_limit", "fail", "lnnz", "unnz", "ok", "csc", "Ls", "Us", "colp",
-                 "colp_dev")
+                 "colp_dev", "fail_dev", "solvable")
 
     def ensure_rows(self):
         """Build the row-oriented factor copy (row sweeps, exports) once."""
@@ -198,7 +198,11 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
     f.csc = bool(_lib.load().rs_col_sweep_supported(n))
     f.Ls = f.Us = None
     f.colp = f.colp_dev = None
-    if f.ok:
+    # a batch with some failed systems can still be solved on the column-sweep
+    # path: the solver masks the failed ones (rs_solver_args.skip)
+    f.fail_dev = None if f.ok else torch.from_numpy((fail >= 0).astype(np.int32)).to(dev)
+    f.solvable = f.ok or (f.csc and bool(np.any(fail < 0)))
+    if f.solvable:
         f.rdiag = torch.empty(B * n, dtype=torch.complex128, device=dev)
         _lib.call("rs_pivot_recip", B, n, _lib.ptr(Up), _lib.ptr(Ux), capU,
                   _lib.ptr(f.rdiag), st)

@@ -3,8 +3,12 @@ reference krylov module (pkg/src/rhosolve/krylov.py:24-291).
 
 Each call is one launch of the device-resident solver (csrc/solver.cu) with
 the reference control flow (monitor on the preconditioned residual,
-true-residual confirmation, stall exit, breakdown flags).  The `trace`
-argument of the reference is not supported (no per-iteration host I/O)."""
+true-residual confirmation, stall exit, breakdown flags).  `trace` (a text
+stream, krylov.py:62-64) receives the same "iteration,residual" rows as the
+reference's: the kernel records them on the device and they are written out
+after the solve.  A preconditioner built with a column pre-ordering
+(factor.ilutp(col_perm=...)) is applied with its x[q] = y scatter
+(factor.py:147-148), as krylov's solve_lu calls do."""
 
 from __future__ import annotations
 
@@ -47,7 +51,7 @@ class IterResult:
     breakdown: bool
 
 
-def _run(mode, a, b, opts):
+def _run(mode, a, b, opts, trace=None):
     from .steady import _solve  # shared launcher
     A = a.matrix if hasattr(a, "matrix") else a
     opts = opts if opts is not None else IterOptions()
@@ -58,17 +62,17 @@ def _run(mode, a, b, opts):
     if bt.numel() != A.n * A.nsys:
         raise ValueError("system must be square with matching rhs length")
     x, st = _solve(mode, A, None, opts.preconditioner, bt, opts.tol, opts.max_iter,
-                   opts.restart_m, False)
+                   opts.restart_m, False, trace=trace)
     s = st[0]
     return IterResult(x.cpu().numpy() if host else x, int(s["inner_last"]),
                       float(s["final_residual"]), bool(s["converged"]), bool(s["breakdown"]))
 
 
-def gmres(a, b, opts=None):
+def gmres(a, b, opts=None, trace=None):
     """Restarted GMRES(m), left-preconditioned, x0 = 0 (krylov.py:67-178)."""
-    return _run(_lib.LIN_GMRES, a, b, opts)
+    return _run(_lib.LIN_GMRES, a, b, opts, trace)
 
 
-def bicgstab(a, b, opts=None):
+def bicgstab(a, b, opts=None, trace=None):
     """Left-preconditioned BiCGStab, x0 = 0 (krylov.py:181-291)."""
-    return _run(_lib.LIN_BICGSTAB, a, b, opts)
+    return _run(_lib.LIN_BICGSTAB, a, b, opts, trace)

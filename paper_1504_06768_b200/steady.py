@@ -153,9 +153,9 @@ def _require_plain(L, values_stream=None):
 
 def _prepare(system, ordering_name, plain=None, side=None, rcm=None):
     """steady._prepare (steady.py:74-108) on the device.  Returns (matrix,
-    rhs, plain_ordered, forward, label, x0_gather): the solution is x[forward]
-    (None: unchanged); x0_gather maps a start vector drawn in the reference's
-    coordinates into the working ones (None: the same).  `side`: a stream on
+    rhs, plain_ordered, forward, label, col_fwd): the solution is x[forward]
+    (None: unchanged); col_fwd is the column pre-ordering of the factorization
+    ('cmd'; None otherwise), see _factor.  `side`: a stream on
     which the plain matrix (read only by the solve) is permuted, overlapping
     the factorization; the caller makes its stream wait for `side` before
     the solve.  rcm: (forward, inverse) already computed for this pattern
@@ -186,24 +186,36 @@ def _prepare(system, ordering_name, plain=None, side=None, rcm=None):
         return pm, prhs, pp, fwd, "rcm", None
     if ordering_name == "cmd":
         # MBM rows (when the diagonal is not fully stored) and the minimum-
-        # degree column order, both host-native (csrc/cmd_order.cu).  The
-        # reference keeps x in original coordinates and applies the column
-        # order inside factor/solve_lu; here the columns of the working matrix
-        # are permuted instead (identical factors), so the iterate lives in
-        # elimination order: x0 is gathered into it and the solution gathered
-        # back (x[j] = y[colp.forward[j]]).
+        # degree column order, both host-native (csrc/cmd_order.cu).  As in
+        # the reference (steady.py:95-107) the working matrix, the iterate and
+        # the plain matrix stay in the original column coordinates; the
+        # column order only feeds the factorization (`colp`, applied by
+        # _factor below) and every preconditioner apply ends with x[q] = y.
         (rf, ri, cf, ci), label = ordering.cmd_plan(m)
-        pm = ordering.permute_rows_cols(m, ri, cf)
-        prhs = None
-        if system.rhs is not None:
-            prhs = (ordering.permute_vector(system.rhs, rf, m.nsys, m.n, gather=False)
-                    if rf is not None else system.rhs)
-        pp = ordering.permute_rows_cols(plain, None, cf) if plain is not None else None
-        return pm, prhs, pp, cf, label, ci
+        pm = ordering.permute_rows_cols(m, ri, None) if ri is not None else m
+        prhs = system.rhs
+        if system.rhs is not None and rf is not None:
+            prhs = ordering.permute_vector(system.rhs, rf, m.nsys, m.n, gather=False)
+        return pm, prhs, plain, None, label, cf
     raise ValueError(f"unknown ordering {ordering_name!r}")
 
 
-def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0):
+def _factor(mat, d, p, col_fwd=None, raise_on_fail=True):
+    """factor.lu / factor.ilutp with the optional column pre-ordering of the
+    'cmd' path (factor.py:76-78): the column-permuted matrix is factored in
+    natural order (bit-identical factors) and the factors remember the
+    permutation, which every apply undoes (x[q] = y, factor.py:147-148)."""
+    if col_fwd is None:
+        return factor.factor_batch(mat, d, p, raise_on_fail=raise_on_fail)
+    f = factor.factor_batch(ordering.permute_rows_cols(mat, None, col_fwd), d, p,
+                            raise_on_fail=raise_on_fail)
+    f.colp_dev = col_fwd
+    from .sparse import Permutation
+    f.colp = Permutation(col_fwd[:mat.n].cpu().numpy().astype(np.int64))
+    return f
+
+
+def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0, trace=None):
     dev = A.values.device
     B, n = A.nsys, A.n
     if not threads:
@@ -231,12 +243,24 @@ def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0
             a.L_rp, a.L_ci, a.L_v = f.L_rp.data_ptr(), f.L_ci.data_ptr(), f.L_v.data_ptr()
             a.U_rp, a.U_ci, a.U_v = f.U_rp.data_ptr(), f.U_ci.data_ptr(), f.U_v.data_ptr()
         a.rdiag, a.pinv = f.rdiag.data_ptr(), f.pinv.data_ptr()
+        if f.colp_dev is not None:  # every apply ends with x[q] = y (factor.py:147-148)
+            a.colp = f.colp_dev.data_ptr()
+        if not f.ok:  # systems whose factorization failed are masked out
+            a.skip = f.fail_dev.data_ptr()
     a.rhs, a.x, a.stats = rhs.data_ptr(), x.data_ptr(), stats.data_ptr()
     a.tol, a.max_iter, a.restart_m = float(tol), int(max_iter), int(restart_m)
     a.max_outer, a.want_condest = MAX_OUTER, 1 if want_condest else 0
+    if trace is not None:  # residual history of system 0 (krylov.py:62-64)
+        tbuf = torch.zeros(2 * (int(max_iter) + 2), dtype=torch.float64, device=dev)
+        tcnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        a.trace, a.trace_count, a.trace_cap = tbuf.data_ptr(), tcnt.data_ptr(), int(max_iter) + 2
     import ctypes
     _lib.call("rs_steady_solve", ctypes.byref(a), _lib.stream_ptr())
     st = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=_STATS_DT)
+    if trace is not None:
+        rows = tbuf.cpu().numpy().reshape(-1, 2)[:min(int(tcnt.item()), int(max_iter) + 2)]
+        for it, res in rows:
+            trace.write(f"{int(it)},{res:.17g}\n")
     return x, st
 
 
@@ -275,9 +299,9 @@ def solve_direct(L, ordering_name="natural", w=None):
     L = _require_plain(L)
     t0 = _sync()
     modified = liouville.build_modified(L, w)
-    mat, rhs, _, fwd, label, _ = _prepare(modified, ordering_name)
+    mat, rhs, _, fwd, label, colf = _prepare(modified, ordering_name)
     t1 = _sync()
-    f = factor.lu(mat)
+    f = _factor(mat, 0.0, float("inf"), colf)
     t2 = _sync()
     x, _ = _solve(_lib.LIN_DIRECT, mat, None, f, rhs, 1.0, 1, 1, False)
     rho, res = _postprocess(x, fwd, L)
@@ -297,9 +321,13 @@ def solve_iterative(L, ordering_name="natural", solver="gmres", d=1e-4, p=300.0,
     _check_ops(tol, max_iter, restart_m)
     t0 = _sync()
     modified = liouville.build_modified(L, w)
-    mat, rhs, _, fwd, label, _ = _prepare(modified, ordering_name)
+    if d < 0:
+        raise ValueError("drop tolerance d must be >= 0")
+    if not p >= 1:
+        raise ValueError("fill limit p must be >= 1")
+    mat, rhs, _, fwd, label, colf = _prepare(modified, ordering_name)
     t1 = _sync()
-    f = factor.ilutp(mat, d=d, p=p)
+    f = _factor(mat, float(d), float(p), colf)
     t2 = _sync()
     mode = _lib.LIN_GMRES if solver == "gmres" else _lib.LIN_BICGSTAB
     x, st = _solve(mode, mat, None, f, rhs, tol, max_iter, restart_m, True)
@@ -339,8 +367,8 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
         raise ValueError(f"unknown inner solve {inner!r}")
     if not tol > 0:
         raise ValueError("tol must be > 0")
-    if inner == "iterative" and solver not in ("gmres", "bicgstab"):
-        raise ValueError(f"unknown solver {solver!r}")
+    # like the reference (steady.py:210), any solver name other than "gmres"
+    # selects BiCGStab
     _check_ops(None, max_iter, restart_m)
     t0 = _sync()
     # the seeded start vectors (numpy PCG64, drawn exactly as steady.py:171-174)
@@ -351,29 +379,27 @@ def _power_core(L, sigma, tol, inner, ordering_name, solver, d, p, restart_m, ma
     rcm = ordering.rcm_device(L.matrix) if ordering_name == "rcm" else None
     torch.cuda.current_stream(device).wait_stream(side)  # the values have landed
     shifted = liouville.shift(L, sigma)
-    mat, _, plain, fwd, label, x0_map = _prepare(shifted, ordering_name, plain=L.matrix,
-                                                 side=side, rcm=rcm)
+    mat, _, plain, fwd, label, colf = _prepare(shifted, ordering_name, plain=L.matrix,
+                                               side=side, rcm=rcm)
     if plain is None:
         plain = L.matrix
     t1 = _sync()
     if inner == "direct":
-        f = factor.factor_batch(mat, 0.0, float("inf"), raise_on_fail=raise_errors)
+        f = _factor(mat, 0.0, float("inf"), colf, raise_on_fail=raise_errors)
         mode = _lib.INV_DIRECT
     else:
         if d < 0:
             raise ValueError("drop tolerance d must be >= 0")
         if not p >= 1:
             raise ValueError("fill limit p must be >= 1")
-        f = factor.factor_batch(mat, float(d), float(p), raise_on_fail=raise_errors)
+        f = _factor(mat, float(d), float(p), colf, raise_on_fail=raise_errors)
         mode = _lib.INV_GMRES if solver == "gmres" else _lib.INV_BICGSTAB
     t2 = _sync()
     x0, _host = x0_future.result()
     main = torch.cuda.current_stream(device)
     main.wait_stream(side)  # the start vectors and the permuted plain matrix
     x0.record_stream(main)
-    if x0_map is not None:
-        x0 = ordering.permute_vector(x0, x0_map, mat.nsys, mat.n, gather=True)
-    if not f.ok:  # some system of the batch failed to factor
+    if not f.ok and not f.solvable:  # nothing of the batch can be solved
         return None, f, None, None, label, (t0, t1, t2, _sync())
     x, st = _solve(mode, mat, plain, f, x0, tol, max_iter, restart_m, inner == "iterative",
                    threads)
@@ -420,14 +446,18 @@ def inverse_power_batch(L, seeds, sigma=DEFAULT_SIGMA, tol=1e-14, inner="direct"
     results = []
     method = "power-direct" if inner == "direct" else "power-doubly-iterative"
     fills = np.asarray(f.fill_factors, dtype=np.float64).tolist()
-    if out is None:
+    fail = f.fail.tolist()
+    bt, ft = t1 - t0, t2 - t1
+
+    def failed(b, msg):
+        return SteadyStateResult(
+            rho=None, method=method, ordering=label, residual=float("nan"), iterations=0,
+            fill_factor=fills[b], condest=None, build_time=bt, factor_time=ft, solve_time=0.0,
+            converged=False, seed=seeds[b], error=msg)
+
+    if out is None:  # no system could be solved: every entry carries the reason
         for b in range(L.nsys):
-            err = (f"zero pivot at elimination step {int(f.fail[b])}" if f.fail[b] >= 0
-                   else None)
-            results.append(SteadyStateResult(
-                rho=None, method=method, ordering=label, residual=float("nan"), iterations=0,
-                fill_factor=fills[b], condest=None, build_time=t1 - t0,
-                factor_time=t2 - t1, solve_time=0.0, seed=seeds[b], error=err))
+            results.append(failed(b, _factor_error(fail[b])))
         return results
     # per-system fields as Python lists once (structured-array element access
     # per system costs more than the solve of a small system)
@@ -438,8 +468,11 @@ def inverse_power_batch(L, seeds, sigma=DEFAULT_SIGMA, tol=1e-14, inner="direct"
     it = inner == "iterative"
     cond = st["condest"].tolist() if it else None
     inner_tot = st["inner_total"].tolist() if it else None
-    bt, ft, stime = t1 - t0, t2 - t1, t3 - t2
+    stime = t3 - t2
     for b in range(L.nsys):
+        if status[b] == _lib.SOLVE_SKIPPED:  # only this system is lost
+            results.append(failed(b, _factor_error(fail[b])))
+            continue
         err = None if status[b] == _lib.SOLVE_OK else _STATUS_MSG[int(status[b])][1]
         results.append(SteadyStateResult(
             rho=rho[b], method=method, ordering=label, residual=resid[b],
@@ -450,27 +483,49 @@ def inverse_power_batch(L, seeds, sigma=DEFAULT_SIGMA, tol=1e-14, inner="direct"
     return results
 
 
+def _factor_error(step):
+    if step >= 0:
+        return f"zero pivot at elimination step {int(step)}"
+    return "not solved: another system of the batch failed to factor"
+
+
 def solve_batch(L, method="bicgstab", ordering_name="natural", d=1e-4, p=300.0, tol=1e-14,
                 restart_m=20, max_iter=1000, w=None, threads=0):
-    """solve_iterative / solve_direct (method="direct") over a batch."""
+    """solve_iterative / solve_direct (method="direct") over a batch.  A
+    system whose factorization hits a zero pivot is reported on its result's
+    `error` field; the others are solved."""
+    if method not in ("direct", "gmres", "bicgstab"):
+        raise ValueError(f"unknown method {method!r}")
     L = _require_plain(L)
+    _check_ops(tol, max_iter, restart_m)
     t0 = _sync()
     modified = liouville.build_modified(L, w)
-    mat, rhs, _, fwd, label, _ = _prepare(modified, ordering_name)
+    mat, rhs, _, fwd, label, colf = _prepare(modified, ordering_name)
     t1 = _sync()
     if method == "direct":
-        f = factor.factor_batch(mat, 0.0, float("inf"))
+        f = _factor(mat, 0.0, float("inf"), colf, raise_on_fail=False)
         mode = _lib.LIN_DIRECT
     else:
-        f = factor.factor_batch(mat, float(d), float(p))
+        f = _factor(mat, float(d), float(p), colf, raise_on_fail=False)
         mode = _lib.LIN_GMRES if method == "gmres" else _lib.LIN_BICGSTAB
     t2 = _sync()
+    name = "direct" if method == "direct" else f"iterative-{method}"
+    fail = f.fail.tolist()
+
+    def failed(b):
+        return SteadyStateResult(
+            rho=None, method=name, ordering=label, residual=float("nan"), iterations=0,
+            fill_factor=float(f.fill_factors[b]), condest=None, build_time=t1 - t0,
+            factor_time=t2 - t1, solve_time=0.0, converged=False, error=_factor_error(fail[b]))
+
+    if not f.ok and not f.solvable:
+        return [failed(b) for b in range(L.nsys)]
     x, st = _solve(mode, mat, None, f, rhs, tol, max_iter, restart_m, method != "direct",
                    threads)
     rho, res = _postprocess(x, fwd, L)
     t3 = _sync()
-    name = "direct" if method == "direct" else f"iterative-{method}"
-    return [SteadyStateResult(rho=rho[b], method=name, ordering=label, residual=float(res[b]),
+    return [failed(b) if st[b]["status"] == _lib.SOLVE_SKIPPED else
+            SteadyStateResult(rho=rho[b], method=name, ordering=label, residual=float(res[b]),
                               iterations=int(st[b]["inner_last"]),
                               fill_factor=float(f.fill_factors[b]),
                               condest=None if method == "direct" else float(st[b]["condest"]),

@@ -37,7 +37,7 @@ def test_header_symbols_exported():
     for sym in sorted(declared):
         assert hasattr(lib, sym), sym
     assert set(_lib.EXPORTED) == declared
-    assert lib.rs_abi_version() == 1
+    assert lib.rs_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_device():
