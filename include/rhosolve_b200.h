@@ -371,6 +371,79 @@ int rs_postprocess(int32_t nsys, int32_t D, const rs_complex* x,
                    rs_complex* rho, double* residual, rs_complex* trace,
                    void* stream);
 
+/* ---- grid-wide solver for large systems (config 3, config 5) --------------
+ * One cooperative launch runs the whole solve on every SM: SpMV, the
+ * preconditioner apply as sync-free level-ordered triangular sweeps
+ * (bit-identical to lower_solve / upper_solve, _ckernels.pyx:53-85),
+ * deterministic grid-wide reductions and the reference's BiCGStab / GMRES /
+ * inverse-power control flow (krylov.py:67-291, steady.py:177-260). */
+
+/* Dependency levels of a row-oriented triangular factor from rs_factor_rows
+ * (upper = 0: strictly lower L; 1: strictly upper U): level[b*n + i] = 1 +
+ * the largest level among the rows that row i's off-diagonal columns name
+ * (0 when it has none); *nlevels (host) = number of levels. */
+int rs_tri_levels(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
+                  int32_t* level, int64_t* nlevels, void* stream);
+
+/* Rows sorted by (level, row) with every level padded to a multiple of H rows
+ * (H = 32 / lanes-per-row, a power of two <= 32): order[pos] = global row
+ * b*n + i, or -1 for padding.  order must hold nsys*n + H*nlevels entries;
+ * *npos (host) = positions used (a multiple of H). */
+int rs_tri_order(int32_t nsys, int32_t n, const int32_t* level, int64_t nlevels, int32_t H,
+                 int32_t* order, int64_t* npos, void* stream);
+
+/* Level-ordered SELL copy of the factor: slice s = positions H*s..H*s+H-1;
+ * lane r*G + j (G = 32/H) holds entries j, j+G, ... of the slice's r-th row in
+ * the reference fold order (L ascending, U descending column), entry (k, lane)
+ * at sptr[s] + 32k + lane, global column indices, -1 = padding.  Two passes:
+ * sci == NULL fills sptr[npos/H + 1] and *total (host). */
+int rs_tri_sell(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
+                const rs_complex* v, const int32_t* order, int64_t npos, int32_t H,
+                int32_t* sptr, int32_t* sci, rs_complex* sv, int64_t* total, void* stream);
+
+typedef struct rs_tri_factor {
+  const int32_t* order;
+  const int32_t* sptr;
+  const int32_t* sci;
+  const rs_complex* sv;
+  int32_t nslices;       /* npos / H */
+  int32_t lanes_per_row; /* G = 32 / H */
+} rs_tri_factor;
+
+typedef struct rs_grid_args {
+  int32_t n;    /* order of the whole system */
+  int32_t nb;   /* order of one preconditioner block (block-Jacobi: n = blocks * nb;
+                   a single factorization: nb = n) */
+  int32_t mode; /* rs_solve_mode */
+  int32_t want_condest;
+  /* solver-ready ordered system matrix and (inverse power) the plain one: n x n CSR */
+  const int32_t* A_rp;
+  const int32_t* A_ci;
+  const rs_complex* A_v;
+  const int32_t* P_rp;
+  const int32_t* P_ci;
+  const rs_complex* P_v;
+  /* preconditioner (L.order == NULL: none) */
+  rs_tri_factor L;
+  rs_tri_factor U;
+  const rs_complex* rdiag; /* recipc(U_cc), rs_pivot_recip */
+  const int32_t* pinv;     /* row permutation of the factors, local to each block */
+  const int32_t* colp;     /* column pre-ordering, single block only; NULL: identity */
+  const rs_complex* rhs;   /* rhs (linear modes) / un-normalised start vector */
+  rs_complex* x;
+  rs_solve_stats* stats;   /* device, one entry */
+  double tol;
+  int32_t max_iter;
+  int32_t restart_m;
+  int32_t max_outer;
+  int32_t reserved;
+} rs_grid_args;
+
+int rs_grid_solve(const rs_grid_args* args, void* stream);
+/* x = M^{-1} rhs only (factor.solve_lu, factor.py:137-149) through the same
+ * level-ordered sweeps; A / P / stats are ignored. */
+int rs_grid_apply(const rs_grid_args* args, void* stream);
+
 /* ---- grid-wide vector operations (large-system / sharded path) ---------- */
 
 /* out[2k], out[2k+1] = re, im of vdot(xs[k], ys[k]) = sum conj(x) y, k < npairs

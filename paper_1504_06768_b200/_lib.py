@@ -68,6 +68,21 @@ class SolverArgs(ctypes.Structure):
                 ("trace", _vp), ("trace_count", _vp), ("trace_cap", _i32)]
 
 
+class TriFactor(ctypes.Structure):
+    _fields_ = [("order", _vp), ("sptr", _vp), ("sci", _vp), ("sv", _vp), ("nslices", _i32),
+                ("lanes_per_row", _i32)]
+
+
+class GridArgs(ctypes.Structure):
+    _fields_ = [("n", _i32), ("nb", _i32), ("mode", _i32), ("want_condest", _i32),
+                ("A_rp", _vp), ("A_ci", _vp), ("A_v", _vp),
+                ("P_rp", _vp), ("P_ci", _vp), ("P_v", _vp),
+                ("L", TriFactor), ("U", TriFactor), ("rdiag", _vp), ("pinv", _vp),
+                ("colp", _vp), ("rhs", _vp), ("x", _vp), ("stats", _vp), ("tol", _f64),
+                ("max_iter", _i32), ("restart_m", _i32), ("max_outer", _i32),
+                ("reserved", _i32)]
+
+
 # name -> argtypes; every function returns int32 status
 _SIGS = {
     "rs_abi_version": [],
@@ -85,6 +100,12 @@ _SIGS = {
     "rs_lu_solve_cols": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp, _vp],
     "rs_lu_solve": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "rs_tri_levels": [_i32, _i32, _i32, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp],
+    "rs_tri_order": [_i32, _i32, _vp, _i64, _i32, _vp, ctypes.POINTER(_i64), _vp],
+    "rs_tri_sell": [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp,
+                    ctypes.POINTER(_i64), _vp],
+    "rs_grid_solve": [ctypes.POINTER(GridArgs), _vp],
+    "rs_grid_apply": [ctypes.POINTER(GridArgs), _vp],
     "rs_lower_solve": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp],
     "rs_upper_solve": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp],
     "rs_liouvillian": [_i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp,

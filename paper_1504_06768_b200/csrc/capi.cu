@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "solver.cuh"
+#include "grid.cuh"
 
 namespace rs {
 
@@ -123,6 +124,114 @@ int rs_debug_frontal_probe(int enable, double* out4) { return rs::frontal_probe(
 int rs_debug_factor_probe(void* buf) {
   g_factor_probe = reinterpret_cast<unsigned long long*>(buf);
   return 0;
+}
+
+int rs_tri_levels(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
+                  int32_t* level, int64_t* nlevels, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  RS_CHECK_ARG(nlevels != nullptr, "null nlevels");
+  RS_CHECK_ARG(!(nsys && n) || (rp && ci && level), "null pointer");
+  return tri_levels(nsys, n, upper, rp, ci, level, nlevels, S(stream));
+}
+
+int rs_tri_order(int32_t nsys, int32_t n, const int32_t* level, int64_t nlevels, int32_t H,
+                 int32_t* order, int64_t* npos, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0 && nlevels >= 0, "negative size");
+  RS_CHECK_ARG(H >= 1 && H <= 32 && (H & (H - 1)) == 0, "H must be a power of two <= 32");
+  RS_CHECK_ARG(npos != nullptr, "null npos");
+  return tri_order(nsys, n, level, nlevels, H, order, npos, S(stream));
+}
+
+int rs_tri_sell(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
+                const rs_complex* v, const int32_t* order, int64_t npos, int32_t H,
+                int32_t* sptr, int32_t* sci, rs_complex* sv, int64_t* total, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0 && npos >= 0, "negative size");
+  RS_CHECK_ARG(H >= 1 && H <= 32 && (H & (H - 1)) == 0 && npos % H == 0, "bad slice height");
+  return tri_sell(nsys, n, upper, rp, ci, C2(v), order, npos, H, sptr, sci, M2(sv), total,
+                  S(stream));
+}
+
+static int grid_args(const rs_grid_args* p, GridArgs* a) {
+  RS_CHECK_ARG(p != nullptr, "null args");
+  RS_CHECK_ARG(p->n >= 0 && p->nb > 0 && p->n % p->nb == 0, "n must be a multiple of nb");
+  a->n = p->n;
+  a->nb = p->nb;
+  a->mode = p->mode;
+  a->Arp = p->A_rp;
+  a->Aci = p->A_ci;
+  a->Av = C2(p->A_v);
+  a->Prp = p->P_rp;
+  a->Pci = p->P_ci;
+  a->Pv = C2(p->P_v);
+  auto tf = [](const rs_tri_factor& f) {
+    TriSell t;
+    t.order = f.order;
+    t.sptr = f.sptr;
+    t.sci = f.sci;
+    t.sv = C2(f.sv);
+    t.nslices = f.nslices;
+    t.G = f.lanes_per_row;
+    return t;
+  };
+  a->L = tf(p->L);
+  a->U = tf(p->U);
+  a->have_M = p->L.order != nullptr;
+  if (a->have_M) {
+    RS_CHECK_ARG(p->U.order && p->rdiag && p->pinv, "incomplete preconditioner");
+    for (int g : {a->L.G, a->U.G})
+      RS_CHECK_ARG(g >= 1 && g <= 32 && (g & (g - 1)) == 0, "lanes_per_row must be a power of two");
+    RS_CHECK_ARG(!p->colp || p->nb == p->n, "column pre-ordering needs a single block");
+  }
+  a->rd = C2(p->rdiag);
+  a->pinv = p->pinv;
+  a->colp = p->colp;
+  a->rhs = C2(p->rhs);
+  a->xout = M2(p->x);
+  a->stats = reinterpret_cast<SolveStats*>(p->stats);
+  a->tol = p->tol;
+  a->max_iter = p->max_iter;
+  a->restart_m = p->restart_m;
+  a->max_outer = p->max_outer > 0 ? p->max_outer : 50;
+  a->want_condest = p->want_condest;
+  return RS_OK;
+}
+
+int rs_grid_solve(const rs_grid_args* p, void* stream) {
+  RS_TRY(keep_pool_memory());
+  GridArgs a{};
+  RS_TRY(grid_args(p, &a));
+  RS_CHECK_ARG(p->mode >= RS_INV_DIRECT && p->mode <= RS_LIN_GMRES, "unknown mode");
+  RS_CHECK_ARG(p->tol > 0.0 && p->max_iter >= 1 && p->restart_m >= 1, "bad iteration options");
+  RS_CHECK_ARG(p->mode >= RS_LIN_DIRECT || p->P_rp != nullptr,
+               "inverse power needs the plain matrix");
+  if (!a.n) return RS_OK;
+  RS_CHECK_ARG(a.Arp && a.rhs && a.xout && a.stats, "null pointer");
+  cudaStream_t st = S(stream);
+  const int64_t wl = grid_work_len(a.n, a.restart_m);
+  const size_t pbytes = sizeof(double) * 2 * 8 * (size_t)std::max(grid_blocks(), 1);
+  char* buf = nullptr;
+  RS_CUDA_TRY(cudaMallocAsync(&buf, sizeof(double2) * wl + pbytes, st));
+  a.work = reinterpret_cast<double2*>(buf);
+  a.part = reinterpret_cast<double*>(buf + sizeof(double2) * wl);
+  const int rc = launch_grid_solver(a, st);
+  cudaFreeAsync(buf, st);
+  return rc;
+}
+
+int rs_grid_apply(const rs_grid_args* p, void* stream) {
+  RS_TRY(keep_pool_memory());
+  GridArgs a{};
+  RS_TRY(grid_args(p, &a));
+  if (!a.n) return RS_OK;
+  RS_CHECK_ARG(a.have_M && a.rhs && a.xout, "null pointer");
+  cudaStream_t st = S(stream);
+  char* buf = nullptr;
+  RS_CUDA_TRY(cudaMallocAsync(&buf, sizeof(double2) * 3 * (size_t)a.n + 256, st));
+  a.work = reinterpret_cast<double2*>(buf);
+  a.part = reinterpret_cast<double*>(buf + sizeof(double2) * 3 * (size_t)a.n);
+  const int rc = launch_grid_apply(a, st);
+  cudaFreeAsync(buf, st);
+  return rc;
 }
 
 int rs_lower_solve(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li,

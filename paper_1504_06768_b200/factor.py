@@ -46,12 +46,31 @@ class LUFactors:
     __slots__ = ("n", "nsys", "raw", "capL", "capU", "pinv", "L_rp", "L_ci", "L_v", "U_rp",
                  "U_ci", "U_v", "rdiag", "fill_factors", "complete", "drop_tol",
                  "fill_limit", "fail", "lnnz", "unnz", "ok", "csc", "Ls", "Us", "colp",
-                 "colp_dev", "fail_dev", "solvable")
+                 "colp_dev", "fail_dev", "solvable", "Llev", "Ulev")
+
+    def ensure_cols(self):
+        """Column streams of L and U for the one-CTA column sweeps
+        (csrc/colsweep.cuh), built once."""
+        if self.Ls is None and self.solvable:
+            Lp, Li, Lx, Up, Ui, Ux = self.raw
+            dev = self.pinv.device
+            self.Ls = _col_stream(self.nsys, self.n, 0, Lp, Li, Lx, self.capL, None, dev)
+            self.Us = _col_stream(self.nsys, self.n, 1, Up, Ui, Ux, self.capU, self.rdiag, dev)
+        return self
 
     def ensure_rows(self):
         """Build the row-oriented factor copy (row sweeps, exports) once."""
         if self.L_rp is None and self.ok:
             _build_rows(self, self.pinv.device)
+        return self
+
+    def ensure_levels(self):
+        """Level-ordered copies of L and U for the grid-wide sweeps
+        (csrc/levels.cu, csrc/trisell.cuh), built once."""
+        if self.Llev is None and self.ok:
+            self.ensure_rows()
+            self.Llev = _tri_levels(self, False)
+            self.Ulev = _tri_levels(self, True)
         return self
 
     @property
@@ -119,7 +138,7 @@ def _transpose(M):
     return rp, ci, v
 
 
-def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
+def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None, eager=True):
     """factor._factor (factor.py:70-112) for every system of a DeviceCSR."""
     n, B = M.n, M.nsys
     dev = M.values.device
@@ -197,6 +216,7 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
     # larger systems use the row-oriented copy
     f.csc = bool(_lib.load().rs_col_sweep_supported(n))
     f.Ls = f.Us = None
+    f.Llev = f.Ulev = None
     f.colp = f.colp_dev = None
     # a batch with some failed systems can still be solved on the column-sweep
     # path: the solver masks the failed ones (rs_solver_args.skip)
@@ -206,12 +226,18 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None):
         f.rdiag = torch.empty(B * n, dtype=torch.complex128, device=dev)
         _lib.call("rs_pivot_recip", B, n, _lib.ptr(Up), _lib.ptr(Ux), capU,
                   _lib.ptr(f.rdiag), st)
-        if f.csc:
-            f.Ls = _col_stream(B, n, 0, Lp, Li, Lx, capL, None, dev)
-            f.Us = _col_stream(B, n, 1, Up, Ui, Ux, capU, f.rdiag, dev)
-        else:
-            _build_rows(f, dev)
+        # the apply layouts are built on first use: column streams (one CTA
+        # per system), row-oriented CSR, or level-ordered SELL (grid-wide)
+        if eager and f.csc and n < grid_min_n():
+            f.ensure_cols()
     return f
+
+
+def grid_min_n():
+    """Systems of at least this order are solved by the grid-wide kernels
+    (csrc/grid.cu) instead of one CTA per system."""
+    import os
+    return int(os.environ.get("RHOSOLVE_GRID_MIN_N", "8192"))
 
 
 COL_STREAM_WIDTH = 64  # entries per stream row (csrc/colsweep.cuh CW)
@@ -264,6 +290,53 @@ def _build_rows(f, dev):
     f.rdiag = rd
 
 
+class TriLevels:
+    """One triangle in level order (csrc/levels.cu): rows sorted by dependency
+    level, levels padded to whole slices of H = 32/G rows, SELL storage."""
+
+    __slots__ = ("order", "sptr", "sci", "sv", "nslices", "G", "nlevels", "entries")
+
+    def fill(self, t):
+        """Populate an _lib.TriFactor."""
+        t.order, t.sptr = self.order.data_ptr(), self.sptr.data_ptr()
+        t.sci, t.sv = self.sci.data_ptr(), self.sv.data_ptr()
+        t.nslices, t.lanes_per_row = self.nslices, self.G
+
+
+def _tri_levels(f, upper):
+    B, n = f.nsys, f.n
+    N = B * n
+    dev = f.pinv.device
+    rp, ci, v = (f.U_rp, f.U_ci, f.U_v) if upper else (f.L_rp, f.L_ci, f.L_v)
+    st = _lib.stream_ptr()
+    level = torch.empty(N, dtype=torch.int32, device=dev)
+    nlev = ctypes.c_int64(0)
+    _lib.call("rs_tri_levels", B, n, int(upper), _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(level),
+              ctypes.byref(nlev), st)
+    # rows per slice: as many as a level typically holds (power of two <= 32);
+    # the other 32/H lanes of a warp share each row's entries
+    H = 1
+    while H < 32 and 2 * H <= N / max(nlev.value, 1):
+        H *= 2
+    order = torch.empty(N + H * nlev.value, dtype=torch.int32, device=dev)
+    npos = ctypes.c_int64(0)
+    _lib.call("rs_tri_order", B, n, _lib.ptr(level), nlev.value, H, _lib.ptr(order),
+              ctypes.byref(npos), st)
+    nsl = npos.value // H
+    sptr = torch.empty(nsl + 1, dtype=torch.int32, device=dev)
+    total = ctypes.c_int64(0)
+    args = (B, n, int(upper), _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(v), _lib.ptr(order),
+            npos.value, H, _lib.ptr(sptr))
+    _lib.call("rs_tri_sell", *args, None, None, ctypes.byref(total), st)
+    t = TriLevels()
+    t.sci = torch.empty(max(total.value, 1), dtype=torch.int32, device=dev)
+    t.sv = torch.empty(max(total.value, 1), dtype=torch.complex128, device=dev)
+    _lib.call("rs_tri_sell", *args, _lib.ptr(t.sci), _lib.ptr(t.sv), ctypes.byref(total), st)
+    t.order, t.sptr, t.nslices, t.G = order[:npos.value], sptr, nsl, 32 // H
+    t.nlevels, t.entries = nlev.value, total.value
+    return t
+
+
 def _mat(a):
     return a.matrix if hasattr(a, "matrix") else a
 
@@ -310,9 +383,38 @@ def solve_lu_device(f, b):
     return x
 
 
+def _levels_no_colp(f, b):
+    """solve_lu_levels without the final column scatter (the caller applies it)."""
+    keep, f.colp_dev = f.colp_dev, None
+    try:
+        return solve_lu_levels(f, b)
+    finally:
+        f.colp_dev = keep
+
+
+def solve_lu_levels(f, b):
+    """x = M^{-1} b through the grid-wide level-ordered sweeps (the apply of the
+    large-system solver, csrc/grid.cu); bit-identical to the column sweeps."""
+    f.ensure_levels()
+    x = torch.empty_like(b)
+    a = _lib.GridArgs()
+    a.n, a.nb = f.nsys * f.n, f.n
+    f.Llev.fill(a.L)
+    f.Ulev.fill(a.U)
+    a.rdiag, a.pinv = f.rdiag.data_ptr(), f.pinv.data_ptr()
+    if f.colp_dev is not None:
+        a.colp = f.colp_dev.data_ptr()
+    a.rhs, a.x = b.data_ptr(), x.data_ptr()
+    _lib.call("rs_grid_apply", ctypes.byref(a), _lib.stream_ptr())
+    return x
+
+
 def _solve_lu_rows(f, b):
+    if f.n >= grid_min_n() and f.ok:
+        return _levels_no_colp(f, b)
     x = torch.empty_like(b)
     if f.csc:
+        f.ensure_cols()
         (lo, li, lv, lm, _), (uo, ui, uv, um, ur) = f.Ls, f.Us
         _lib.call("rs_lu_solve_cols", f.nsys, f.n, _lib.ptr(f.pinv), _lib.ptr(lo), _lib.ptr(li),
                   _lib.ptr(lv), _lib.ptr(lm), _lib.ptr(uo), _lib.ptr(ui), _lib.ptr(uv),

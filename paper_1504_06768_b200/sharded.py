@@ -370,23 +370,34 @@ def inverse_power_sharded(L, sigma=liouville.DEFAULT_SIGMA, tol=1e-10, d=1e-5, p
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     say(f"block-Jacobi ILUTP {t2 - t1:.2f}s, fill {float(np.sum(M.lnnz + M.unnz)):.3e} entries")
-    x0 = torch.from_numpy(start_vector(n, seed)[r0:r1].copy()).to(S.values.device)
-    x, outer, inner = inverse_power_dist(ops, A, P, M, x0, tol, max_iter, log=say)
-    # gather the (permuted) solution and post-process on every rank
-    if comm.world > 1:
+    if comm.world == 1:
+        # one GPU: the whole doubly-iterative solve is ONE cooperative launch
+        # (csrc/grid.cu); the block-Jacobi factors are block diagonal
+        from . import steady as _st
+        x0 = torch.from_numpy(start_vector(n, seed)).to(S.values.device)
+        xg, stt = _st._solve_grid(_lib.INV_BICGSTAB, S, Pm, M, x0, tol, max_iter, 20, False)
+        s0 = stt[0]
+        if s0["status"] != _lib.SOLVE_OK:
+            exc, msg = _st._STATUS_MSG[int(s0["status"])]
+            raise exc(msg)
+        outer, inner = int(s0["outer"]), [int(s0["inner_total"])]
+    else:
+        x0 = torch.from_numpy(start_vector(n, seed)[r0:r1].copy()).to(S.values.device)
+        x, outer, inner = inverse_power_dist(ops, A, P, M, x0, tol, max_iter, log=say)
+        # gather the (permuted) solution and post-process on every rank
         parts = [torch.empty(shard_range(n, k, comm.world)[1] - shard_range(n, k, comm.world)[0],
                              dtype=x.dtype, device=x.device) for k in range(comm.world)]
         comm.dist.all_gather(parts, x.contiguous(), group=group)
         xg = torch.cat(parts)
-    else:
-        xg = x
     from .steady import _postprocess
     rho, res = _postprocess(xg, fwd, L)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     return SteadyStateResult(
         rho=rho[0], method="power-doubly-iterative", ordering="rcm", residual=float(res[0]),
-        iterations=outer, fill_factor=float(np.sum(M.lnnz + M.unnz) / max(M.nsys, 1)),
+        iterations=outer,
+        # nnz(L+U) / nnz of the factored blocks, as LUFactors.fill_factor (factor.py:53-56)
+        fill_factor=float(np.sum(M.lnnz + M.unnz) / np.sum((M.lnnz + M.unnz) / M.fill_factors)),
         condest=None, build_time=t1 - t0, factor_time=t2 - t1, solve_time=t3 - t2, seed=seed,
         inner_iterations=int(sum(inner)),
         extra={"block": block, "blocks_per_rank": nloc // block, "world": comm.world,

@@ -215,9 +215,45 @@ def _factor(mat, d, p, col_fwd=None, raise_on_fail=True):
     return f
 
 
+_grid_min_n = factor.grid_min_n
+
+
+def _solve_grid(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest):
+    """One cooperative launch over the whole GPU.  f may be a batch of
+    block-Jacobi factors (f.nsys blocks of order f.n tiling the n rows of A)."""
+    import ctypes
+    dev = A.values.device
+    n = A.n
+    x = torch.empty(n, dtype=torch.complex128, device=dev)
+    stats = torch.zeros(_STATS_DT.itemsize, dtype=torch.uint8, device=dev)
+    a = _lib.GridArgs()
+    a.n, a.nb, a.mode = n, n, mode
+    a.A_rp, a.A_ci, a.A_v = A.row_ptr.data_ptr(), A.col_idx.data_ptr(), A.values.data_ptr()
+    if P is not None:
+        a.P_rp, a.P_ci, a.P_v = P.row_ptr.data_ptr(), P.col_idx.data_ptr(), P.values.data_ptr()
+    if f is not None:
+        if f.nsys * f.n != n:
+            raise ValueError("preconditioner blocks do not tile the system")
+        f.ensure_levels()
+        a.nb = f.n
+        f.Llev.fill(a.L)
+        f.Ulev.fill(a.U)
+        a.rdiag, a.pinv = f.rdiag.data_ptr(), f.pinv.data_ptr()
+        if f.colp_dev is not None:
+            a.colp = f.colp_dev.data_ptr()
+    a.rhs, a.x, a.stats = rhs.data_ptr(), x.data_ptr(), stats.data_ptr()
+    a.tol, a.max_iter, a.restart_m = float(tol), int(max_iter), int(restart_m)
+    a.max_outer, a.want_condest = MAX_OUTER, 1 if want_condest else 0
+    _lib.call("rs_grid_solve", ctypes.byref(a), _lib.stream_ptr())
+    st = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=_STATS_DT)
+    return x, st
+
+
 def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0, trace=None):
     dev = A.values.device
     B, n = A.nsys, A.n
+    if B == 1 and n >= _grid_min_n() and trace is None and (f is None or f.ok):
+        return _solve_grid(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest)
     if not threads:
         # one CTA per system: big batches use 4-warp CTAs so four systems stay
         # resident per SM (one wave for the 512-instance sweep); a lone system
@@ -233,6 +269,7 @@ def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0
         a.P_rp, a.P_ci, a.P_v = P.row_ptr.data_ptr(), P.col_idx.data_ptr(), P.values.data_ptr()
     if f is not None:
         if f.csc:  # column streams, reference column sweeps on shared memory
+            f.ensure_cols()
             (lo, li, lv, lm, _), (uo, ui, uv, um, ur) = f.Ls, f.Us
             a.Ls_rowoff, a.Ls_idx, a.Ls_val, a.Ls_meta = (_lib.ptr(lo), _lib.ptr(li),
                                                           _lib.ptr(lv), _lib.ptr(lm))
