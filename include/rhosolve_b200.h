@@ -117,6 +117,25 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
                  int32_t* Ui, rs_complex* Ux, int64_t capU, int32_t* pinv,
                  int32_t* state, void* stream);
 
+/* rs_factorize with two opt-in extensions that the reference does NOT have
+ * (used only by the block-Jacobi preconditioner of config 5; both off is
+ * rs_factorize exactly):
+ *   pivot_floor > 0: a diagonal block of the RCM-ordered matrix can reach a
+ *     column with no usable pivot although the whole matrix factors; such a
+ *     column takes the real value pivot_floor as its pivot, on the lowest
+ *     non-pivotal row of its pattern, or, when the pattern has none, on the
+ *     lowest row not yet pivotal.  state[3b+2] counts the substitutions.
+ *   early_drop != 0: a U entry below the drop threshold (|x| < drop_tol *
+ *     rownorm when its column is reached) is discarded BEFORE it eliminates
+ *     (Saad's ILUT rule); the reference eliminates with it and drops it at
+ *     the end of the column.  Cuts the pre-drop fill cascade of wide bands. */
+int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
+                       const rs_complex* Ax, const int32_t* q, double drop_tol,
+                       int32_t fill_cap, const int32_t* fill_caps, const double* row_norms,
+                       int32_t* Lp, int32_t* Li, rs_complex* Lx, int64_t capL, int32_t* Up,
+                       int32_t* Ui, rs_complex* Ux, int64_t capU, int32_t* pinv,
+                       int32_t* state, double pivot_floor, int32_t early_drop, void* stream);
+
 /* Row-oriented triangular factors for the solves.  From the raw CSC of
  * rs_factorize, builds the strictly-lower L and strictly-upper U in CSR
  * (ascending columns) plus rdiag = recipc(U_kk).  Call with L_ci == NULL to
@@ -407,7 +426,10 @@ typedef struct rs_tri_factor {
   const int32_t* sci;
   const rs_complex* sv;
   int32_t nslices;       /* npos / H */
-  int32_t lanes_per_row; /* G = 32 / H */
+  int32_t lanes_per_row; /* G = 32 / H: 1, 4 or 32 */
+  int32_t active_warps;  /* warps per CTA that sweep (0 = all): the window of slices
+                            in flight; narrow DAGs want few (fewer pollers) */
+  int32_t reserved;
 } rs_tri_factor;
 
 typedef struct rs_grid_args {

@@ -45,6 +45,9 @@ def _lib():
         _c.orc_upper_solve.argtypes = [I, P, P, P, P]
         _c.orc_factorize.argtypes = [I, P, P, P, P, ctypes.c_double, I, P, P]
         _c.orc_factorize.restype = ctypes.c_int
+        _c.orc_factorize_opts.argtypes = [I, P, P, P, P, ctypes.c_double, I, P,
+                                          ctypes.c_double, ctypes.c_int, P, P]
+        _c.orc_factorize_opts.restype = ctypes.c_int
         _c.orc_free_factors.argtypes = [P]
         _c.orc_rcm.argtypes = [I, P, P, P]
         _c.orc_rcm.restype = ctypes.c_int
@@ -238,7 +241,7 @@ class Breakdown(Exception):
 
 
 class Factors:
-    __slots__ = ("n", "Lp", "Li", "Lx", "Up", "Ui", "Ux", "pinv", "fill_factor")
+    __slots__ = ("n", "Lp", "Li", "Lx", "Up", "Ui", "Ux", "pinv", "fill_factor", "nfloor")
 
     def solve(self, b):
         """factor.solve_lu with identity column permutation."""
@@ -250,9 +253,12 @@ class Factors:
         return y
 
 
-def factorize_raw(A, drop_tol, fill_limit, q=None):
+def factorize_raw(A, drop_tol, fill_limit, q=None, pivot_floor=0.0, early_drop=False):
     """factor._factor (factor.py:70-112) -> Factors, or raises Breakdown.
-    q: elimination column order (col_perm.inverse, factor.py:78)."""
+    q: elimination column order (col_perm.inverse, factor.py:78).
+    pivot_floor > 0: the opt-in zero-pivot substitution (not in the reference;
+    see rs_oracle.c orc_factorize_opts); Factors.nfloor counts them.
+    early_drop: the opt-in Saad-ILUT rule (drop before eliminating)."""
     n = A.n
     at = transpose(A)
     incomplete = drop_tol > 0.0 or not math.isinf(fill_limit)
@@ -263,8 +269,10 @@ def factorize_raw(A, drop_tol, fill_limit, q=None):
     cap = -1 if math.isinf(fill_limit) else int(math.ceil(fill_limit * A.nnz / n))
     out = _Factors()
     qa = None if q is None else _i64(q)
-    if _lib().orc_factorize(n, _p(at.rp), _p(at.ci), _p(at.v), _p(qa), float(drop_tol), cap,
-                            _p(rn), ctypes.byref(out)) != 0:
+    nfloor = ctypes.c_int64(0)
+    if _lib().orc_factorize_opts(n, _p(at.rp), _p(at.ci), _p(at.v), _p(qa), float(drop_tol),
+                                 cap, _p(rn), float(pivot_floor), int(bool(early_drop)),
+                                 ctypes.byref(nfloor), ctypes.byref(out)) != 0:
         raise MemoryError
     try:
         if out.fail_col >= 0:
@@ -284,6 +292,7 @@ def factorize_raw(A, drop_tol, fill_limit, q=None):
         f.Ux = arr(out.Ux, out.unnz, np.complex128)
         f.pinv = arr(out.pinv, n, np.int64)
         f.fill_factor = (out.lnnz + out.unnz) / A.nnz
+        f.nfloor = int(nfloor.value)
         return f
     finally:
         _lib().orc_free_factors(ctypes.byref(out))

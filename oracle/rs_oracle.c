@@ -156,10 +156,31 @@ static int grow(int64_t** I, cx** X, int64_t* cap, int64_t need) {
   return 0;
 }
 
+int orc_factorize_opts(int64_t n, const int64_t* Ap, const int64_t* Ai, const cx* Ax,
+                       const int64_t* q, double drop_tol, int64_t fill_cap, const double* rn,
+                       double pivot_floor, int early_drop, int64_t* nfloor, orc_factors* out);
+
 /* Returns 0 and fills *out (caller frees with orc_free_factors); -1 on OOM. */
 int orc_factorize(int64_t n, const int64_t* Ap, const int64_t* Ai, const cx* Ax,
                   const int64_t* q, double drop_tol, int64_t fill_cap, const double* rn,
                   orc_factors* out) {
+  return orc_factorize_opts(n, Ap, Ai, Ax, q, drop_tol, fill_cap, rn, 0.0, 0, 0, out);
+}
+
+/* The reference factorization (_ckernels.pyx:144-385) plus TWO opt-in
+ * extensions the reference does not have (the checker of rs_factorize_opts;
+ * both off = the reference algorithm unchanged):
+ *   pivot_floor > 0: a column without a usable pivot takes the real value
+ *     pivot_floor on the lowest non-pivotal row of its pattern (what the
+ *     reference's tie rule selects among all-zero candidates) or, when the
+ *     pattern has no such row, on the lowest row not yet pivotal;
+ *   early_drop: a U entry that the drop rule is going to discard anyway
+ *     (|x| < drop_tol * rownorm when its column is reached) is discarded at
+ *     once, WITHOUT eliminating with it -- Saad's ILUT rule; the reference
+ *     eliminates first and drops at the end of the column. */
+int orc_factorize_opts(int64_t n, const int64_t* Ap, const int64_t* Ai, const cx* Ax,
+                       const int64_t* q, double drop_tol, int64_t fill_cap, const double* rn,
+                       double pivot_floor, int early_drop, int64_t* nfloor, orc_factors* out) {
   int64_t nnzA = Ap[n];
   int64_t capL = 4 * nnzA > 2 * n ? 4 * nnzA : 2 * n;
   if (capL < 16) capL = 16;
@@ -207,6 +228,7 @@ int orc_factorize(int64_t n, const int64_t* Ap, const int64_t* Ai, const cx* Ax,
     while (hn > 0) {
       const int64_t c = heap_pop(heap, &hn);
       const cx xc = x[prow[c]];
+      if (early_drop && drop_tol > 0.0 && cx_abs1(xc) < drop_tol * rn[prow[c]]) continue;
       ur[nu] = c;
       uv[nu] = xc;
       ++nu;
@@ -235,8 +257,22 @@ int orc_factorize(int64_t n, const int64_t* Ap, const int64_t* Ai, const cx* Ax,
       }
     }
     if (ipiv < 0 || best == 0.0) {
-      out->fail_col = k;
-      break;
+      if (!(pivot_floor > 0.0)) {
+        out->fail_col = k;
+        break;
+      }
+      if (ipiv < 0) {
+        for (int64_t i = 0; i < n; ++i)
+          if (out->pinv[i] < 0) {
+            ipiv = i;
+            break;
+          }
+        mark[ipiv] = k;
+        lr[nl++] = ipiv;
+      }
+      x[ipiv].re = pivot_floor;
+      x[ipiv].im = 0.0;
+      if (nfloor) ++*nfloor;
     }
     const cx piv = x[ipiv];
     int64_t ku = 0, kl = 0;

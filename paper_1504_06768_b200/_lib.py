@@ -70,7 +70,7 @@ class SolverArgs(ctypes.Structure):
 
 class TriFactor(ctypes.Structure):
     _fields_ = [("order", _vp), ("sptr", _vp), ("sci", _vp), ("sv", _vp), ("nslices", _i32),
-                ("lanes_per_row", _i32)]
+                ("lanes_per_row", _i32), ("active_warps", _i32), ("reserved", _i32)]
 
 
 class GridArgs(ctypes.Structure):
@@ -89,6 +89,8 @@ _SIGS = {
     "rs_csr_matvec": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "rs_factorize": [_i32, _i32, _vp, _vp, _vp, _vp, _f64, _i32, _vp, _vp, _vp, _vp, _vp,
                      _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
+    "rs_factorize_opts": [_i32, _i32, _vp, _vp, _vp, _vp, _f64, _i32, _vp, _vp, _vp, _vp, _vp,
+                           _i64, _vp, _vp, _vp, _i64, _vp, _vp, _f64, _i32, _vp],
     "rs_factor_rows": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64,
                        _vp, _vp, _vp, ctypes.POINTER(_i64), _vp, _vp, _vp, _vp,
                        ctypes.POINTER(_i64), _vp],

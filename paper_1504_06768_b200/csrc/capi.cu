@@ -171,6 +171,7 @@ static int grid_args(const rs_grid_args* p, GridArgs* a) {
     t.sv = C2(f.sv);
     t.nslices = f.nslices;
     t.G = f.lanes_per_row;
+    t.apw = f.active_warps;
     return t;
   };
   a->L = tf(p->L);
@@ -179,7 +180,7 @@ static int grid_args(const rs_grid_args* p, GridArgs* a) {
   if (a->have_M) {
     RS_CHECK_ARG(p->U.order && p->rdiag && p->pinv, "incomplete preconditioner");
     for (int g : {a->L.G, a->U.G})
-      RS_CHECK_ARG(g >= 1 && g <= 32 && (g & (g - 1)) == 0, "lanes_per_row must be a power of two");
+      RS_CHECK_ARG(g == 1 || g == 4 || g == 32, "lanes_per_row must be 1, 4 or 32");
     RS_CHECK_ARG(!p->colp || p->nb == p->n, "column pre-ordering needs a single block");
   }
   a->rd = C2(p->rdiag);
@@ -263,7 +264,18 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
                  const int32_t* fill_caps, const double* row_norms, int32_t* Lp, int32_t* Li, rs_complex* Lx,
                  int64_t capL, int32_t* Up, int32_t* Ui, rs_complex* Ux, int64_t capU,
                  int32_t* pinv, int32_t* state, void* stream) {
+  return rs_factorize_opts(nsys, n, Ap, Ai, Ax, q, drop_tol, fill_cap, fill_caps, row_norms, Lp,
+                            Li, Lx, capL, Up, Ui, Ux, capU, pinv, state, 0.0, 0, stream);
+}
+
+int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
+                       const rs_complex* Ax, const int32_t* q, double drop_tol, int32_t fill_cap,
+                       const int32_t* fill_caps, const double* row_norms, int32_t* Lp,
+                       int32_t* Li, rs_complex* Lx, int64_t capL, int32_t* Up, int32_t* Ui,
+                       rs_complex* Ux, int64_t capU, int32_t* pinv, int32_t* state,
+                       double pivot_floor, int32_t early_drop, void* stream) {
   RS_TRY(keep_pool_memory());
+  RS_CHECK_ARG(pivot_floor >= 0.0, "pivot_floor must be >= 0");
   RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
   RS_CHECK_ARG(drop_tol >= 0.0, "drop tolerance must be >= 0");
   RS_CHECK_ARG(!(drop_tol > 0.0) || row_norms, "row_norms required when drop_tol > 0");
@@ -282,6 +294,8 @@ int rs_factorize(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t* Ai,
   a.drop_tol = drop_tol;
   a.fill_cap = fill_cap;
   a.fill_caps = fill_caps;
+  a.pivot_floor = pivot_floor;
+  a.early_drop = early_drop ? 1 : 0;
   a.Lp = Lp;
   a.Li = Li;
   a.Lx = M2(Lx);

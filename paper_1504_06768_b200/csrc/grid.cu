@@ -134,7 +134,7 @@ __device__ __forceinline__ double2 gvdot(Q& q, int n, const double2* a, const do
 // y = A x, bit-exact with csr_matvec (_ckernels.pyx:34-50); the body of
 // spmv_warp_kernel (spmv.cu) for one system, warps striding over 32-row
 // groups.  Barriers: x complete before, y complete after.
-__device__ void g_spmv(Q& q, int n, const int32_t* __restrict__ rp,
+__device__ __noinline__ void g_spmv(Q& q, int n, const int32_t* __restrict__ rp,
                        const int32_t* __restrict__ ci, const double2* __restrict__ v,
                        const double2* x, double2* y) {
   q.g.sync();
@@ -194,7 +194,7 @@ struct Ctx {
 // out = M^{-1} in (factor.solve_lu, factor.py:137-149); out may alias in.
 // Element loops use the grid's fixed element map, so a vector produced by an
 // element loop can be consumed by the next without a barrier.
-__device__ void psolve(Q& q, const Ctx& C, const double2* in, double2* out) {
+__device__ __noinline__ void psolve(Q& q, const Ctx& C, const double2* in, double2* out) {
   const GridArgs& a = *C.a;
   const int n = C.n;
   if (!a.have_M) {
@@ -209,11 +209,9 @@ __device__ void psolve(Q& q, const Ctx& C, const double2* in, double2* out) {
     C.X[i] = S;
   }
   q.g.sync();
-  for (int32_t s = q.gw; s < a.L.nslices; s += q.ngw)
-    tri::sweep_slice_g<false>(a.L, s, C.P, C.Y, nullptr);
+  tri::sweep_grid<false>(a.L, C.P, C.Y, nullptr);
   q.g.sync();
-  for (int32_t s = q.gw; s < a.U.nslices; s += q.ngw)
-    tri::sweep_slice_g<true>(a.U, s, C.Y, C.X, a.rd);
+  tri::sweep_grid<true>(a.U, C.Y, C.X, a.rd);
   q.g.sync();
   if (a.colp) {  // x[q] = y (factor.py:147-148)
     for (int i = q.tid; i < n; i += q.nth) out[i] = __ldcg(C.X + a.colp[i]);
@@ -255,7 +253,7 @@ struct Vecs {
 #define EACH(i) for (int i = q.tid; i < n; i += q.nth)
 
 // krylov.bicgstab, krylov.py:181-291
-__device__ IterOut bicgstab(Q& q, const Ctx& C, const double2* b, const Vecs& W, double tol,
+__device__ __noinline__ IterOut bicgstab(Q& q, const Ctx& C, const double2* b, const Vecs& W, double tol,
                             int max_iter) {
   const int n = C.n;
   IterOut out{0, 0.0, false, false};
@@ -389,7 +387,7 @@ __device__ IterOut bicgstab(Q& q, const Ctx& C, const double2* b, const Vecs& W,
 
 // krylov.gmres, krylov.py:67-178.  H is (m+1) x m row-major in shared memory
 // (every CTA keeps its own, identical copy), then g (m+1), sn (m), y (m).
-__device__ IterOut gmres(Q& q, const Ctx& C, const double2* b, const Vecs& W, double tol,
+__device__ __noinline__ IterOut gmres(Q& q, const Ctx& C, const double2* b, const Vecs& W, double tol,
                          int max_iter, int m) {
   const int n = C.n;
   IterOut out{0, 0.0, false, false};
@@ -760,6 +758,16 @@ int launch_grid_apply(const GridArgs& a, cudaStream_t st) {
   count_launch();
   return RS_OK;
 }
+
+}  // namespace rs
+
+extern "C" int rs_debug_slice_times(void* buf) {
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+  RS_CUDA_TRY(cudaMemcpyToSymbol(rs::tri::g_slice_times, &p, sizeof(p)));
+  return 0;
+}
+
+namespace rs {
 
 int grid_blocks() {
   int dev = 0, sms = 0;

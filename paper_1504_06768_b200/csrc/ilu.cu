@@ -313,6 +313,13 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
       // here instead of on the column's critical tail
       const bool ukk = !(drop > 0.0 && cabs1(xc) < drop * rnc);
       __syncwarp();
+      if (INC && a.early_drop && !ukk) {
+        // opt-in Saad-ILUT rule (not the reference's): an entry the drop rule
+        // discards is discarded before it eliminates anything
+        if (lane == 0) atomicAnd(&bits[w], ~(1u << (c & 31)));
+        __syncwarp();
+        continue;
+      }
       if (lane == 0) {
         atomicAnd(&bits[w], ~(1u << (c & 31)));
         urow[unum] = c;
@@ -425,12 +432,46 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
       }
     }
     if (gipiv < 0 || gbest == 0.0) {
-      if (lane == 0) {
-        state[0] = FAC_ZERO_PIVOT;
-        state[1] = k;
-        ctl[1] = 1;
+      if (!(a.pivot_floor > 0.0)) {
+        if (lane == 0) {
+          state[0] = FAC_ZERO_PIVOT;
+          state[1] = k;
+          ctl[1] = 1;
+        }
+        break;
       }
-      break;
+      // Opt-in remedy (not in the reference; the block-Jacobi preconditioner
+      // of config 5 asks for it): a column with no usable pivot takes the
+      // value pivot_floor on the row the reference's tie rule names (the
+      // lowest non-pivotal pattern row), or -- when every pattern row is
+      // already pivotal -- on the lowest row not yet pivotal, which joins
+      // the pattern.  Every column < k is final here, so pinv is exact.
+      if (gipiv < 0) {
+        int r = 0x7fffffff;
+        for (int base = 0; base < n && r == 0x7fffffff; base += 32) {
+          const int i = base + lane;
+          const bool open = i < n && vload(pinv + i) < 0;
+          const unsigned m = __ballot_sync(FULL, open);
+          if (m) r = base + __ffs(m) - 1;
+        }
+        gipiv = r;
+        ipiv = -1;
+        ipos = -1;
+        if (lane == 0) {
+          lrow[lnum] = r;
+          if (INC) lkeep[lnum] = 0;
+          flag[r] = k;
+          ipiv = r;
+          ipos = lnum;
+          ikeep = 0;
+        }
+        lnum += 1;
+      }
+      if (lane == 0) {
+        x[gipiv] = make_double2(a.pivot_floor, 0.0);
+        atomicAdd(&state[2], 1);  // substituted pivots of this system
+      }
+      __syncwarp();
     }
     // the pivot row is never an L entry: the owning lane clears its keep
     const bool owner = (ipiv == gipiv) && ipos >= 0;

@@ -38,6 +38,8 @@ struct FactorArgs {
   double drop_tol;
   int32_t fill_cap;   // -1: no cap
   const int32_t* fill_caps;  // optional per-system caps (overrides fill_cap)
+  double pivot_floor;  // > 0: substitute this value for a missing / zero pivot (opt-in)
+  int early_drop;      // 1: drop a U entry before eliminating with it (opt-in, Saad ILUT)
   // outputs per system b; pointers are relative to b*cap
   int32_t* Lp;  // [B*(n+1)]
   int32_t* Li;
@@ -49,7 +51,7 @@ struct FactorArgs {
   int64_t capU;
   int32_t* pinv;  // [B*n]
   int32_t* prow;  // [B*n]
-  int32_t* state;  // [B*3]: status, fail/next col, unused
+  int32_t* state;  // [B*3]: status, fail/next col, substituted pivots
   // per-warp private scratch: (B*warps) slices of n
   double2* wx;
   int32_t* wflag;

@@ -28,51 +28,138 @@ struct TriSell {
   const int32_t* sci;    // global column per entry, -1 = padding
   const double2* sv;
   int32_t nslices;
-  int32_t G;  // lanes per row (1, 2, 4, 8, 16, 32); H = 32 / G rows per slice
+  int32_t G;  // lanes per row (1, 4 or 32); H = 32 / G rows per slice
+  // Warps per CTA that take part in the sweep (0 = all).  Every waiting lane
+  // polls a value near the sweep's frontier, so a narrow DAG (config 3: ~3
+  // rows per level) swept by every resident warp turns the frontier's L2
+  // sectors into a hot spot (measured: 41 us per level with 2,368 warps);
+  // the window of slices in flight only needs to cover the pre-fold latency.
+  int32_t apw;
 };
 
 namespace tri {
 
-// One slice.  rhs: right-hand side (final values, plain loads); out: solution
-// vector (sentinel-initialised, published per row); rd: recipc(U_cc) (UPPER).
-template <bool UPPER, int G>
-__device__ __forceinline__ void sweep_slice(const TriSell& T, int32_t s, const double2* rhs,
-                                            double2* out, const double2* rd) {
+// tuning hook: per-slice (start, first step done, end) global-timer stamps [3 * nslices]
+__device__ unsigned long long* g_slice_times = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Ordered fold of one step's products into the row accumulators: the G lanes
+// of a row subtract their products in lane order (= storage order).
+template <int G>
+__device__ __forceinline__ void fold_step(double2& acc, double2 p, int r) {
   constexpr unsigned FULL = 0xffffffffu;
+  if (G == 1) {
+    acc = csub(acc, p);
+  } else {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const double px = __shfl_sync(FULL, p.x, r * G + j);
+      const double py = __shfl_sync(FULL, p.y, r * G + j);
+      acc = csub(acc, make_double2(px, py));
+    }
+  }
+}
+
+// One slice.  rhs: right-hand side (final values); out: solution vector
+// (sentinel-initialised, published per row); rd: recipc(U_cc) (UPPER).
+//
+// Waiting is decoupled from folding.  A slice of up to KREG steps (the sparse
+// factors of config 5) keeps all its entries in registers: every source value
+// is requested at once, the not-yet-published ones are re-polled together,
+// and the fold runs from registers -- so a dependency hop costs one L2 round
+// trip, not one per step.  Wider slices first wait for every source (loads
+// four steps deep), then stream the fold with plain pipelined loads.
+constexpr int KREG = 8;
+
+template <bool UPPER, int G>
+__device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const double2* rhs,
+                                         double2* out, const double2* rd) {
   constexpr int H = 32 / G;
   const int lane = threadIdx.x & 31;
   const int r = lane / G;
   const int32_t row = __ldg(T.order + (int64_t)s * H + r);
   const int32_t base = __ldg(T.sptr + s);
   const int32_t w = (__ldg(T.sptr + s + 1) - base) >> 5;
+  unsigned long long* const tt = (!UPPER && lane == 0) ? g_slice_times : nullptr;
+  if (tt) tt[3 * (int64_t)s] = gtime();
   double2 acc = row >= 0 ? __ldcg(rhs + row) : make_double2(0.0, 0.0);
-  int32_t c_n = -1;
-  double2 a_n = make_double2(0.0, 0.0);
-  if (w > 0) {
-    c_n = __ldg(T.sci + base + lane);
-    a_n = ldg2(T.sv + base + lane);
-  }
-  for (int32_t k = 0; k < w; ++k) {
-    const int32_t c = c_n;
-    const double2 a = a_n;
-    if (k + 1 < w) {  // next step's entry is in flight while this one waits
-      c_n = __ldg(T.sci + base + 32 * (k + 1) + lane);
-      a_n = ldg2(T.sv + base + 32 * (k + 1) + lane);
-    }
-    double2 p = make_double2(0.0, 0.0);
-    if (c >= 0) {
-      double2 yv = cta::vld2(out + c);
-      while (!cta::is_ready(yv)) yv = cta::vld2(out + c);
-      p = cmul_plain(a, yv);
-    }
-    if (G == 1) {
-      acc = csub(acc, p);
-    } else {
+  const int32_t* ci = T.sci + base + lane;
+  const double2* av = T.sv + base + lane;
+  if (w <= KREG) {
+    int32_t c[KREG];
+    double2 a[KREG], y[KREG];
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const double px = __shfl_sync(FULL, p.x, r * G + j);
-        const double py = __shfl_sync(FULL, p.y, r * G + j);
-        acc = csub(acc, make_double2(px, py));
+    for (int k = 0; k < KREG; ++k) {
+      c[k] = -1;
+      if (k < w) {
+        c[k] = __ldg(ci + 32 * k);
+        a[k] = ldg2(av + 32 * k);
+      }
+    }
+    unsigned pend = 0;
+#pragma unroll
+    for (int k = 0; k < KREG; ++k)
+      if (c[k] >= 0) y[k] = cta::vld2(out + c[k]);
+#pragma unroll
+    for (int k = 0; k < KREG; ++k)
+      if (c[k] >= 0 && !cta::is_ready(y[k])) pend |= 1u << k;
+    while (pend) {
+#pragma unroll
+      for (int k = 0; k < KREG; ++k)
+        if ((pend >> k) & 1u) y[k] = cta::vld2(out + c[k]);
+#pragma unroll
+      for (int k = 0; k < KREG; ++k)
+        if (((pend >> k) & 1u) && cta::is_ready(y[k])) pend &= ~(1u << k);
+    }
+    if (tt) tt[3 * (int64_t)s + 1] = gtime();
+#pragma unroll
+    for (int k = 0; k < KREG; ++k) {
+      if (k < w) {  // warp-uniform
+        const double2 p = c[k] >= 0 ? cmul_plain(a[k], y[k]) : make_double2(0.0, 0.0);
+        fold_step<G>(acc, p, r);
+      }
+    }
+  } else {
+    // phase A: every source of this lane is published (four steps in flight)
+    for (int32_t k0 = 0; k0 < w; k0 += 4) {
+      int32_t c[4];
+      double2 y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = (k0 + u < w) ? __ldg(ci + 32 * (k0 + u)) : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c[u] >= 0) y[u] = cta::vld2(out + c[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c[u] >= 0)
+          while (!cta::is_ready(y[u])) y[u] = cta::vld2(out + c[u]);
+    }
+    if (tt) tt[3 * (int64_t)s + 1] = gtime();
+    // phase B: ordered fold, plain loads (published values never change)
+    for (int32_t k0 = 0; k0 < w; k0 += 4) {
+      int32_t c[4];
+      double2 a[4], y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] = -1;
+        if (k0 + u < w) {
+          c[u] = __ldg(ci + 32 * (k0 + u));
+          a[u] = ldg2(av + 32 * (k0 + u));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c[u] >= 0) y[u] = __ldcg(out + c[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k0 + u < w) {
+          const double2 p = c[u] >= 0 ? cmul_plain(a[u], y[u]) : make_double2(0.0, 0.0);
+          fold_step<G>(acc, p, r);
+        }
       }
     }
   }
@@ -80,19 +167,32 @@ __device__ __forceinline__ void sweep_slice(const TriSell& T, int32_t s, const d
     if (UPPER) acc = cmul_plain(acc, rd[row]);
     cta::vst2(out + row, acc);
   }
+  if (tt) tt[3 * (int64_t)s + 2] = gtime();
 }
 
 template <bool UPPER>
 __device__ __forceinline__ void sweep_slice_g(const TriSell& T, int32_t s, const double2* rhs,
                                               double2* out, const double2* rd) {
-  switch (T.G) {
+  switch (T.G) {  // the layouts levels.cu is asked for: 32, 8 or 1 rows per slice
     case 1: sweep_slice<UPPER, 1>(T, s, rhs, out, rd); break;
-    case 2: sweep_slice<UPPER, 2>(T, s, rhs, out, rd); break;
     case 4: sweep_slice<UPPER, 4>(T, s, rhs, out, rd); break;
-    case 8: sweep_slice<UPPER, 8>(T, s, rhs, out, rd); break;
-    case 16: sweep_slice<UPPER, 16>(T, s, rhs, out, rd); break;
     default: sweep_slice<UPPER, 32>(T, s, rhs, out, rd); break;
   }
+}
+
+// The whole sweep from inside a grid-wide kernel: the first apw warps of
+// every CTA take slices in ascending order, consecutive slices going to
+// different CTAs.  All participants are co-resident, so waits cannot deadlock.
+template <bool UPPER>
+__device__ __noinline__ void sweep_grid(const TriSell& T, const double2* rhs, double2* out,
+                                           const double2* rd) {
+  const int wpc = blockDim.x >> 5;
+  const int apw = (T.apw > 0 && T.apw < wpc) ? T.apw : wpc;
+  const int lw = threadIdx.x >> 5;
+  if (lw >= apw) return;
+  const int32_t stride = apw * (int32_t)gridDim.x;
+  for (int32_t s = lw * (int32_t)gridDim.x + blockIdx.x; s < T.nslices; s += stride)
+    sweep_slice_g<UPPER>(T, s, rhs, out, rd);
 }
 
 }  // namespace tri

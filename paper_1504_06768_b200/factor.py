@@ -46,7 +46,7 @@ class LUFactors:
     __slots__ = ("n", "nsys", "raw", "capL", "capU", "pinv", "L_rp", "L_ci", "L_v", "U_rp",
                  "U_ci", "U_v", "rdiag", "fill_factors", "complete", "drop_tol",
                  "fill_limit", "fail", "lnnz", "unnz", "ok", "csc", "Ls", "Us", "colp",
-                 "colp_dev", "fail_dev", "solvable", "Llev", "Ulev")
+                 "colp_dev", "fail_dev", "solvable", "Llev", "Ulev", "nfloor")
 
     def ensure_cols(self):
         """Column streams of L and U for the one-CTA column sweeps
@@ -138,8 +138,13 @@ def _transpose(M):
     return rp, ci, v
 
 
-def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None, eager=True):
-    """factor._factor (factor.py:70-112) for every system of a DeviceCSR."""
+def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None, eager=True,
+                 pivot_floor=0.0, early_drop=False):
+    """factor._factor (factor.py:70-112) for every system of a DeviceCSR.
+    pivot_floor > 0 switches on the zero-pivot substitution of
+    rs_factorize_opts (NOT reference behaviour; block-Jacobi blocks only);
+    LUFactors.nfloor then counts the substituted pivots per system; early_drop
+    is the Saad-ILUT rule (drop a U entry before eliminating with it)."""
     n, B = M.n, M.nsys
     dev = M.values.device
     if n == 0 or M.nnz == 0:
@@ -178,10 +183,11 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None, eag
     state = torch.zeros(3 * B, dtype=torch.int32, device=dev)
     st = _lib.stream_ptr()
     while True:
-        _lib.call("rs_factorize", B, n, _lib.ptr(Ap), _lib.ptr(Ai), _lib.ptr(Ax), None,
-                  float(drop_tol), cap, _lib.ptr(caps_t), _lib.ptr(rn), _lib.ptr(Lp), _lib.ptr(Li), _lib.ptr(Lx),
-                  capL, _lib.ptr(Up), _lib.ptr(Ui), _lib.ptr(Ux), capU, _lib.ptr(pinv),
-                  _lib.ptr(state), st)
+        _lib.call("rs_factorize_opts", B, n, _lib.ptr(Ap), _lib.ptr(Ai), _lib.ptr(Ax), None,
+                  float(drop_tol), cap, _lib.ptr(caps_t), _lib.ptr(rn), _lib.ptr(Lp),
+                  _lib.ptr(Li), _lib.ptr(Lx), capL, _lib.ptr(Up), _lib.ptr(Ui), _lib.ptr(Ux),
+                  capU, _lib.ptr(pinv), _lib.ptr(state), float(pivot_floor),
+                  1 if early_drop else 0, st)
         sh = state.reshape(B, 3).cpu().numpy()
         if not np.any(sh[:, 0] == 3):
             break
@@ -208,6 +214,7 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None, eag
     f.drop_tol = float(drop_tol) if incomplete else None
     f.fill_limit = float(fill_limit) if incomplete else None
     f.fail = fail
+    f.nfloor = sh[:, 2].copy()
     f.ok = bool(np.all(fail < 0))
     f.L_rp = f.L_ci = f.L_v = f.U_rp = f.U_ci = f.U_v = None
     f.rdiag = None
@@ -294,13 +301,14 @@ class TriLevels:
     """One triangle in level order (csrc/levels.cu): rows sorted by dependency
     level, levels padded to whole slices of H = 32/G rows, SELL storage."""
 
-    __slots__ = ("order", "sptr", "sci", "sv", "nslices", "G", "nlevels", "entries")
+    __slots__ = ("order", "sptr", "sci", "sv", "nslices", "G", "nlevels", "entries", "apw")
 
     def fill(self, t):
         """Populate an _lib.TriFactor."""
         t.order, t.sptr = self.order.data_ptr(), self.sptr.data_ptr()
         t.sci, t.sv = self.sci.data_ptr(), self.sv.data_ptr()
         t.nslices, t.lanes_per_row = self.nslices, self.G
+        t.active_warps = self.apw
 
 
 def _tri_levels(f, upper):
@@ -315,9 +323,8 @@ def _tri_levels(f, upper):
               ctypes.byref(nlev), st)
     # rows per slice: as many as a level typically holds (power of two <= 32);
     # the other 32/H lanes of a warp share each row's entries
-    H = 1
-    while H < 32 and 2 * H <= N / max(nlev.value, 1):
-        H *= 2
+    per_level = N / max(nlev.value, 1)
+    H = 32 if per_level >= 24 else (8 if per_level >= 6 else 1)
     order = torch.empty(N + H * nlev.value, dtype=torch.int32, device=dev)
     npos = ctypes.c_int64(0)
     _lib.call("rs_tri_order", B, n, _lib.ptr(level), nlev.value, H, _lib.ptr(order),
@@ -334,6 +341,15 @@ def _tri_levels(f, upper):
     _lib.call("rs_tri_sell", *args, _lib.ptr(t.sci), _lib.ptr(t.sv), ctypes.byref(total), st)
     t.order, t.sptr, t.nslices, t.G = order[:npos.value], sptr, nsl, 32 // H
     t.nlevels, t.entries = nlev.value, total.value
+    # sweep window: enough slices in flight to cover ~16 levels of look-ahead,
+    # spread over the SMs (16 warps per CTA at most; 0 = all)
+    import os
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    want = 16.0 * nsl / max(nlev.value, 1)
+    t.apw = int(min(16, max(1, round(want / sms))))
+    env = os.environ.get("RHOSOLVE_TRI_APW")
+    if env:
+        t.apw = int(env)
     return t
 
 

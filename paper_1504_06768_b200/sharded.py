@@ -305,7 +305,7 @@ def inverse_power_dist(ops, A, P, M, x0, tol, max_iter, max_outer=MAX_OUTER, log
     raise PowerIterationError(f"no convergence within {max_outer} outer iterations")
 
 
-def _block_jacobi(A_local_rows, r0, nloc, block, d, p):
+def _block_jacobi(A_local_rows, r0, nloc, block, d, p, pivot_floor=0.0, early_drop=False):
     """Diagonal blocks of this rank's rows -> batched ILUTP factors."""
     import ctypes
     dev = A_local_rows[0].device
@@ -320,7 +320,8 @@ def _block_jacobi(A_local_rows, r0, nloc, block, d, p):
     _lib.call("rs_block_extract", nloc, block, r0, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(v),
               _lib.ptr(orp), _lib.ptr(oci), _lib.ptr(ov), ctypes.byref(nnz), st)
     B = DeviceCSR(block, nloc // block, orp, oci[:nnz.value], ov[:nnz.value])
-    return factor.factor_batch(B, d, p, raise_on_fail=True)
+    return factor.factor_batch(B, d, p, raise_on_fail=True, pivot_floor=pivot_floor,
+                               early_drop=early_drop)
 
 
 def pick_block(nloc, target=5000):
@@ -335,7 +336,8 @@ def pick_block(nloc, target=5000):
 
 
 def inverse_power_sharded(L, sigma=liouville.DEFAULT_SIGMA, tol=1e-10, d=1e-5, p=10.0,
-                          max_iter=1000, seed=3, blocks=8, group=None, log=None):
+                          max_iter=1000, seed=3, blocks=8, group=None, log=None,
+                          pivot_floor=0.0, early_drop=False):
     """Doubly-iterative inverse power (inner BiCGStab, block-Jacobi ILUTP under
     RCM) with the rows sharded over the ranks of `group` (one GPU each).
     `blocks` = total block-Jacobi blocks (a multiple of the world size), so
@@ -366,7 +368,7 @@ def inverse_power_sharded(L, sigma=liouville.DEFAULT_SIGMA, tol=1e-10, d=1e-5, p
     block = n // blocks
     rp = S.row_ptr[r0:r1 + 1]
     say(f"permute + shard {t1 - t0:.2f}s total; factoring {nloc // block} blocks of {block}")
-    M = _block_jacobi((rp, S.col_idx, S.values), r0, nloc, block, d, p)
+    M = _block_jacobi((rp, S.col_idx, S.values), r0, nloc, block, d, p, pivot_floor, early_drop)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     say(f"block-Jacobi ILUTP {t2 - t1:.2f}s, fill {float(np.sum(M.lnnz + M.unnz)):.3e} entries")

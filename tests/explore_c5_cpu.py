@@ -36,8 +36,8 @@ def levels_csc(n, cp, ci, lower):
     return int(lev.max()) + 1
 
 
-def main(N=12, blocks=8, d=1e-3, p=2.0, max_iter=1000, floor=0):
-    N, blocks, max_iter, floor = int(N), int(blocks), int(max_iter), int(floor)
+def main(N=12, blocks=8, d=1e-3, p=2.0, max_iter=1000, floor=0, early=0):
+    N, blocks, max_iter, floor = int(N), int(blocks), int(max_iter), float(floor)
     d, p = float(d), float(p)
     t = time.perf_counter()
     H, c = configs.kerr_kerr(N=N)
@@ -62,7 +62,9 @@ def main(N=12, blocks=8, d=1e-3, p=2.0, max_iter=1000, floor=0):
         Bc = O.CSR(r1 - r0, r1 - r0, Bk.indptr.astype(np.int64), Bk.indices.astype(np.int64),
                    Bk.data.astype(np.complex128))
         try:
-            f = O.factorize_raw(Bc, d, p) if not floor else O.factorize_raw(Bc, d, p, floor=True)
+            f = O.factorize_raw(Bc, d, p, pivot_floor=float(floor), early_drop=int(early))
+            if f.nfloor:
+                print(f"  block {b}: {f.nfloor} substituted pivots", flush=True)
         except O.Breakdown as e:
             print(f"block {b}: {e}")
             return
