@@ -397,36 +397,44 @@ int rs_postprocess(int32_t nsys, int32_t D, const rs_complex* x,
  * deterministic grid-wide reductions and the reference's BiCGStab / GMRES /
  * inverse-power control flow (krylov.py:67-291, steady.py:177-260). */
 
-/* Dependency levels of a row-oriented triangular factor from rs_factor_rows
- * (upper = 0: strictly lower L; 1: strictly upper U): level[b*n + i] = 1 +
- * the largest level among the rows that row i's off-diagonal columns name
- * (0 when it has none); *nlevels (host) = number of levels. */
-int rs_tri_levels(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
-                  int32_t* level, int64_t* nlevels, void* stream);
+/* Dependency levels of a triangular factor (upper = 0: L, 1: U): level[b*n +
+ * i] = 1 + the largest level among the rows that row i's off-diagonal columns
+ * name (0 when it has none); *nlevels (host) = number of levels.  rp = row
+ * pointers of the row-oriented factor (rs_factor_rows: the dependency counts);
+ * cp / ri / cap = column pointers, row indices and per-system stride of the
+ * raw CSC factor of rs_factorize (column c lists the rows depending on c). */
+int rs_tri_levels(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* cp,
+                  const int32_t* ri, int64_t cap, int32_t* level, int64_t* nlevels,
+                  void* stream);
 
-/* Rows sorted by (level, row) with every level padded to a multiple of H rows
- * (H = 32 / lanes-per-row, a power of two <= 32): order[pos] = global row
- * b*n + i, or -1 for padding.  order must hold nsys*n + H*nlevels entries;
- * *npos (host) = positions used (a multiple of H). */
-int rs_tri_order(int32_t nsys, int32_t n, const int32_t* level, int64_t nlevels, int32_t H,
-                 int32_t* order, int64_t* npos, void* stream);
+/* Rows sorted by (level, longest row first, row) with every level padded to a
+ * multiple of H rows (H = 32 / lanes-per-row: 32, 16, 8 or 1): order[pos] = global
+ * row b*n + i, or -1 for padding.  rp = the row-oriented factor's row
+ * pointers.  order must hold nsys*n + H*nlevels entries; *npos (host) =
+ * positions used (a multiple of H). */
+int rs_tri_order(int32_t nsys, int32_t n, const int32_t* level, const int32_t* rp,
+                 int64_t nlevels, int32_t H, int32_t* order, int64_t* npos, void* stream);
 
 /* Level-ordered SELL copy of the factor: slice s = positions H*s..H*s+H-1;
  * lane r*G + j (G = 32/H) holds entries j, j+G, ... of the slice's r-th row in
  * the reference fold order (L ascending, U descending column), entry (k, lane)
- * at sptr[s] + 32k + lane, global column indices, -1 = padding.  Two passes:
- * sci == NULL fills sptr[npos/H + 1] and *total (host). */
+ * at sptr[s] + 32k + lane, global column indices, -1 = padding; skey[s] = the
+ * slice's dependency of the highest level (the one its warp watches), -1 when
+ * it has none.  Two passes: sci == NULL fills sptr[npos/H + 1] and *total
+ * (host); the second fills sci / sv / skey[npos/H]. */
 int rs_tri_sell(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
                 const rs_complex* v, const int32_t* order, int64_t npos, int32_t H,
-                int32_t* sptr, int32_t* sci, rs_complex* sv, int64_t* total, void* stream);
+                const int32_t* level, int32_t* sptr, int32_t* sci, rs_complex* sv,
+                int32_t* skey, int64_t* total, void* stream);
 
 typedef struct rs_tri_factor {
   const int32_t* order;
   const int32_t* sptr;
   const int32_t* sci;
   const rs_complex* sv;
+  const int32_t* skey;
   int32_t nslices;       /* npos / H */
-  int32_t lanes_per_row; /* G = 32 / H: 1, 4 or 32 */
+  int32_t lanes_per_row; /* G = 32 / H: 1, 2, 4 or 32 */
   int32_t active_warps;  /* warps per CTA that sweep (0 = all): the window of slices
                             in flight; narrow DAGs want few (fewer pollers) */
   int32_t reserved;

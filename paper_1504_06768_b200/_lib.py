@@ -69,7 +69,8 @@ class SolverArgs(ctypes.Structure):
 
 
 class TriFactor(ctypes.Structure):
-    _fields_ = [("order", _vp), ("sptr", _vp), ("sci", _vp), ("sv", _vp), ("nslices", _i32),
+    _fields_ = [("order", _vp), ("sptr", _vp), ("sci", _vp), ("sv", _vp), ("skey", _vp),
+                ("nslices", _i32),
                 ("lanes_per_row", _i32), ("active_warps", _i32), ("reserved", _i32)]
 
 
@@ -102,9 +103,9 @@ _SIGS = {
     "rs_lu_solve_cols": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp, _vp],
     "rs_lu_solve": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
-    "rs_tri_levels": [_i32, _i32, _i32, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp],
-    "rs_tri_order": [_i32, _i32, _vp, _i64, _i32, _vp, ctypes.POINTER(_i64), _vp],
-    "rs_tri_sell": [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp,
+    "rs_tri_levels": [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_i64), _vp],
+    "rs_tri_order": [_i32, _i32, _vp, _vp, _i64, _i32, _vp, ctypes.POINTER(_i64), _vp],
+    "rs_tri_sell": [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp,
                     ctypes.POINTER(_i64), _vp],
     "rs_grid_solve": [ctypes.POINTER(GridArgs), _vp],
     "rs_grid_apply": [ctypes.POINTER(GridArgs), _vp],

@@ -126,29 +126,31 @@ int rs_debug_factor_probe(void* buf) {
   return 0;
 }
 
-int rs_tri_levels(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
-                  int32_t* level, int64_t* nlevels, void* stream) {
-  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+int rs_tri_levels(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* cp,
+                  const int32_t* ri, int64_t cap, int32_t* level, int64_t* nlevels,
+                  void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0 && cap >= 0, "negative size");
   RS_CHECK_ARG(nlevels != nullptr, "null nlevels");
-  RS_CHECK_ARG(!(nsys && n) || (rp && ci && level), "null pointer");
-  return tri_levels(nsys, n, upper, rp, ci, level, nlevels, S(stream));
+  RS_CHECK_ARG(!(nsys && n) || (rp && cp && ri && level), "null pointer");
+  return tri_levels(nsys, n, upper, rp, cp, ri, cap, level, nlevels, S(stream));
 }
 
-int rs_tri_order(int32_t nsys, int32_t n, const int32_t* level, int64_t nlevels, int32_t H,
-                 int32_t* order, int64_t* npos, void* stream) {
+int rs_tri_order(int32_t nsys, int32_t n, const int32_t* level, const int32_t* rp,
+                 int64_t nlevels, int32_t H, int32_t* order, int64_t* npos, void* stream) {
   RS_CHECK_ARG(nsys >= 0 && n >= 0 && nlevels >= 0, "negative size");
   RS_CHECK_ARG(H >= 1 && H <= 32 && (H & (H - 1)) == 0, "H must be a power of two <= 32");
   RS_CHECK_ARG(npos != nullptr, "null npos");
-  return tri_order(nsys, n, level, nlevels, H, order, npos, S(stream));
+  return tri_order(nsys, n, level, rp, nlevels, H, order, npos, S(stream));
 }
 
 int rs_tri_sell(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
                 const rs_complex* v, const int32_t* order, int64_t npos, int32_t H,
-                int32_t* sptr, int32_t* sci, rs_complex* sv, int64_t* total, void* stream) {
+                const int32_t* level, int32_t* sptr, int32_t* sci, rs_complex* sv, int32_t* skey,
+                int64_t* total, void* stream) {
   RS_CHECK_ARG(nsys >= 0 && n >= 0 && npos >= 0, "negative size");
   RS_CHECK_ARG(H >= 1 && H <= 32 && (H & (H - 1)) == 0 && npos % H == 0, "bad slice height");
-  return tri_sell(nsys, n, upper, rp, ci, C2(v), order, npos, H, sptr, sci, M2(sv), total,
-                  S(stream));
+  return tri_sell(nsys, n, upper, rp, ci, C2(v), order, npos, H, level, sptr, sci, M2(sv), skey,
+                  total, S(stream));
 }
 
 static int grid_args(const rs_grid_args* p, GridArgs* a) {
@@ -169,6 +171,7 @@ static int grid_args(const rs_grid_args* p, GridArgs* a) {
     t.sptr = f.sptr;
     t.sci = f.sci;
     t.sv = C2(f.sv);
+    t.skey = f.skey;
     t.nslices = f.nslices;
     t.G = f.lanes_per_row;
     t.apw = f.active_warps;
@@ -178,9 +181,10 @@ static int grid_args(const rs_grid_args* p, GridArgs* a) {
   a->U = tf(p->U);
   a->have_M = p->L.order != nullptr;
   if (a->have_M) {
-    RS_CHECK_ARG(p->U.order && p->rdiag && p->pinv, "incomplete preconditioner");
+    RS_CHECK_ARG(p->U.order && p->rdiag && p->pinv && p->L.skey && p->U.skey,
+                 "incomplete preconditioner");
     for (int g : {a->L.G, a->U.G})
-      RS_CHECK_ARG(g == 1 || g == 4 || g == 32, "lanes_per_row must be 1, 4 or 32");
+      RS_CHECK_ARG(g == 1 || g == 2 || g == 4 || g == 32, "lanes_per_row must be 1, 2, 4 or 32");
     RS_CHECK_ARG(!p->colp || p->nb == p->n, "column pre-ordering needs a single block");
   }
   a->rd = C2(p->rdiag);

@@ -20,6 +20,8 @@
 // handling: their DAGs are simply disjoint.
 #include <cub/cub.cuh>
 
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -29,48 +31,46 @@ namespace {
 
 inline unsigned grid_of(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-__device__ __forceinline__ int ld_lvl(const int32_t* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void st_lvl(int32_t* p, int v) {
-  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// Levels by Kahn's topological sweep over the raw CSC factor (column c lists
+// the rows that depend on row c): one launch per level, the frontier of rows
+// whose dependencies are all settled handed from launch to launch through two
+// device buffers, so the work is O(nnz) plus one small launch per level and
+// nothing ever spins.  (A first version propagated levels row by row with
+// spinning warps: 31.7 s on config 5's 2.56M-row factor -- every waiting lane
+// polling hammers L2 and starves the rows that could progress.)
+__global__ void kahn_init_kernel(int64_t N, const int32_t* __restrict__ rp,
+                                 int32_t* __restrict__ indeg, int32_t* __restrict__ frontier,
+                                 int32_t* __restrict__ counts) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= N) return;
+  const int32_t d = rp[g + 1] - rp[g];
+  indeg[g] = d;
+  if (d == 0) frontier[atomicAdd(counts, 1)] = (int32_t)g;
 }
 
-// Levels by propagation in sweep order.  Warps claim rows through a ticket
-// (4 at a time), so a row only ever waits on rows claimed before it: no
-// deadlock whatever the number of resident CTAs.  level[] starts at -1.
-constexpr int CLAIM = 4;
-__global__ void __launch_bounds__(256) tri_level_kernel(int64_t N, int32_t n, int upper,
-                                                        const int32_t* __restrict__ rp,
-                                                        const int32_t* __restrict__ ci,
-                                                        int32_t* level,
-                                                        unsigned long long* next) {
+// one warp per frontier row
+__global__ void __launch_bounds__(256) kahn_level_kernel(
+    int32_t lev, int32_t n, int upper, const int32_t* __restrict__ cp,
+    const int32_t* __restrict__ ri, int64_t cap, const int32_t* __restrict__ cur,
+    int32_t* __restrict__ nxt, int32_t* counts, int32_t* indeg, int32_t* __restrict__ level,
+    unsigned long long* processed) {
+  const int32_t m = counts[lev];
+  if (blockIdx.x == 0 && threadIdx.x == 0 && m > 0) atomicAdd(processed, (unsigned long long)m);
   const int lane = threadIdx.x & 31;
-  while (true) {
-    unsigned long long q0 = 0;
-    if (lane == 0) q0 = atomicAdd(next, (unsigned long long)CLAIM);
-    q0 = __shfl_sync(0xffffffffu, q0, 0);
-    if (q0 >= (unsigned long long)N) break;
-    const int64_t q1 = min((int64_t)q0 + CLAIM, N);
-    for (int64_t q = (int64_t)q0; q < q1; ++q) {
-      const int64_t b = q / n;
-      const int32_t j = (int32_t)(q % n);
-      const int64_t g = b * n + (upper ? n - 1 - j : j);
-      const int32_t p0 = rp[g], p1 = rp[g + 1];
-      int m = 0;
-      for (int32_t p = p0 + lane; p < p1; p += 32) {
-        const int32_t* d = level + b * n + ci[p];
-        int lv;
-        do {
-          lv = ld_lvl(d);
-        } while (lv < 0);
-        m = max(m, lv + 1);
-      }
-      for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) st_lvl(level + g, m);
-      __syncwarp();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < m; t += nw) {
+    const int32_t g = cur[t];
+    if (lane == 0) level[g] = lev;
+    const int64_t b = g / n;
+    const int32_t c = g - (int32_t)(b * n);
+    const int32_t* col = cp + b * (n + 1);
+    // L: skip the unit diagonal (first); U: skip the pivot (last)
+    const int32_t p0 = upper ? col[c] : col[c] + 1;
+    const int32_t p1 = upper ? col[c + 1] - 1 : col[c + 1];
+    const int32_t* rows = ri + b * cap;
+    for (int32_t p = p0 + lane; p < p1; p += 32) {
+      const int32_t i = (int32_t)(b * n) + rows[p];
+      if (atomicSub(indeg + i, 1) == 1) nxt[atomicAdd(counts + lev + 1, 1)] = i;
     }
   }
 }
@@ -87,20 +87,28 @@ __global__ void level_pad_kernel(int64_t nlev, int32_t H, const int32_t* __restr
   if (l < nlev) padded[l] = (hist[l] + H - 1) / H * H;
 }
 
-__global__ void iota_kernel(int64_t N, int32_t* __restrict__ v) {
+// sort key (level, longest row first); value = row.  Rows of one level are
+// independent, so their order is free: sorting them by length gives slices of
+// uniform width (less padding, and most slices fit one register chunk).
+__global__ void sort_keys_kernel(int64_t N, const int32_t* __restrict__ level,
+                                 const int32_t* __restrict__ rp, unsigned long long* __restrict__ key,
+                                 int32_t* __restrict__ v) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < N) v[g] = (int32_t)g;
+  if (g >= N) return;
+  const unsigned len = (unsigned)(rp[g + 1] - rp[g]);
+  key[g] = ((unsigned long long)(unsigned)level[g] << 32) | (0xffffffffu - len);
+  v[g] = (int32_t)g;
 }
 
 // sorted index k (rows sorted by level, ties by row) -> padded position
-__global__ void level_place_kernel(int64_t N, const int32_t* __restrict__ lev_sorted,
+__global__ void level_place_kernel(int64_t N, const unsigned long long* __restrict__ key_sorted,
                                    const int32_t* __restrict__ row_sorted,
                                    const int32_t* __restrict__ off,
                                    const int32_t* __restrict__ poff,
                                    int32_t* __restrict__ order) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= N) return;
-  const int32_t l = lev_sorted[k];
+  const int32_t l = (int32_t)(key_sorted[k] >> 32);
   order[poff[l] + ((int32_t)k - off[l])] = row_sorted[k];
 }
 
@@ -114,6 +122,32 @@ __global__ void trisell_width_kernel(int64_t npos, int32_t H, const int32_t* __r
   const int32_t G = 32 / H;
   const int32_t len = rp[g + 1] - rp[g];
   atomicMax(width + pos / H, 32 * ((len + G - 1) / G));
+}
+
+// the dependency of the highest level per slice (packed level:column, max)
+__global__ void trisell_key_kernel(int64_t npos, int32_t n, int32_t H,
+                                   const int32_t* __restrict__ order,
+                                   const int32_t* __restrict__ rp,
+                                   const int32_t* __restrict__ ci,
+                                   const int32_t* __restrict__ level,
+                                   unsigned long long* __restrict__ best) {
+  const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= npos) return;
+  const int32_t g = order[pos];
+  if (g < 0) return;
+  const int32_t cb = (g / n) * n;
+  unsigned long long m = 0;
+  for (int32_t p = rp[g]; p < rp[g + 1]; ++p) {
+    const int32_t c = cb + ci[p];
+    const unsigned long long k = ((unsigned long long)(unsigned)(level[c] + 1) << 32) | (unsigned)c;
+    m = k > m ? k : m;
+  }
+  if (m) atomicMax(best + pos / H, m);
+}
+__global__ void trisell_key_out_kernel(int64_t nslices, const unsigned long long* __restrict__ best,
+                                       int32_t* __restrict__ skey) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nslices) skey[s] = best[s] ? (int32_t)(best[s] & 0xffffffffu) : -1;
 }
 
 // one thread per (slice, lane)
@@ -155,54 +189,85 @@ __global__ void trisell_fill_kernel(int64_t nslices, int32_t n, int32_t H, int u
 
 }  // namespace
 
-int tri_levels(int B, int32_t n, int upper, const int32_t* rp, const int32_t* ci, int32_t* level,
-               int64_t* nlev_host, cudaStream_t st) {
+int tri_levels(int B, int32_t n, int upper, const int32_t* rp, const int32_t* cp,
+               const int32_t* ri, int64_t cap, int32_t* level, int64_t* nlev_host,
+               cudaStream_t st) {
   const int64_t N = (int64_t)B * n;
-  if (N == 0) {
-    *nlev_host = 0;
-    return RS_OK;
-  }
-  unsigned long long* next = nullptr;
-  RS_CUDA_TRY(cudaMallocAsync(&next, 16, st));
-  RS_CUDA_TRY(cudaMemsetAsync(next, 0, 16, st));
-  RS_CUDA_TRY(cudaMemsetAsync(level, 0xff, sizeof(int32_t) * N, st));
-  int dev = 0, sms = 0;
-  RS_CUDA_TRY(cudaGetDevice(&dev));
-  RS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const unsigned grid = (unsigned)std::min<int64_t>((N + 8 * CLAIM - 1) / (8 * CLAIM), 8 * sms);
-  tri_level_kernel<<<grid, 256, 0, st>>>(N, n, upper, rp, ci, level, next);
+  *nlev_host = 0;
+  if (N == 0) return RS_OK;
+  int32_t *indeg = nullptr, *fr = nullptr, *counts = nullptr;
+  unsigned long long* processed = nullptr;
+  auto cleanup = [&]() {
+    for (void* p : {(void*)indeg, (void*)fr, (void*)counts, (void*)processed})
+      if (p) cudaFreeAsync(p, st);
+  };
+#define LV_TRY(expr)                                                        \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) {                                                \
+      ::rs::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,            \
+                      cudaGetErrorString(_e));                              \
+      cleanup();                                                            \
+      return RS_ERR_CUDA;                                                   \
+    }                                                                       \
+  } while (0)
+  LV_TRY(cudaMallocAsync(&indeg, sizeof(int32_t) * N, st));
+  LV_TRY(cudaMallocAsync(&fr, sizeof(int32_t) * 2 * N, st));
+  LV_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (N + 2), st));
+  LV_TRY(cudaMallocAsync(&processed, sizeof(unsigned long long), st));
+  LV_TRY(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (N + 2), st));
+  LV_TRY(cudaMemsetAsync(processed, 0, sizeof(unsigned long long), st));
+  kahn_init_kernel<<<grid_of(N, 256), 256, 0, st>>>(N, rp, indeg, fr, counts);
   count_launch();
-  RS_CUDA_TRY(cudaGetLastError());
-  // max level -> host
-  int32_t* dmax = reinterpret_cast<int32_t*>(next + 1);
-  size_t tmp_bytes = 0;
-  RS_CUDA_TRY(cub::DeviceReduce::Max(nullptr, tmp_bytes, level, dmax, (int)N, st));
-  void* tmp = nullptr;
-  RS_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
-  cudaError_t e = cub::DeviceReduce::Max(tmp, tmp_bytes, level, dmax, (int)N, st);
-  cudaFreeAsync(tmp, st);
-  RS_CUDA_TRY(e);
-  int32_t mx = 0;
-  RS_CUDA_TRY(cudaMemcpyAsync(&mx, dmax, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  RS_CUDA_TRY(cudaStreamSynchronize(st));
-  cudaFreeAsync(next, st);
-  *nlev_host = (int64_t)mx + 1;
+  int dev = 0, sms = 0;
+  LV_TRY(cudaGetDevice(&dev));
+  LV_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid = (unsigned)(4 * sms);
+  int64_t lev = 0;
+  unsigned long long done = 0;
+  while (done < (unsigned long long)N && lev <= N) {
+    for (int k = 0; k < 64 && lev <= N; ++k, ++lev) {
+      kahn_level_kernel<<<grid, 256, 0, st>>>((int32_t)lev, n, upper, cp, ri, cap,
+                                              fr + (lev & 1) * N, fr + ((lev + 1) & 1) * N, counts,
+                                              indeg, level, processed);
+      count_launch();
+    }
+    LV_TRY(cudaGetLastError());
+    LV_TRY(cudaMemcpyAsync(&done, processed, sizeof(done), cudaMemcpyDeviceToHost, st));
+    LV_TRY(cudaStreamSynchronize(st));
+  }
+  if (done != (unsigned long long)N) {
+    cleanup();
+    set_error("tri_levels: dependency structure is not triangular");
+    return RS_ERR_ARG;
+  }
+  // number of levels = leading non-empty frontiers
+  std::vector<int32_t> h((size_t)lev);
+  LV_TRY(cudaMemcpyAsync(h.data(), counts, sizeof(int32_t) * (size_t)lev, cudaMemcpyDeviceToHost,
+                         st));
+  LV_TRY(cudaStreamSynchronize(st));
+#undef LV_TRY
+  int64_t nl = 0;
+  while (nl < lev && h[(size_t)nl] > 0) ++nl;
+  cleanup();
+  *nlev_host = nl;
   return RS_OK;
 }
 
 // order[pos] = global row (or -1) with every level padded to a multiple of H.
 // order must hold N + H * nlev entries; *npos_host = positions used.
-int tri_order(int B, int32_t n, const int32_t* level, int64_t nlev, int32_t H, int32_t* order,
-              int64_t* npos_host, cudaStream_t st) {
+int tri_order(int B, int32_t n, const int32_t* level, const int32_t* rp, int64_t nlev, int32_t H,
+              int32_t* order, int64_t* npos_host, cudaStream_t st) {
   const int64_t N = (int64_t)B * n;
   *npos_host = 0;
   if (N == 0 || nlev == 0) return RS_OK;
-  int32_t *hist = nullptr, *padded = nullptr, *off = nullptr, *poff = nullptr, *keys = nullptr,
-          *rows = nullptr, *rows_in = nullptr;
+  int32_t *hist = nullptr, *padded = nullptr, *off = nullptr, *poff = nullptr, *rows = nullptr,
+          *rows_in = nullptr;
+  unsigned long long *keys = nullptr, *keys_in = nullptr;
   void* tmp = nullptr;
   auto cleanup = [&]() {
     for (void* p : {(void*)hist, (void*)padded, (void*)off, (void*)poff, (void*)keys,
-                    (void*)rows, (void*)rows_in, tmp})
+                    (void*)keys_in, (void*)rows, (void*)rows_in, tmp})
       if (p) cudaFreeAsync(p, st);
   };
 #define LV_TRY(expr)                                                        \
@@ -219,7 +284,8 @@ int tri_order(int B, int32_t n, const int32_t* level, int64_t nlev, int32_t H, i
   LV_TRY(cudaMallocAsync(&padded, sizeof(int32_t) * nlev, st));
   LV_TRY(cudaMallocAsync(&off, sizeof(int32_t) * (nlev + 1), st));
   LV_TRY(cudaMallocAsync(&poff, sizeof(int32_t) * (nlev + 1), st));
-  LV_TRY(cudaMallocAsync(&keys, sizeof(int32_t) * N, st));
+  LV_TRY(cudaMallocAsync(&keys, sizeof(unsigned long long) * N, st));
+  LV_TRY(cudaMallocAsync(&keys_in, sizeof(unsigned long long) * N, st));
   LV_TRY(cudaMallocAsync(&rows, sizeof(int32_t) * N, st));
   LV_TRY(cudaMallocAsync(&rows_in, sizeof(int32_t) * N, st));
   LV_TRY(cudaMemsetAsync(hist, 0, sizeof(int32_t) * nlev, st));
@@ -234,17 +300,17 @@ int tri_order(int B, int32_t n, const int32_t* level, int64_t nlev, int32_t H, i
     cleanup();
     return rc;
   }
-  // stable sort of the rows by level (ties keep ascending row order)
-  iota_kernel<<<grid_of(N, 256), 256, 0, st>>>(N, rows_in);
+  // stable sort of the rows by (level, longest first); ties keep ascending rows
+  sort_keys_kernel<<<grid_of(N, 256), 256, 0, st>>>(N, level, rp, keys_in, rows_in);
   count_launch();
   int bits = 1;
   while (((int64_t)1 << bits) < nlev) ++bits;
   size_t tmp_bytes = 0;
-  LV_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, level, keys, rows_in, rows, (int)N,
-                                         0, bits, st));
+  LV_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys, rows_in, rows, (int)N,
+                                         0, 32 + bits, st));
   LV_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
-  LV_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, level, keys, rows_in, rows, (int)N, 0,
-                                         bits, st));
+  LV_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys, rows_in, rows, (int)N, 0,
+                                         32 + bits, st));
   LV_TRY(cudaMemsetAsync(order, 0xff, sizeof(int32_t) * npos, st));
   level_place_kernel<<<grid_of(N, 256), 256, 0, st>>>(N, keys, rows, off, poff, order);
   count_launch();
@@ -258,8 +324,8 @@ int tri_order(int B, int32_t n, const int32_t* level, int64_t nlev, int32_t H, i
 // Pass 1 (sci == null): sptr[npos/H + 1] and *total (padded entries, host).
 // Pass 2: fill sci / sv.
 int tri_sell(int B, int32_t n, int upper, const int32_t* rp, const int32_t* ci, const double2* v,
-             const int32_t* order, int64_t npos, int32_t H, int32_t* sptr, int32_t* sci,
-             double2* sv, int64_t* total, cudaStream_t st) {
+             const int32_t* order, int64_t npos, int32_t H, const int32_t* level, int32_t* sptr,
+             int32_t* sci, double2* sv, int32_t* skey, int64_t* total, cudaStream_t st) {
   const int64_t nslices = npos / H;
   if (!sci) {
     int32_t* width = nullptr;
@@ -284,6 +350,17 @@ int tri_sell(int B, int32_t n, int upper, const int32_t* rp, const int32_t* ci, 
     trisell_fill_kernel<<<grid_of(nslices * 32, 256), 256, 0, st>>>(nslices, n, H, upper, order,
                                                                     rp, ci, v, sptr, sci, sv);
     count_launch();
+    if (skey) {  // the slice's latest dependency: what its warp waits on first
+      unsigned long long* best = nullptr;
+      RS_CUDA_TRY(cudaMallocAsync(&best, sizeof(unsigned long long) * nslices, st));
+      RS_CUDA_TRY(cudaMemsetAsync(best, 0, sizeof(unsigned long long) * nslices, st));
+      trisell_key_kernel<<<grid_of(npos, 256), 256, 0, st>>>(npos, n, H, order, rp, ci, level,
+                                                             best);
+      count_launch();
+      trisell_key_out_kernel<<<grid_of(nslices, 256), 256, 0, st>>>(nslices, best, skey);
+      count_launch();
+      cudaFreeAsync(best, st);
+    }
     RS_CUDA_TRY(cudaGetLastError());
   }
   return RS_OK;

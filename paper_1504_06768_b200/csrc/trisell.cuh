@@ -27,8 +27,9 @@ struct TriSell {
   const int32_t* sptr;   // [nslices + 1] entry offsets (multiples of 32)
   const int32_t* sci;    // global column per entry, -1 = padding
   const double2* sv;
+  const int32_t* skey;   // [nslices] the slice's dependency of the highest level (-1: none)
   int32_t nslices;
-  int32_t G;  // lanes per row (1, 4 or 32); H = 32 / G rows per slice
+  int32_t G;  // lanes per row (1, 2, 4 or 32); H = 32 / G rows per slice
   // Warps per CTA that take part in the sweep (0 = all).  Every waiting lane
   // polls a value near the sweep's frontier, so a narrow DAG (config 3: ~3
   // rows per level) swept by every resident warp turns the frontier's L2
@@ -49,14 +50,21 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 // Ordered fold of one step's products into the row accumulators: the G lanes
 // of a row subtract their products in lane order (= storage order).
+// `live`: ballot of the lanes holding a real entry in this step; trailing
+// lane positions that are padding in every row of the slice are skipped
+// (subtracting their +0 would change nothing).
 template <int G>
-__device__ __forceinline__ void fold_step(double2& acc, double2 p, int r) {
+__device__ __forceinline__ void fold_step(double2& acc, double2 p, int r, unsigned live) {
   constexpr unsigned FULL = 0xffffffffu;
   if (G == 1) {
     acc = csub(acc, p);
   } else {
+    unsigned m = live;
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
+    for (int sh = G; sh < 32; sh <<= 1) m |= m >> sh;
+    m &= (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
+    const int cnt = 32 - __clz(m);  // lane positions 0 .. cnt-1 of a row are in use
+    for (int j = 0; j < cnt; ++j) {
       const double px = __shfl_sync(FULL, p.x, r * G + j);
       const double py = __shfl_sync(FULL, p.y, r * G + j);
       acc = csub(acc, make_double2(px, py));
@@ -67,12 +75,14 @@ __device__ __forceinline__ void fold_step(double2& acc, double2 p, int r) {
 // One slice.  rhs: right-hand side (final values); out: solution vector
 // (sentinel-initialised, published per row); rd: recipc(U_cc) (UPPER).
 //
-// Waiting is decoupled from folding.  A slice of up to KREG steps (the sparse
-// factors of config 5) keeps all its entries in registers: every source value
-// is requested at once, the not-yet-published ones are re-polled together,
-// and the fold runs from registers -- so a dependency hop costs one L2 round
-// trip, not one per step.  Wider slices first wait for every source (loads
-// four steps deep), then stream the fold with plain pipelined loads.
+// Waiting is decoupled from loading and folding.  The slice is consumed in
+// chunks of KREG steps held in registers: a chunk's factor entries are loaded
+// with KREG independent loads per lane, every source value is requested at
+// once, the not-yet-published ones are re-polled together, and the fold runs
+// from registers in storage order.  The static loads of a slice's first chunk
+// are issued before any waiting, so a dependency hop costs one L2 round trip
+// plus the fold -- not one round trip per step (measured: 30 us per level with
+// step-by-step loads on config 5).
 constexpr int KREG = 8;
 
 template <bool UPPER, int G>
@@ -87,18 +97,32 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
   unsigned long long* const tt = (!UPPER && lane == 0) ? g_slice_times : nullptr;
   if (tt) tt[3 * (int64_t)s] = gtime();
   double2 acc = row >= 0 ? __ldcg(rhs + row) : make_double2(0.0, 0.0);
+  double2 rdv = make_double2(1.0, 0.0);
+  if (UPPER && row >= 0) rdv = ldg2(rd + row);
   const int32_t* ci = T.sci + base + lane;
   const double2* av = T.sv + base + lane;
-  if (w <= KREG) {
+  for (int32_t k0 = 0; k0 < w; k0 += KREG) {
     int32_t c[KREG];
     double2 a[KREG], y[KREG];
 #pragma unroll
     for (int k = 0; k < KREG; ++k) {
       c[k] = -1;
-      if (k < w) {
-        c[k] = __ldg(ci + 32 * k);
-        a[k] = ldg2(av + 32 * k);
+      if (k0 + k < w) {
+        c[k] = __ldg(ci + 32 * (k0 + k));
+        a[k] = ldg2(av + 32 * (k0 + k));
       }
+    }
+    if (k0 == 0) {
+      // One lane watches the slice's latest dependency (highest level) while
+      // the entry loads above are in flight; when it is published the others
+      // almost always are.  Polling every source from every waiting lane
+      // (1,184 warps x 32 lanes x 8 loads on config 5) saturates L2 and
+      // stretches each dependency hop to ~16 us.
+      const int32_t key = __ldg(T.skey + s);
+      if (key >= 0 && lane == 0)
+        while (!cta::is_ready(cta::vld2(out + key))) {
+        }
+      __syncwarp();
     }
     unsigned pend = 0;
 #pragma unroll
@@ -115,56 +139,17 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
       for (int k = 0; k < KREG; ++k)
         if (((pend >> k) & 1u) && cta::is_ready(y[k])) pend &= ~(1u << k);
     }
-    if (tt) tt[3 * (int64_t)s + 1] = gtime();
+    if (tt && k0 == 0) tt[3 * (int64_t)s + 1] = gtime();
 #pragma unroll
     for (int k = 0; k < KREG; ++k) {
-      if (k < w) {  // warp-uniform
+      if (k0 + k < w) {  // warp-uniform
         const double2 p = c[k] >= 0 ? cmul_plain(a[k], y[k]) : make_double2(0.0, 0.0);
-        fold_step<G>(acc, p, r);
-      }
-    }
-  } else {
-    // phase A: every source of this lane is published (four steps in flight)
-    for (int32_t k0 = 0; k0 < w; k0 += 4) {
-      int32_t c[4];
-      double2 y[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = (k0 + u < w) ? __ldg(ci + 32 * (k0 + u)) : -1;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c[u] >= 0) y[u] = cta::vld2(out + c[u]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c[u] >= 0)
-          while (!cta::is_ready(y[u])) y[u] = cta::vld2(out + c[u]);
-    }
-    if (tt) tt[3 * (int64_t)s + 1] = gtime();
-    // phase B: ordered fold, plain loads (published values never change)
-    for (int32_t k0 = 0; k0 < w; k0 += 4) {
-      int32_t c[4];
-      double2 a[4], y[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        c[u] = -1;
-        if (k0 + u < w) {
-          c[u] = __ldg(ci + 32 * (k0 + u));
-          a[u] = ldg2(av + 32 * (k0 + u));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c[u] >= 0) y[u] = __ldcg(out + c[u]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (k0 + u < w) {
-          const double2 p = c[u] >= 0 ? cmul_plain(a[u], y[u]) : make_double2(0.0, 0.0);
-          fold_step<G>(acc, p, r);
-        }
+        fold_step<G>(acc, p, r, G == 1 ? 0u : __ballot_sync(0xffffffffu, c[k] >= 0));
       }
     }
   }
   if (row >= 0 && lane % G == 0) {
-    if (UPPER) acc = cmul_plain(acc, rd[row]);
+    if (UPPER) acc = cmul_plain(acc, rdv);
     cta::vst2(out + row, acc);
   }
   if (tt) tt[3 * (int64_t)s + 2] = gtime();
@@ -173,8 +158,9 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
 template <bool UPPER>
 __device__ __forceinline__ void sweep_slice_g(const TriSell& T, int32_t s, const double2* rhs,
                                               double2* out, const double2* rd) {
-  switch (T.G) {  // the layouts levels.cu is asked for: 32, 8 or 1 rows per slice
+  switch (T.G) {  // the layouts levels.cu is asked for: 32, 16, 8 or 1 rows per slice
     case 1: sweep_slice<UPPER, 1>(T, s, rhs, out, rd); break;
+    case 2: sweep_slice<UPPER, 2>(T, s, rhs, out, rd); break;
     case 4: sweep_slice<UPPER, 4>(T, s, rhs, out, rd); break;
     default: sweep_slice<UPPER, 32>(T, s, rhs, out, rd); break;
   }

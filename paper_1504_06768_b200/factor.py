@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -301,12 +302,13 @@ class TriLevels:
     """One triangle in level order (csrc/levels.cu): rows sorted by dependency
     level, levels padded to whole slices of H = 32/G rows, SELL storage."""
 
-    __slots__ = ("order", "sptr", "sci", "sv", "nslices", "G", "nlevels", "entries", "apw")
+    __slots__ = ("order", "sptr", "sci", "sv", "skey", "nslices", "G", "nlevels", "entries",
+                 "apw", "level")
 
     def fill(self, t):
         """Populate an _lib.TriFactor."""
         t.order, t.sptr = self.order.data_ptr(), self.sptr.data_ptr()
-        t.sci, t.sv = self.sci.data_ptr(), self.sv.data_ptr()
+        t.sci, t.sv, t.skey = self.sci.data_ptr(), self.sv.data_ptr(), self.skey.data_ptr()
         t.nslices, t.lanes_per_row = self.nslices, self.G
         t.active_warps = self.apw
 
@@ -319,31 +321,44 @@ def _tri_levels(f, upper):
     st = _lib.stream_ptr()
     level = torch.empty(N, dtype=torch.int32, device=dev)
     nlev = ctypes.c_int64(0)
-    _lib.call("rs_tri_levels", B, n, int(upper), _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(level),
-              ctypes.byref(nlev), st)
+    Lp, Li, _, Up, Ui, _ = f.raw
+    cp, ri, cap = (Up, Ui, f.capU) if upper else (Lp, Li, f.capL)
+    _lib.call("rs_tri_levels", B, n, int(upper), _lib.ptr(rp), _lib.ptr(cp), _lib.ptr(ri), cap,
+              _lib.ptr(level), ctypes.byref(nlev), st)
     # rows per slice: as many as a level typically holds (power of two <= 32);
     # the other 32/H lanes of a warp share each row's entries
     per_level = N / max(nlev.value, 1)
-    H = 32 if per_level >= 24 else (8 if per_level >= 6 else 1)
+    avg_len = float(rp[-1].item()) / max(N, 1)
+    if per_level >= 24:
+        # wide DAG: a slice should fit one register chunk (8 steps) -- two
+        # lanes per row once rows average more than ~5 entries
+        H = 32 if avg_len <= 5.0 else 16
+    else:
+        H = 8 if per_level >= 6 else 1
+    env_h = os.environ.get("RHOSOLVE_TRI_H")
+    if env_h:
+        H = int(env_h)
     order = torch.empty(N + H * nlev.value, dtype=torch.int32, device=dev)
     npos = ctypes.c_int64(0)
-    _lib.call("rs_tri_order", B, n, _lib.ptr(level), nlev.value, H, _lib.ptr(order),
-              ctypes.byref(npos), st)
+    _lib.call("rs_tri_order", B, n, _lib.ptr(level), _lib.ptr(rp), nlev.value, H,
+              _lib.ptr(order), ctypes.byref(npos), st)
     nsl = npos.value // H
     sptr = torch.empty(nsl + 1, dtype=torch.int32, device=dev)
     total = ctypes.c_int64(0)
     args = (B, n, int(upper), _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(v), _lib.ptr(order),
-            npos.value, H, _lib.ptr(sptr))
-    _lib.call("rs_tri_sell", *args, None, None, ctypes.byref(total), st)
+            npos.value, H, _lib.ptr(level), _lib.ptr(sptr))
+    _lib.call("rs_tri_sell", *args, None, None, None, ctypes.byref(total), st)
     t = TriLevels()
     t.sci = torch.empty(max(total.value, 1), dtype=torch.int32, device=dev)
     t.sv = torch.empty(max(total.value, 1), dtype=torch.complex128, device=dev)
-    _lib.call("rs_tri_sell", *args, _lib.ptr(t.sci), _lib.ptr(t.sv), ctypes.byref(total), st)
+    t.skey = torch.empty(max(nsl, 1), dtype=torch.int32, device=dev)
+    _lib.call("rs_tri_sell", *args, _lib.ptr(t.sci), _lib.ptr(t.sv), _lib.ptr(t.skey),
+              ctypes.byref(total), st)
     t.order, t.sptr, t.nslices, t.G = order[:npos.value], sptr, nsl, 32 // H
     t.nlevels, t.entries = nlev.value, total.value
+    t.level = level  # per-row dependency level (diagnostics)
     # sweep window: enough slices in flight to cover ~16 levels of look-ahead,
     # spread over the SMs (16 warps per CTA at most; 0 = all)
-    import os
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     want = 16.0 * nsl / max(nlev.value, 1)
     t.apw = int(min(16, max(1, round(want / sms))))
@@ -426,8 +441,8 @@ def solve_lu_levels(f, b):
 
 
 def _solve_lu_rows(f, b):
-    if f.n >= grid_min_n() and f.ok:
-        return _levels_no_colp(f, b)
+    if f.n >= grid_min_n() and f.ok and float(np.sum(f.lnnz + f.unnz)) / (f.nsys * f.n) < 64.0:
+        return _levels_no_colp(f, b)  # wide DAG (steady._wide): grid-wide level sweeps
     x = torch.empty_like(b)
     if f.csc:
         f.ensure_cols()

@@ -249,10 +249,27 @@ def _solve_grid(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest):
     return x, st
 
 
+def _wide(f):
+    """True when the factors' dependency DAG is wide enough for the grid-wide
+    level sweeps.  A hop between SMs costs ~2 us (tools/hop_probe.py), the
+    one-warp column sweep of colsweep.cuh ~1.4 us per column, so a chain-like
+    DAG (config 3: ~350 entries per row, ~3 rows per level) is faster on one
+    CTA; sparse factors (config 5: ~9 entries per row, thousands of rows per
+    level) belong on the grid.  Decided from the mean row length, which needs
+    no analysis pass; RHOSOLVE_GRID_FORCE=1/0 overrides."""
+    import os
+    force = os.environ.get("RHOSOLVE_GRID_FORCE")
+    if force is not None:
+        return force != "0"
+    if f is None:
+        return True
+    return float(np.sum(f.lnnz + f.unnz)) / (f.nsys * f.n) < 64.0
+
+
 def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0, trace=None):
     dev = A.values.device
     B, n = A.nsys, A.n
-    if B == 1 and n >= _grid_min_n() and trace is None and (f is None or f.ok):
+    if B == 1 and n >= _grid_min_n() and trace is None and (f is None or f.ok) and _wide(f):
         return _solve_grid(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest)
     if not threads:
         # one CTA per system: big batches use 4-warp CTAs so four systems stay

@@ -25,6 +25,7 @@ def _host(o):
 @pytest.fixture
 def grid_everything(monkeypatch):
     monkeypatch.setenv("RHOSOLVE_GRID_MIN_N", "0")
+    monkeypatch.setenv("RHOSOLVE_GRID_FORCE", "1")
 
 
 def _ordered(name, variant, **kw):
