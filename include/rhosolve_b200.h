@@ -418,14 +418,18 @@ int rs_tri_order(int32_t nsys, int32_t n, const int32_t* level, const int32_t* r
 /* Level-ordered SELL copy of the factor: slice s = positions H*s..H*s+H-1;
  * lane r*G + j (G = 32/H) holds entries j, j+G, ... of the slice's r-th row in
  * the reference fold order (L ascending, U descending column), entry (k, lane)
- * at sptr[s] + 32k + lane, global column indices, -1 = padding; skey[s] = the
- * slice's dependency of the highest level (the one its warp watches), -1 when
- * it has none.  Two passes: sci == NULL fills sptr[npos/H + 1] and *total
- * (host); the second fills sci / sv / skey[npos/H]. */
+ * at sptr[s] + 32k + lane, global column indices, -1 = padding; skey holds, for
+ * every chunk of 8 steps of every slice, the chunk's dependency of the highest
+ * level (the one the slice's warp watches), -1 when it has none.  Two passes:
+ * sci == NULL fills sptr[npos/H + 1] and *total (host); the second (with
+ * *total as returned) fills sci / sv / skey[rs_tri_sell_keys(total, npos/H)]. */
 int rs_tri_sell(int32_t nsys, int32_t n, int32_t upper, const int32_t* rp, const int32_t* ci,
                 const rs_complex* v, const int32_t* order, int64_t npos, int32_t H,
                 const int32_t* level, int32_t* sptr, int32_t* sci, rs_complex* sv,
                 int32_t* skey, int64_t* total, void* stream);
+
+/* Entries of rs_tri_sell's skey array. */
+int64_t rs_tri_sell_keys(int64_t total, int64_t nslices);
 
 typedef struct rs_tri_factor {
   const int32_t* order;

@@ -134,7 +134,8 @@ _SIGS = {
                          _vp],
 }
 
-EXPORTED = tuple(_SIGS) + ("rs_last_error", "rs_launch_count", "rs_debug_frontal_taken")
+EXPORTED = tuple(_SIGS) + ("rs_last_error", "rs_launch_count", "rs_debug_frontal_taken",
+                            "rs_tri_sell_keys")
 
 _lib = None
 
@@ -157,6 +158,8 @@ def load():
     lib.rs_last_error.restype = ctypes.c_char_p
     lib.rs_launch_count.argtypes = []
     lib.rs_launch_count.restype = ctypes.c_longlong
+    lib.rs_tri_sell_keys.argtypes = [_i64, _i64]
+    lib.rs_tri_sell_keys.restype = _i64
     lib.rs_debug_frontal_taken.argtypes = []
     lib.rs_debug_frontal_taken.restype = _i32
     _lib = lib

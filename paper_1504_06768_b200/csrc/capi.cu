@@ -175,6 +175,7 @@ static int grid_args(const rs_grid_args* p, GridArgs* a) {
     t.nslices = f.nslices;
     t.G = f.lanes_per_row;
     t.apw = f.active_warps;
+    t.mode = f.reserved;
     return t;
   };
   a->L = tf(p->L);
@@ -238,6 +239,8 @@ int rs_grid_apply(const rs_grid_args* p, void* stream) {
   cudaFreeAsync(buf, st);
   return rc;
 }
+
+int64_t rs_tri_sell_keys(int64_t total, int64_t nslices) { return tri_sell_keys(total, nslices); }
 
 int rs_lower_solve(int32_t nsys, int32_t n, const int32_t* Lp, const int32_t* Li,
                    const rs_complex* Lx, int64_t cap, rs_complex* y, void* stream) {

@@ -49,6 +49,7 @@ int tri_levels(int B, int32_t n, int upper, const int32_t* rp, const int32_t* cp
                cudaStream_t st);
 int tri_order(int B, int32_t n, const int32_t* level, const int32_t* rp, int64_t nlev, int32_t H,
               int32_t* order, int64_t* npos_host, cudaStream_t st);
+int64_t tri_sell_keys(int64_t total, int64_t nslices);
 int tri_sell(int B, int32_t n, int upper, const int32_t* rp, const int32_t* ci, const double2* v,
              const int32_t* order, int64_t npos, int32_t H, const int32_t* level, int32_t* sptr,
              int32_t* sci, double2* sv, int32_t* skey, int64_t* total, cudaStream_t st);

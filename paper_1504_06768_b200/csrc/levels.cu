@@ -124,30 +124,37 @@ __global__ void trisell_width_kernel(int64_t npos, int32_t H, const int32_t* __r
   atomicMax(width + pos / H, 32 * ((len + G - 1) / G));
 }
 
-// the dependency of the highest level per slice (packed level:column, max)
-__global__ void trisell_key_kernel(int64_t npos, int32_t n, int32_t H,
+// The dependency of the highest level per CHUNK of KCH steps of every slice
+// (packed level:column, max): what the slice's warp watches before it touches
+// that chunk's sources.  Chunk j of slice s has index (sptr[s]/32)/KCH + s + j.
+constexpr int KCH = 8;  // = tri::KREG (trisell.cuh)
+__global__ void trisell_key_kernel(int64_t npos, int32_t n, int32_t H, int upper,
                                    const int32_t* __restrict__ order,
                                    const int32_t* __restrict__ rp,
                                    const int32_t* __restrict__ ci,
                                    const int32_t* __restrict__ level,
+                                   const int32_t* __restrict__ sptr,
                                    unsigned long long* __restrict__ best) {
   const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= npos) return;
   const int32_t g = order[pos];
   if (g < 0) return;
+  const int32_t G = 32 / H;
+  const int64_t s = pos / H;
+  const int64_t cbase = (sptr[s] >> 5) / KCH + s;
   const int32_t cb = (g / n) * n;
-  unsigned long long m = 0;
-  for (int32_t p = rp[g]; p < rp[g + 1]; ++p) {
-    const int32_t c = cb + ci[p];
+  const int32_t e0 = rp[g], len = rp[g + 1] - e0;
+  for (int32_t e = 0; e < len; ++e) {  // e-th term in fold order
+    const int32_t src = upper ? e0 + len - 1 - e : e0 + e;
+    const int32_t c = cb + ci[src];
     const unsigned long long k = ((unsigned long long)(unsigned)(level[c] + 1) << 32) | (unsigned)c;
-    m = k > m ? k : m;
+    atomicMax(best + cbase + (e / G) / KCH, k);
   }
-  if (m) atomicMax(best + pos / H, m);
 }
-__global__ void trisell_key_out_kernel(int64_t nslices, const unsigned long long* __restrict__ best,
+__global__ void trisell_key_out_kernel(int64_t nkeys, const unsigned long long* __restrict__ best,
                                        int32_t* __restrict__ skey) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < nslices) skey[s] = best[s] ? (int32_t)(best[s] & 0xffffffffu) : -1;
+  if (s < nkeys) skey[s] = best[s] ? (int32_t)(best[s] & 0xffffffffu) : -1;
 }
 
 // one thread per (slice, lane)
@@ -321,8 +328,11 @@ int tri_order(int B, int32_t n, const int32_t* level, const int32_t* rp, int64_t
   return RS_OK;
 }
 
+// entries of the per-chunk key array for `total` padded entries in `nslices` slices
+int64_t tri_sell_keys(int64_t total, int64_t nslices) { return (total >> 5) / KCH + nslices + 1; }
+
 // Pass 1 (sci == null): sptr[npos/H + 1] and *total (padded entries, host).
-// Pass 2: fill sci / sv.
+// Pass 2 (*total as returned by pass 1): fill sci / sv / skey[tri_sell_keys()].
 int tri_sell(int B, int32_t n, int upper, const int32_t* rp, const int32_t* ci, const double2* v,
              const int32_t* order, int64_t npos, int32_t H, const int32_t* level, int32_t* sptr,
              int32_t* sci, double2* sv, int32_t* skey, int64_t* total, cudaStream_t st) {
@@ -350,14 +360,15 @@ int tri_sell(int B, int32_t n, int upper, const int32_t* rp, const int32_t* ci, 
     trisell_fill_kernel<<<grid_of(nslices * 32, 256), 256, 0, st>>>(nslices, n, H, upper, order,
                                                                     rp, ci, v, sptr, sci, sv);
     count_launch();
-    if (skey) {  // the slice's latest dependency: what its warp waits on first
+    if (skey) {  // per chunk: the latest dependency, what the slice's warp watches
+      const int64_t nkeys = tri_sell_keys(total ? *total : 0, nslices);
       unsigned long long* best = nullptr;
-      RS_CUDA_TRY(cudaMallocAsync(&best, sizeof(unsigned long long) * nslices, st));
-      RS_CUDA_TRY(cudaMemsetAsync(best, 0, sizeof(unsigned long long) * nslices, st));
-      trisell_key_kernel<<<grid_of(npos, 256), 256, 0, st>>>(npos, n, H, order, rp, ci, level,
-                                                             best);
+      RS_CUDA_TRY(cudaMallocAsync(&best, sizeof(unsigned long long) * nkeys, st));
+      RS_CUDA_TRY(cudaMemsetAsync(best, 0, sizeof(unsigned long long) * nkeys, st));
+      trisell_key_kernel<<<grid_of(npos, 256), 256, 0, st>>>(npos, n, H, upper, order, rp, ci,
+                                                             level, sptr, best);
       count_launch();
-      trisell_key_out_kernel<<<grid_of(nslices, 256), 256, 0, st>>>(nslices, best, skey);
+      trisell_key_out_kernel<<<grid_of(nkeys, 256), 256, 0, st>>>(nkeys, best, skey);
       count_launch();
       cudaFreeAsync(best, st);
     }

@@ -27,7 +27,7 @@ struct TriSell {
   const int32_t* sptr;   // [nslices + 1] entry offsets (multiples of 32)
   const int32_t* sci;    // global column per entry, -1 = padding
   const double2* sv;
-  const int32_t* skey;   // [nslices] the slice's dependency of the highest level (-1: none)
+  const int32_t* skey;   // per chunk of KREG steps: its dependency of the highest level (-1: none)
   int32_t nslices;
   int32_t G;  // lanes per row (1, 2, 4 or 32); H = 32 / G rows per slice
   // Warps per CTA that take part in the sweep (0 = all).  Every waiting lane
@@ -36,6 +36,7 @@ struct TriSell {
   // sectors into a hot spot (measured: 41 us per level with 2,368 warps);
   // the window of slices in flight only needs to cover the pre-fold latency.
   int32_t apw;
+  int32_t mode;  // tuning: 1 = wait for every chunk's key before the first chunk
 };
 
 namespace tri {
@@ -101,6 +102,16 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
   if (UPPER && row >= 0) rdv = ldg2(rd + row);
   const int32_t* ci = T.sci + base + lane;
   const double2* av = T.sv + base + lane;
+  const int32_t* keys = T.skey + ((base >> 5) / KREG + s);
+  if (T.mode == 1) {  // tuning: serialize the whole slice behind its latest dependency
+    for (int32_t k0 = 0; k0 < w; k0 += KREG) {
+      const int32_t key = __ldg(keys + k0 / KREG);
+      if (key >= 0 && lane == 0)
+        while (!cta::is_ready(cta::vld2(out + key))) {
+        }
+    }
+    __syncwarp();
+  }
   for (int32_t k0 = 0; k0 < w; k0 += KREG) {
     int32_t c[KREG];
     double2 a[KREG], y[KREG];
@@ -112,13 +123,15 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
         a[k] = ldg2(av + 32 * (k0 + k));
       }
     }
-    if (k0 == 0) {
-      // One lane watches the slice's latest dependency (highest level) while
-      // the entry loads above are in flight; when it is published the others
-      // almost always are.  Polling every source from every waiting lane
-      // (1,184 warps x 32 lanes x 8 loads on config 5) saturates L2 and
-      // stretches each dependency hop to ~16 us.
-      const int32_t key = __ldg(T.skey + s);
+    {
+      // One lane watches this chunk's latest dependency (highest level) while
+      // the entry loads above are in flight; when it is published the chunk's
+      // other sources almost always are.  Early chunks hold the oldest
+      // sources, so they are folded long before the chain arrives and only
+      // the last chunk sits on the critical path.  (Polling every source from
+      // every waiting lane -- 1,184 warps x 32 lanes x 8 loads on config 5 --
+      // saturates L2 and stretches a dependency hop to ~16 us.)
+      const int32_t key = __ldg(keys + k0 / KREG);
       if (key >= 0 && lane == 0)
         while (!cta::is_ready(cta::vld2(out + key))) {
         }

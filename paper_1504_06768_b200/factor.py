@@ -311,6 +311,7 @@ class TriLevels:
         t.sci, t.sv, t.skey = self.sci.data_ptr(), self.sv.data_ptr(), self.skey.data_ptr()
         t.nslices, t.lanes_per_row = self.nslices, self.G
         t.active_warps = self.apw
+        t.reserved = int(os.environ.get("RHOSOLVE_TRI_MODE", "0"))  # tuning hook
 
 
 def _tri_levels(f, upper):
@@ -330,9 +331,10 @@ def _tri_levels(f, upper):
     per_level = N / max(nlev.value, 1)
     avg_len = float(rp[-1].item()) / max(N, 1)
     if per_level >= 24:
-        # wide DAG: a slice should fit one register chunk (8 steps) -- two
-        # lanes per row once rows average more than ~5 entries
-        H = 32 if avg_len <= 5.0 else 16
+        # wide DAG: one lane per row (two lanes per row halve the steps of a
+        # slice but double the slices and their polling: measured slower on
+        # config 5, 12.1 vs 7.8 ms per apply)
+        H = 32
     else:
         H = 8 if per_level >= 6 else 1
     env_h = os.environ.get("RHOSOLVE_TRI_H")
@@ -351,7 +353,8 @@ def _tri_levels(f, upper):
     t = TriLevels()
     t.sci = torch.empty(max(total.value, 1), dtype=torch.int32, device=dev)
     t.sv = torch.empty(max(total.value, 1), dtype=torch.complex128, device=dev)
-    t.skey = torch.empty(max(nsl, 1), dtype=torch.int32, device=dev)
+    nkeys = int(_lib.load().rs_tri_sell_keys(total.value, nsl))
+    t.skey = torch.empty(nkeys, dtype=torch.int32, device=dev)
     _lib.call("rs_tri_sell", *args, _lib.ptr(t.sci), _lib.ptr(t.sv), _lib.ptr(t.skey),
               ctypes.byref(total), st)
     t.order, t.sptr, t.nslices, t.G = order[:npos.value], sptr, nsl, 32 // H

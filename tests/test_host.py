@@ -31,7 +31,7 @@ def test_operator_inputs_match_reference(name, kw):
 def test_header_symbols_exported():
     with open(os.path.join(ROOT, "include", "rhosolve_b200.h")) as fh:
         hdr = fh.read()
-    declared = set(re.findall(r"^\s*(?:int|const char\*|long long)\s+(rs_\w+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|const char\*|long long)\s+(rs_\w+)\s*\(", hdr, re.M))
     assert declared, "no declarations parsed"
     lib = _lib.load()
     for sym in sorted(declared):

@@ -39,11 +39,15 @@ def main(N="20", blocks="16", d="1e-2", p="2"):
         w = (tl.sptr[1:] - tl.sptr[:-1]).cpu().numpy() // 32
         print(f"   steps/slice median {np.median(w)} mean {w.mean():.1f} max {w.max()}", flush=True)
     apply_stats(M, f"c5 N={N} blocks={blocks}")
-    for apw in (1, 2, 4, 8, 16):
-        M.Llev.apw = M.Ulev.apw = apw
-        b = torch.randn(n, dtype=torch.complex128, device="cuda")
-        ms = ev_time(lambda: factor.solve_lu_levels(M, b), reps=3)
-        print(f"  apw={apw}: apply {ms:.3f} ms", flush=True)
+    b = torch.randn(n, dtype=torch.complex128, device="cuda")
+    for mode in ("0", "1", "0", "1"):
+        os.environ["RHOSOLVE_TRI_MODE"] = mode
+        for apw in (2, 4, 8, 16):
+            M.Llev.apw = M.Ulev.apw = apw
+            ms = ev_time(lambda: factor.solve_lu_levels(M, b), reps=3)
+            print(f"  mode={mode} apw={apw}: apply {ms:.3f} ms", flush=True)
+    os.environ["RHOSOLVE_TRI_MODE"] = "0"
+    M.Llev.apw = M.Ulev.apw = 4
     # slice timeline of the L sweep
     ns = M.Llev.nslices
     buf = torch.zeros(3 * ns, dtype=torch.int64, device="cuda")
