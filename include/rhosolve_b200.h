@@ -227,6 +227,20 @@ int rs_liouvillian(int32_t D, const int32_t* H_rp, const int32_t* H_ci,
                    double* herm_dev, int32_t* out_rp, int32_t* out_ci,
                    rs_complex* out_v, int64_t* nnz, void* stream);
 
+/* build_liouvillian for nsys systems of equal dimension and operator count in
+ * ONE launch set (the config-4 sweep: 512 instances): H and every C_k are
+ * block-diagonal batches (row pointers over nsys*D rows with absolute
+ * positions, local column indices; H_nnz / C_nnz = entries of the whole
+ * batch).  out_rp spans nsys*D*D rows -- the batch layout of every other entry
+ * point.  *herm_dev = max over the batch.  Two passes as rs_liouvillian;
+ * bit-identical per system. */
+int rs_liouvillian_batch(int32_t nsys, int32_t D, const int32_t* H_rp, const int32_t* H_ci,
+                         const rs_complex* H_v, int64_t H_nnz, int32_t K,
+                         const int32_t* const* C_rp, const int32_t* const* C_ci,
+                         const rs_complex* const* C_v, const int64_t* C_nnz, double* herm_dev,
+                         int32_t* out_rp, int32_t* out_ci, rs_complex* out_v, int64_t* nnz,
+                         void* stream);
+
 /* shift (liouville.py:80-96): L - sigma I, every diagonal stored.  Two passes
  * as above (out_ci == NULL: row pointers and *nnz only). */
 int rs_shift(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,

@@ -113,6 +113,8 @@ _SIGS = {
     "rs_upper_solve": [_i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp],
     "rs_liouvillian": [_i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
                        ctypes.POINTER(_f64), _vp, _vp, _vp, ctypes.POINTER(_i64), _vp],
+    "rs_liouvillian_batch": [_i32, _i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
+                             ctypes.POINTER(_f64), _vp, _vp, _vp, ctypes.POINTER(_i64), _vp],
     "rs_shift": [_i32, _i32, _vp, _vp, _vp, _f64, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp],
     "rs_default_weight": [_i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp],
     "rs_trace_modify": [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -39,6 +39,7 @@ struct OpCSR {
 struct AssembleArgs {
   int32_t D;
   int32_t K;
+  int32_t B;  // systems: every operator is a block-diagonal batch of B D x D CSRs
   OpCSR H, Ht;
   OpCSR C[MAX_COPS], CDC[MAX_COPS], CDCt[MAX_COPS];
 };
@@ -84,8 +85,10 @@ __global__ void assemble_kernel(AssembleArgs a, int32_t* counts, const int32_t* 
   const int32_t D = a.D;
   const int64_t n = (int64_t)D * D;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int32_t i = (int32_t)(r / D), k = (int32_t)(r % D);
+  if (r >= n * a.B) return;
+  const int64_t ob = (r / n) * D;  // first operator row of this system
+  const int32_t rl = (int32_t)(r % n);
+  const int32_t i = rl / D, k = rl % D;
   const int nt = 2 + 3 * a.K;
   Cursor cur[2 + 3 * MAX_COPS];
   int kinds[2 + 3 * MAX_COPS];
@@ -108,12 +111,12 @@ __global__ void assemble_kernel(AssembleArgs a, int32_t* counts, const int32_t* 
     mats[t] = X;
     Cursor c;
     const int32_t rowsel = (kind == 0) ? k : i;
-    c.p = X.rp[rowsel];
-    c.pe = X.rp[rowsel + 1];
+    c.p = X.rp[ob + rowsel];
+    c.pe = X.rp[ob + rowsel + 1];
     c.ts = c.te = c.t = 0;
     if (kind == 2) {
-      c.ts = c.t = X.rp[k];
-      c.te = X.rp[k + 1];
+      c.ts = c.t = X.rp[ob + k];
+      c.te = X.rp[ob + k + 1];
       if (c.ts == c.te) c.p = c.pe;  // empty inner row: no entries
     }
     cur[t] = c;
@@ -183,18 +186,20 @@ __global__ void assemble_kernel(AssembleArgs a, int32_t* counts, const int32_t* 
 }
 
 // ---- C^dag C ----------------------------------------------------------------
-// One CTA per output row i; dense accumulator row in global scratch (D
-// complex + presence flags); sequential over the inner index j (ascending),
-// parallel over the entries of C's row j (distinct output columns).
+// One CTA per output row (global over the batch); dense accumulator row in
+// global scratch (D complex + presence flags); sequential over the inner index
+// j (ascending), parallel over the entries of C's row j (distinct output
+// columns).
 __global__ void cdc_dense_kernel(int32_t D, OpCSR Ct, OpCSR C, double2* acc, int8_t* pres,
                                  int32_t* counts) {
-  const int32_t i = blockIdx.x;
-  double2* row = acc + (int64_t)i * D;
-  int8_t* pr = pres + (int64_t)i * D;
+  const int64_t i = blockIdx.x;
+  const int64_t ob = (i / D) * D;  // first operator row of this system
+  double2* row = acc + i * D;
+  int8_t* pr = pres + i * D;
   for (int32_t c = threadIdx.x; c < D; c += blockDim.x) pr[c] = 0;
   __syncthreads();
   for (int32_t p = Ct.rp[i]; p < Ct.rp[i + 1]; ++p) {
-    const int32_t j = Ct.ci[p];
+    const int64_t j = ob + Ct.ci[p];
     const double2 vj = make_double2(Ct.v[p].x, -Ct.v[p].y);  // adjoint = conj(transpose)
     for (int32_t t = C.rp[j] + threadIdx.x; t < C.rp[j + 1]; t += blockDim.x) {
       const int32_t c = C.ci[t];
@@ -221,14 +226,15 @@ __global__ void cdc_dense_kernel(int32_t D, OpCSR Ct, OpCSR C, double2* acc, int
   }
 }
 
-__global__ void cdc_compact_kernel(int32_t D, const double2* acc, const int8_t* pres,
-                                   const int32_t* rp, int32_t* ci, double2* v) {
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= D) return;
+__global__ void cdc_compact_kernel(int64_t rows, int32_t D, const double2* acc,
+                                   const int8_t* pres, const int32_t* rp, int32_t* ci,
+                                   double2* v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
   int32_t o = rp[i];
   for (int32_t c = 0; c < D; ++c) {
-    const double2 x = acc[(int64_t)i * D + c];
-    if (pres[(int64_t)i * D + c] && !cis_zero(x)) {
+    const double2 x = acc[i * D + c];
+    if (pres[i * D + c] && !cis_zero(x)) {
       ci[o] = c;
       v[o] = x;
       ++o;
@@ -237,12 +243,14 @@ __global__ void cdc_compact_kernel(int32_t D, const double2* acc, const int8_t* 
 }
 
 // max |H - H^dag| over stored entries (liouville.py:62-64).
-__global__ void herm_dev_kernel(int32_t D, OpCSR H, unsigned long long* out) {
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= D) return;
+__global__ void herm_dev_kernel(int64_t rows, int32_t D, OpCSR H, unsigned long long* out) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= rows) return;
+  const int64_t ob = (g / D) * D;
+  const int32_t i = (int32_t)(g - ob);
   double m = 0.0;
-  for (int32_t p = H.rp[i]; p < H.rp[i + 1]; ++p) {
-    const int32_t j = H.ci[p];
+  for (int32_t p = H.rp[g]; p < H.rp[g + 1]; ++p) {
+    const int64_t j = ob + H.ci[p];
     double2 d = H.v[p];
     int32_t lo = H.rp[j], hi = H.rp[j + 1];
     while (lo < hi) {
@@ -273,28 +281,30 @@ static void free_op(OpBufs& b, cudaStream_t st) {
   b = OpBufs();
 }
 
-static int op_transpose(int32_t D, const OpCSR& X, int64_t nnz, OpBufs& out, cudaStream_t st) {
-  RS_CUDA_TRY(cudaMallocAsync(&out.rp, sizeof(int32_t) * (D + 1), st));
+static int op_transpose(int B, int32_t D, const OpCSR& X, int64_t nnz, OpBufs& out,
+                        cudaStream_t st) {
+  RS_CUDA_TRY(cudaMallocAsync(&out.rp, sizeof(int32_t) * ((int64_t)B * D + 1), st));
   RS_CUDA_TRY(cudaMallocAsync(&out.ci, sizeof(int32_t) * (nnz + 1), st));
   RS_CUDA_TRY(cudaMallocAsync(&out.v, sizeof(double2) * (nnz + 1), st));
-  return csr_transpose(1, D, X.rp, X.ci, X.v, out.rp, out.ci, out.v, st);
+  return csr_transpose(B, D, X.rp, X.ci, X.v, out.rp, out.ci, out.v, st);
 }
 
-static int op_cdc(int32_t D, const OpCSR& C, const OpCSR& Ct, OpBufs& out, int64_t* nnz,
+static int op_cdc(int B, int32_t D, const OpCSR& C, const OpCSR& Ct, OpBufs& out, int64_t* nnz,
                   cudaStream_t st) {
   double2* acc = nullptr;
   int8_t* pres = nullptr;
   int32_t* counts = nullptr;
-  RS_CUDA_TRY(cudaMallocAsync(&acc, sizeof(double2) * (int64_t)D * D, st));
-  RS_CUDA_TRY(cudaMallocAsync(&pres, (int64_t)D * D, st));
-  RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (D + 1), st));
-  RS_CUDA_TRY(cudaMallocAsync(&out.rp, sizeof(int32_t) * (D + 1), st));
-  cdc_dense_kernel<<<D, 128, 0, st>>>(D, Ct, C, acc, pres, counts); ::rs::count_launch();
-  int rc = scan_counts(counts, out.rp, D, nnz, st);
+  const int64_t rows = (int64_t)B * D;
+  RS_CUDA_TRY(cudaMallocAsync(&acc, sizeof(double2) * rows * D, st));
+  RS_CUDA_TRY(cudaMallocAsync(&pres, rows * D, st));
+  RS_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (rows + 1), st));
+  RS_CUDA_TRY(cudaMallocAsync(&out.rp, sizeof(int32_t) * (rows + 1), st));
+  cdc_dense_kernel<<<(unsigned)rows, 128, 0, st>>>(D, Ct, C, acc, pres, counts); ::rs::count_launch();
+  int rc = scan_counts(counts, out.rp, rows, nnz, st);
   if (rc == RS_OK) {
     RS_CUDA_TRY(cudaMallocAsync(&out.ci, sizeof(int32_t) * (*nnz + 1), st));
     RS_CUDA_TRY(cudaMallocAsync(&out.v, sizeof(double2) * (*nnz + 1), st));
-    cdc_compact_kernel<<<gridn(D, 128), 128, 0, st>>>(D, acc, pres, out.rp, out.ci, out.v); ::rs::count_launch();
+    cdc_compact_kernel<<<gridn(rows, 128), 128, 0, st>>>(rows, D, acc, pres, out.rp, out.ci, out.v); ::rs::count_launch();
   }
   cudaFreeAsync(acc, st);
   cudaFreeAsync(pres, st);
@@ -305,8 +315,8 @@ static int op_cdc(int32_t D, const OpCSR& C, const OpCSR& Ct, OpBufs& out, int64
 
 // Count pass when out_ci == nullptr (fills out_rp, returns *nnz_out); fill
 // pass otherwise (out_rp must hold the count-pass result).
-int liouvillian_assemble(int32_t D, const int32_t* Hrp, const int32_t* Hci, const double2* Hv,
-                         int64_t Hnnz, int32_t K, const int32_t* const* Crp,
+int liouvillian_assemble(int32_t B, int32_t D, const int32_t* Hrp, const int32_t* Hci,
+                         const double2* Hv, int64_t Hnnz, int32_t K, const int32_t* const* Crp,
                          const int32_t* const* Cci, const double2* const* Cv,
                          const int64_t* Cnnz, double* herm_dev, int32_t* out_rp,
                          int32_t* out_ci, double2* out_v, int64_t* nnz_out, cudaStream_t st) {
@@ -314,30 +324,31 @@ int liouvillian_assemble(int32_t D, const int32_t* Hrp, const int32_t* Hci, cons
     set_error("at most %d collapse operators supported, got %d", MAX_COPS, K);
     return RS_ERR_UNSUPPORTED;
   }
-  const int64_t n = (int64_t)D * D;
+  const int64_t n = (int64_t)B * D * D;  // output rows over the whole batch
   AssembleArgs a;
   a.D = D;
   a.K = K;
+  a.B = B;
   a.H = OpCSR{Hrp, Hci, Hv};
   OpBufs ht, ct[MAX_COPS], cdc[MAX_COPS], cdct[MAX_COPS];
-  int rc = op_transpose(D, a.H, Hnnz, ht, st);
+  int rc = op_transpose(B, D, a.H, Hnnz, ht, st);
   a.Ht = OpCSR{ht.rp, ht.ci, ht.v};
   for (int c = 0; c < K && rc == RS_OK; ++c) {
     a.C[c] = OpCSR{Crp[c], Cci[c], Cv[c]};
-    rc = op_transpose(D, a.C[c], Cnnz[c], ct[c], st);
+    rc = op_transpose(B, D, a.C[c], Cnnz[c], ct[c], st);
     if (rc) break;
     int64_t cnnz = 0;
-    rc = op_cdc(D, a.C[c], OpCSR{ct[c].rp, ct[c].ci, ct[c].v}, cdc[c], &cnnz, st);
+    rc = op_cdc(B, D, a.C[c], OpCSR{ct[c].rp, ct[c].ci, ct[c].v}, cdc[c], &cnnz, st);
     if (rc) break;
     a.CDC[c] = OpCSR{cdc[c].rp, cdc[c].ci, cdc[c].v};
-    rc = op_transpose(D, a.CDC[c], cnnz, cdct[c], st);
+    rc = op_transpose(B, D, a.CDC[c], cnnz, cdct[c], st);
     a.CDCt[c] = OpCSR{cdct[c].rp, cdct[c].ci, cdct[c].v};
   }
   if (rc == RS_OK && herm_dev) {
     unsigned long long* dm = nullptr;
     RS_CUDA_TRY(cudaMallocAsync(&dm, sizeof(unsigned long long), st));
     RS_CUDA_TRY(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
-    herm_dev_kernel<<<gridn(D, 128), 128, 0, st>>>(D, a.H, dm); ::rs::count_launch();
+    herm_dev_kernel<<<gridn((int64_t)B * D, 128), 128, 0, st>>>((int64_t)B * D, D, a.H, dm); ::rs::count_launch();
     unsigned long long hv = 0;
     RS_CUDA_TRY(cudaMemcpyAsync(&hv, dm, sizeof(hv), cudaMemcpyDeviceToHost, st));
     RS_CUDA_TRY(cudaStreamSynchronize(st));

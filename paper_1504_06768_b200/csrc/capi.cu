@@ -46,8 +46,8 @@ int csr_row_norms(int64_t nrows, const int32_t* rp, const double2* v, double* rn
 int factor_to_csr(int B, int32_t n, const int32_t* cp, const int32_t* ri, const double2* rv,
                   int64_t cap, int lower, int32_t* out_rp, int32_t* out_ci, double2* out_v,
                   double2* rU, int64_t* nnz_out, cudaStream_t st);
-int liouvillian_assemble(int32_t D, const int32_t* Hrp, const int32_t* Hci, const double2* Hv,
-                         int64_t Hnnz, int32_t K, const int32_t* const* Crp,
+int liouvillian_assemble(int32_t B, int32_t D, const int32_t* Hrp, const int32_t* Hci,
+                         const double2* Hv, int64_t Hnnz, int32_t K, const int32_t* const* Crp,
                          const int32_t* const* Cci, const double2* const* Cv,
                          const int64_t* Cnnz, double* herm_dev, int32_t* out_rp,
                          int32_t* out_ci, double2* out_v, int64_t* nnz_out, cudaStream_t st);
@@ -507,7 +507,22 @@ int rs_liouvillian(int32_t D, const int32_t* H_rp, const int32_t* H_ci, const rs
   RS_CHECK_ARG(D >= 1, "hilbert dimension must be >= 1");
   RS_CHECK_ARG(K >= 0, "negative collapse operator count");
   RS_CHECK_ARG((int64_t)D * D < ((int64_t)1 << 31), "D*D exceeds int32 indexing");
-  return liouvillian_assemble(D, H_rp, H_ci, C2(H_v), H_nnz, K, C_rp, C_ci,
+  return liouvillian_assemble(1, D, H_rp, H_ci, C2(H_v), H_nnz, K, C_rp, C_ci,
+                              reinterpret_cast<const double2* const*>(C_v), C_nnz, herm_dev,
+                              out_rp, out_ci, M2(out_v), nnz, S(stream));
+}
+
+int rs_liouvillian_batch(int32_t nsys, int32_t D, const int32_t* H_rp, const int32_t* H_ci,
+                         const rs_complex* H_v, int64_t H_nnz, int32_t K,
+                         const int32_t* const* C_rp, const int32_t* const* C_ci,
+                         const rs_complex* const* C_v, const int64_t* C_nnz, double* herm_dev,
+                         int32_t* out_rp, int32_t* out_ci, rs_complex* out_v, int64_t* nnz,
+                         void* stream) {
+  RS_TRY(keep_pool_memory());
+  RS_CHECK_ARG(nsys >= 1 && D >= 1, "sizes must be >= 1");
+  RS_CHECK_ARG(K >= 0, "negative collapse operator count");
+  RS_CHECK_ARG((int64_t)nsys * D * D < ((int64_t)1 << 31), "nsys*D*D exceeds int32 indexing");
+  return liouvillian_assemble(nsys, D, H_rp, H_ci, C2(H_v), H_nnz, K, C_rp, C_ci,
                               reinterpret_cast<const double2* const*>(C_v), C_nnz, herm_dev,
                               out_rp, out_ci, M2(out_v), nnz, S(stream));
 }

@@ -132,13 +132,63 @@ def concat_systems(mats):
                      torch.cat([m.values for m in mats]))
 
 
+def _stack_ops(ops, dev):
+    """Block-diagonal batch of D x D operator CSRs (host) on the device:
+    absolute row pointers over len(ops)*D rows, local column indices."""
+    hs = [as_host_csr(o.matrix) for o in ops]
+    D = hs[0].nrows
+    nnz = np.fromiter((h.nnz for h in hs), dtype=np.int64, count=len(hs))
+    offs = np.concatenate(([0], np.cumsum(nnz)))
+    rp = np.empty(len(hs) * D + 1, dtype=np.int32)
+    for b, h in enumerate(hs):
+        rp[b * D:(b + 1) * D] = h.row_ptr[:-1] + offs[b]
+    rp[-1] = offs[-1]
+    ci = np.concatenate([h.col_idx for h in hs]).astype(np.int32)
+    v = np.ascontiguousarray(np.concatenate([h.values for h in hs]), dtype=np.complex128)
+    return (torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev),
+            torch.from_numpy(v).to(dev), int(offs[-1]))
+
+
 def build_liouvillian_batch(models, device=None):
-    """Assemble several (H, c_ops) of equal dimension into one block-diagonal
-    plain LiouvillianSystem (the config-4 parameter sweep)."""
+    """Assemble several (H, c_ops) of equal dimension and operator count into
+    one block-diagonal plain LiouvillianSystem (the config-4 parameter sweep)
+    with ONE launch set for the whole batch (rs_liouvillian_batch): per system
+    bit-identical to build_liouvillian."""
     _lib.require_cuda()
     dev = device or torch.device("cuda")
-    mats = [_assemble(H, list(c), dev) for H, c in models]
-    return LiouvillianSystem(concat_systems(mats), models[0][0].matrix.nrows, "plain")
+    models = [(H, list(c)) for H, c in models]
+    H0, c0 = models[0]
+    D, K, B = H0.matrix.nrows, len(c0), len(models)
+    for H, c in models:
+        if H.matrix.nrows != D or len(c) != K:
+            raise ValueError("batch members must share the dimension and operator count")
+        for x in c:
+            if tuple(x.dims) != tuple(H.dims):
+                raise ValueError(f"collapse operator dims {x.dims} do not match H {H.dims}")
+    hrp, hci, hv, hnnz = _stack_ops([H for H, _ in models], dev)
+    cops = [_stack_ops([c[k] for _, c in models], dev) for k in range(K)]
+    PArr = ctypes.c_void_p * max(K, 1)
+    c_rp = PArr(*[c[0].data_ptr() for c in cops])
+    c_ci = PArr(*[c[1].data_ptr() for c in cops])
+    c_v = PArr(*[c[2].data_ptr() for c in cops])
+    c_nnz = (ctypes.c_int64 * max(K, 1))(*[c[3] for c in cops])
+    n = D * D
+    rp = torch.empty(B * n + 1, dtype=torch.int32, device=dev)
+    nnz = ctypes.c_int64(0)
+    herm = ctypes.c_double(0.0)
+    st = _lib.stream_ptr()
+    _lib.call("rs_liouvillian_batch", B, D, _lib.ptr(hrp), _lib.ptr(hci), _lib.ptr(hv), hnnz, K,
+              c_rp, c_ci, c_v, c_nnz, ctypes.byref(herm), _lib.ptr(rp), None, None,
+              ctypes.byref(nnz), st)
+    if herm.value > _HERM_TOL:
+        raise ValueError("Hamiltonian is not Hermitian within 1e-12")
+    ci = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+    v = torch.empty(max(nnz.value, 1), dtype=torch.complex128, device=dev)
+    _lib.call("rs_liouvillian_batch", B, D, _lib.ptr(hrp), _lib.ptr(hci), _lib.ptr(hv), hnnz, K,
+              c_rp, c_ci, c_v, c_nnz, None, _lib.ptr(rp), _lib.ptr(ci), _lib.ptr(v),
+              ctypes.byref(nnz), st)
+    torch.cuda.current_stream().synchronize()  # inputs stay alive until the stream drains
+    return LiouvillianSystem(DeviceCSR(n, B, rp, ci[:nnz.value], v[:nnz.value]), D, "plain")
 
 
 def shift(L, sigma=DEFAULT_SIGMA):

@@ -324,3 +324,74 @@ def test_half_solves_bit_exact(cuda, name, kw):
         h = y.cpu().numpy()
         assert bits_equal(h[:n], ref)
         assert np.allclose(h[n:], 2.0 * ref, rtol=1e-12, atol=0)
+
+
+# ---- a1: the whole sweep assembled by one launch set ---------------------------
+def test_batched_assembly_bit_exact(cuda):
+    """rs_liouvillian_batch: every system of the batch bit-identical to the
+    oracle's build_liouvillian (c4 instances 0 / 255 / 511 among others), also
+    for members with different sparsity patterns."""
+    idx = [0, 3, 255, 256, 511]
+    models = [model("c4", i=i) for i in idx]
+    L = liouville.build_liouvillian_batch(models)
+    assert L.nsys == len(idx) and L.hilbert_dim == 40
+    for b, (H, c) in enumerate(models):
+        o = oracle_L(H, c)
+        h = L.matrix.system(b)
+        assert bits_equal(h.row_ptr, o.rp) and bits_equal(h.col_idx, o.ci)
+        assert bits_equal(h.values, o.v)
+    mixed = [configs.kerr(N=12), configs.kerr(N=12, chi=0.0, F=0.25), configs.kerr(N=12, delta=0.0)]
+    L = liouville.build_liouvillian_batch(mixed)
+    for b, (H, c) in enumerate(mixed):
+        o = oracle_L(H, c)
+        h = L.matrix.system(b)
+        assert bits_equal(h.row_ptr, o.rp) and bits_equal(h.col_idx, o.ci)
+        assert bits_equal(h.values, o.v)
+    one = liouville.build_liouvillian(*mixed[1])
+    assert csr_equal(one.matrix, oracle_L(*mixed[1]))
+    with pytest.raises(ValueError):
+        liouville.build_liouvillian_batch([configs.kerr(N=12), configs.kerr(N=10)])
+
+
+# ---- the block-Jacobi opt-ins of ILUTP (NOT reference behaviour) ---------------
+@pytest.mark.parametrize("early", [False, True])
+def test_ilutp_optins_bit_exact_vs_oracle(cuda, early):
+    """pivot_floor / early_drop (rs_factorize_opts) against the oracle carrying
+    the same two opt-ins, on diagonal blocks of the RCM-ordered Kerr x Kerr
+    matrix (the config-5 preconditioner) and on a block that needs the floor."""
+    import scipy.sparse as sp
+    H, c = configs.kerr_kerr(N=8)
+    Lo = oracle_L(H, c)
+    S = O.shift(Lo)
+    fwd, _ = O.rcm(S)
+    A = O.permute(S, fwd)
+    n = A.n
+    As = sp.csr_matrix((A.v, A.ci, A.rp), shape=(n, n))
+    bs = n // 4
+    blocks = []
+    for b in range(4):
+        Bk = As[b * bs:(b + 1) * bs, b * bs:(b + 1) * bs].tocsr()
+        Bk.sort_indices()
+        blocks.append(O.CSR(bs, bs, Bk.indptr.astype(np.int64), Bk.indices.astype(np.int64),
+                            Bk.data.astype(np.complex128)))
+    # block 1 gets two exactly-zero columns: one keeps stored zeros (all-zero
+    # candidates), the other loses its rows to earlier pivots
+    v = blocks[1].v.copy()
+    v[blocks[1].ci == 5] = 0.0
+    blocks[1] = O.CSR(bs, bs, blocks[1].rp, blocks[1].ci, v)
+    M = from_host([_host(m) for m in blocks])
+    f = factor.factor_batch(M, 1e-2, 2.0, pivot_floor=1.0, early_drop=early)
+    assert f.ok
+    for b, m in enumerate(blocks):
+        fo = O.factorize_raw(m, 1e-2, 2.0, pivot_floor=1.0, early_drop=early)
+        lp, li, lx, up, ui, ux, pinv = f.system_raw(b)
+        assert bits_equal(lp, fo.Lp) and bits_equal(li, fo.Li) and bits_equal(lx, fo.Lx), b
+        assert bits_equal(up, fo.Up) and bits_equal(ui, fo.Ui) and bits_equal(ux, fo.Ux), b
+        assert bits_equal(pinv, fo.pinv)
+        assert int(f.nfloor[b]) == fo.nfloor
+    assert int(f.nfloor[1]) >= 1
+    # without the floor the same block reports the reference's zero pivot
+    g = factor.factor_batch(M, 1e-2, 2.0, raise_on_fail=False, early_drop=early)
+    with pytest.raises(O.Breakdown) as e:
+        O.factorize_raw(blocks[1], 1e-2, 2.0, early_drop=early)
+    assert int(g.fail[1]) == e.value.step and g.fail[0] < 0
