@@ -2,7 +2,7 @@
 """Benchmark: steady-state solves/sec of the doubly-iterative inverse-power
 method (BASELINE.json metric) on B200, plus SpMV / ILU-apply HBM GB/s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c1|c2|c3|c5]
     python bench.py --impl reference ...      # the reference CPU path
 
 Default workload = BASELINE config 4, the parameter sweep "reported in
@@ -13,9 +13,11 @@ doubly-iterative variant breaks down on these matrices, so
 its direct inner solve is the oracle.  A step = the whole sweep from
 assembled Liouvillians to 512 density matrices (shift, RCM, permute, LU, the
 device-resident outer iteration, unpermute + post-processing), instances
-sharded contiguously over ranks ("strong": 512 in total).  --config c2 / c1
-time one doubly-iterative solve (replicas over ranks, "weak").  Rank 0 prints
-one JSON line.
+sharded contiguously over ranks ("strong": 512 in total).  --config c1 / c2 /
+c3 time one doubly-iterative solve (replicas over ranks, "weak"); --config c5
+times the n = 2.56M two-cavity solve (block-Jacobi ILUTP under RCM; one GPU:
+the grid-wide solver; N GPUs: rows sharded over ranks, "strong").  Rank 0
+prints one JSON line.
 """
 
 from __future__ import annotations
@@ -41,6 +43,13 @@ WORKLOADS = {
     "c1": ("c1", {}, dict(tol=1e-12, inner="iterative", ordering_name="rcm",
                           solver="bicgstab", d=1e-5, p=10.0, seed=0), 20),
     "c4": ("c4", {}, dict(tol=1e-12, inner="direct", ordering_name="rcm"), 40),
+    "c3": ("c3", {}, dict(tol=1e-12, inner="iterative", ordering_name="rcm",
+                          solver="bicgstab", d=1e-4, p=300.0, seed=12345), 240),
+    # block-Jacobi ILUTP: 16 blocks, (d, p) = (1e-2, 2), the two documented
+    # opt-ins (zero-pivot floor, early drop); the reference has no
+    # block-Jacobi, its global ILUTP of this matrix does not finish in hours
+    "c5": ("c5", {}, dict(tol=1e-10, d=1e-2, p=2.0, seed=3, blocks=16, max_iter=1000,
+                          pivot_floor=1.0, early_drop=True), 1600),
 }
 SWEEP = 512
 DESCR = {
@@ -50,7 +59,23 @@ DESCR = {
           "tol=1e-12, seed=0",
     "c4": "c4: 512-instance JC sweep N=20 x qubit (n=1600 each), inverse_power inner=direct "
           "(complete LU), RCM, tol=1e-12, seeds 2+i",
+    "c3": "c3: optomechanics Nc=6 x Nm=40 (n=57600), inverse_power inner=BiCGStab, "
+          "ILUTP(d=1e-4,p=300) under RCM, tol=1e-12, seed=12345",
+    "c5": "c5: two coupled Kerr cavities N=40 x 40 (n=2560000, nnz=37.1M), inverse_power "
+          "inner=BiCGStab, block-Jacobi ILUTP (16 RCM row blocks, d=1e-2, p=2, early drop, "
+          "pivot floor) under RCM, tol=1e-10, seed=3",
 }
+
+
+def config_dict(cfg, n, systems, nnz_plain):
+    """The workload description, identical on both arms (the driver compares
+    it): what is solved, not how a given arm runs it."""
+    return {"workload": DESCR[cfg], "n": int(n), "systems": int(systems),
+            "nnz_plain": int(nnz_plain),
+            "parallelism": ("independent instances sharded contiguously over ranks"
+                            if cfg == "c4" else
+                            ("RCM row ranges sharded over ranks" if cfg == "c5" else "replicas")),
+            "l2": "GPU arm: flushed before every timed step (256 MiB write)"}
 
 
 def shard(rank, world, count=SWEEP):
@@ -64,6 +89,88 @@ def build_inputs(cfg, rank=0, world=1):
         idx = list(shard(rank, world))
         return idx, [configs.jc_sweep(i) for i in idx]
     return [0], [configs.CONFIGS[key]["build"](**bkw)]
+
+
+def kernel_timings_c5(L, skw, torch):
+    """Config 5 on one GPU: event-timed launches of the factorization of the
+    block-Jacobi blocks, the 834.75 MB SpMV (the bandwidth kernel SURVEY 8(d)
+    names), the grid-wide level-ordered apply and the cooperative solver."""
+    from paper_1504_06768_b200 import _lib, factor, liouville, ordering, sharded, steady
+    st = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def timed(fn, reps=5):
+        ts = []
+        for _ in range(reps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            flush.zero_()
+            torch.cuda._sleep(100_000)
+            a.record(st)
+            fn()
+            b.record(st)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        return statistics.median(ts)
+
+    sh = liouville.shift(L)
+    fwd, inv = ordering.rcm_device(sh.matrix)
+    A = ordering.permute(sh.matrix, fwd, inv)
+    P = ordering.permute(L.matrix, fwd, inv)
+    n, nnz = A.n, A.nnz
+    blocks = skw["blocks"]
+    out, res = {}, {}
+
+    def run_fact():
+        res["M"] = sharded._block_jacobi((A.row_ptr, A.col_idx, A.values), 0, n, n // blocks,
+                                         skw["d"], skw["p"], skw["pivot_floor"], skw["early_drop"])
+
+    fact_s = timed(run_fact, reps=2)
+    M = res["M"]
+    nLU = int(np.sum(M.lnnz) + np.sum(M.unnz))
+    out["factorize"] = {"seconds": fact_s, "bytes": 20 * nnz + 20 * nLU + 8 * (n + blocks),
+                        "kernel": "ilutp_pipeline_kernel",
+                        "note": f"{blocks} block-Jacobi blocks of {n // blocks} rows, multi-CTA "
+                                "column pipeline (transpose, row norms, factorization)"}
+    x = torch.randn(n, dtype=torch.complex128, device="cuda")
+    y = torch.empty_like(x)
+
+    def run_spmv():
+        _lib.call("rs_csr_matvec", 1, n, _lib.ptr(A.row_ptr), _lib.ptr(A.col_idx),
+                  _lib.ptr(A.values), _lib.ptr(x), _lib.ptr(y), _lib.stream_ptr())
+
+    b_spmv = 20 * nnz + 4 * (n + 1) + 32 * n
+    out["spmv"] = {"seconds": timed(run_spmv, reps=20), "bytes": b_spmv,
+                   "kernel": "spmv_warp_kernel"}
+    M.ensure_levels()
+
+    def run_apply():
+        factor.solve_lu_levels(M, x)
+
+    b_apply = 20 * nLU + 72 * n
+    out["ilu_apply"] = {"seconds": timed(run_apply, reps=5), "bytes": b_apply,
+                        "kernel": "grid_apply_kernel",
+                        "note": f"level-ordered sync-free sweeps: L {M.Llev.nlevels} / U "
+                                f"{M.Ulev.nlevels} dependency levels"}
+    x0 = torch.from_numpy(steady.start_vector(n, skw["seed"])).cuda()
+
+    def run_solver():
+        xs, stt = steady._solve_grid(_lib.INV_BICGSTAB, A, P, M, x0, skw["tol"],
+                                     skw["max_iter"], 20, False)
+        res["st"] = stt
+
+    t_solver = timed(run_solver, reps=2)
+    its = int(res["st"]["inner_total"][0])
+    outer = int(res["st"]["outer"][0])
+    # per BiCGStab iteration: 2 SpMV + 2 applies + 11 vector passes (3 fused
+    # reductions, 3 updates); per outer step psolve(b), the plain-L SpMV and
+    # ~8 vector passes
+    b_solver = (its * (2 * b_spmv + 2 * b_apply + 16 * n * 11)
+                + outer * (b_apply + b_spmv + 16 * n * 8))
+    out["solver"] = {"seconds": t_solver, "bytes": int(b_solver), "inner_iterations": its,
+                     "outer_iterations": outer, "kernel": "grid_solver_kernel"}
+    return out
 
 
 # ------------------------------------------------------------ reference ----
@@ -94,7 +201,10 @@ def _ref_worker(args):
         if cfg == "c4":
             kw["seed"] = 2 + i
         RSt.inverse_power(L, **kw)
-    return time.perf_counter() - t
+    dt = time.perf_counter() - t
+    if len(args) > 3 and args[3]:  # also report the size of what was solved
+        return dt, int(Ls[0].matrix.nrows), int(sum(L.matrix.nnz for L in Ls))
+    return dt
 
 
 def _oracle_worker(args):
@@ -118,6 +228,8 @@ def cpu_solves_per_sec(cfg, workers, target_s):
     kind = "reference" if _ref_path() else "port"
     fn = _ref_worker if kind == "reference" else _oracle_worker
     probe = fn((cfg, 1))
+    if workers == 1 and probe >= target_s:  # one solve already fills the budget (c3)
+        return 1.0 / probe, kind, 1, probe
     count = max(1, int(target_s / max(probe, 1e-3)))
     if workers == 1:
         dt = fn((cfg, count))
@@ -133,29 +245,45 @@ def cpu_solves_per_sec(cfg, workers, target_s):
 
 def run_reference(args):
     """The reference CPU implementation on all host cores: one process per
-    core, each step = a bounded sample of the workload (c4: min(512, 16 x
-    cores) sweep instances spread over the pool; c1/c2: one solve per core)."""
+    core.  c4: every step is the WHOLE sweep, the 512 instances dealt
+    contiguously to the processes; c1/c2/c3: one solve per core per step (c3:
+    ~1 min per solve, so steps/warmup are clamped to 1/0); c5: the reference
+    cannot run this configuration (its global ILUTP did not finish in 37 min,
+    SURVEY.md 6.3) -- its csr_matvec on the c5 matrix is timed instead and the
+    line says so."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg = args.config
     workers = os.cpu_count() or 1
-    per_worker = max(1, min(SWEEP, 16 * workers) // workers) if cfg == "c4" else 1
-    per_step = []
     kind = "reference" if _ref_path() else "port"
+    if cfg == "c5":
+        return _reference_c5(args, workers, kind)
+    if cfg == "c3":
+        args.steps, args.warmup = 1, 0
     fn = _ref_worker if kind == "reference" else _oracle_worker
+    if cfg == "c4":
+        cuts = [w * SWEEP // workers for w in range(workers + 1)]
+        jobs = [(cfg, cuts[w + 1] - cuts[w], cuts[w], True) for w in range(workers)]
+        solves = SWEEP
+    else:
+        jobs = [(cfg, 1, 0, True)] * workers
+        solves = workers
+    per_step = []
+    n = nnz = 0
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     with ctx.Pool(workers) as pool:
         for s in range(args.warmup + args.steps):
-            jobs = [(cfg, per_worker, w * per_worker) for w in range(workers)]
             # each worker times its own solve loop (assembly is outside the
             # timed region, as on the GPU arm); the step is the slowest worker
-            dt = max(pool.map(fn, jobs))
+            out = pool.map(fn, jobs)
+            out = [o if isinstance(o, tuple) else (o, 0, 0) for o in out]
+            n = out[0][1]
+            nnz = sum(o[2] for o in out) if cfg == "c4" else out[0][2]
             if s >= args.warmup:
-                per_step.append(dt)
+                per_step.append(max(o[0] for o in out))
     total = sum(per_step)
-    solves = workers * per_worker
     value = solves * len(per_step) / total
     line = {
         "impl": "reference", "metric": "steady-state solves/sec", "value": value,
@@ -163,11 +291,55 @@ def run_reference(args):
         "ms_per_step": 1e3 * total / len(per_step), "higher_is_better": True,
         "scaling": "strong" if cfg == "c4" else "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic",
-        "config": {"workload": DESCR[cfg], "parallelism": f"{workers} CPU processes"},
+        "config": config_dict(cfg, n, SWEEP if cfg == "c4" else 1, nnz),
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": workers, "kind": kind,
-                         "sample": f"{solves} solves per step ({workers} processes x "
-                                   f"{per_worker}), OMP/OpenBLAS threads = 1 per process"},
+                         "sample": f"{solves} solves per step over {workers} processes "
+                                   f"(OMP/OpenBLAS threads = 1 per process)"
+                                   + ("; the whole 512-instance sweep" if cfg == "c4" else "")},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _c5_spmv_worker(_):
+    """Seconds per reference csr_matvec on the RCM-ordered config-5 matrix (the
+    one stage of the reference that is feasible at this size)."""
+    os.environ["OMP_NUM_THREADS"] = "1"
+    rp = _ref_path()
+    if rp and rp not in sys.path:
+        sys.path.insert(0, rp)
+    from rhosolve import liouville as RL, operators as RO, sparse as RS
+    from paper_1504_06768_b200 import configs
+    H, c = configs.kerr_kerr(N=24, ops=RO)  # n = 331,776: the same family, built in ~10 s
+    L = RL.build_liouvillian(H, c).matrix
+    x = np.ones(L.nrows, dtype=np.complex128)
+    RS.matvec(L, x)
+    t = time.perf_counter()
+    for _ in range(5):
+        RS.matvec(L, x)
+    dt = (time.perf_counter() - t) / 5
+    return dt, int(L.nrows), int(L.nnz)
+
+
+def _reference_c5(args, workers, kind):
+    dt, n, nnz = _c5_spmv_worker(None)
+    gbs = (20.0 * nnz + 4.0 * (n + 1) + 32.0 * n) / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "steady-state solves/sec", "value": None,
+        "unit": "solves/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic",
+        "config": config_dict("c5", 2560000, 1, 37129599),
+        "unavailable": "the reference cannot solve config 5: its single-threaded global ILUTP of "
+                       "the n=2.56M matrix did not finish in 37 min (SURVEY.md 6.3; ~2-3.5 h "
+                       "extrapolated) and it has no block-Jacobi",
+        "cpu_baseline": {"value": None, "unit": "solves/s", "cores": 1, "kind": kind,
+                         "sample": f"reference csr_matvec on the N=24 member of the family "
+                                   f"(n={n}, nnz={nnz}): {dt * 1e3:.1f} ms/call = {gbs:.2f} GB/s "
+                                   "algorithmic on one core"},
+        "e2e": {"value": None, "unit": "solves/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -417,6 +589,15 @@ def run_gpu(args):
             return steady.inverse_power_batch(Lx, seeds, **skw)
         total_solves = SWEEP
         scaling = "strong"
+    elif cfg == "c5":
+        from paper_1504_06768_b200 import sharded
+        L = liouville.build_liouvillian(*models[0])
+        seeds = [skw["seed"]]
+
+        def step(Lx):
+            return [sharded.inverse_power_sharded(Lx, **skw)]
+        total_solves = 1  # one system, its rows sharded over the ranks
+        scaling = "strong"
     else:
         L = liouville.build_liouvillian(*models[0])
         seeds = [skw["seed"]]
@@ -490,6 +671,24 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_time = float(t.item())
     e2e_value = total_solves / e2e_time
+    # second end-to-end figure: from the operators (H, c_ops) on
+    # the host -- assembly on the device included -- to rho on the host
+    ops_times = []
+    for _ in range(3):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Lo = (liouville.build_liouvillian_batch(models) if cfg == "c4"
+              else liouville.build_liouvillian(*models[0]))
+        step(Lo)
+        torch.cuda.synchronize()
+        ops_times.append(time.perf_counter() - t0)
+        del Lo
+    ops_time = statistics.median(ops_times)
+    if dist:
+        t = torch.tensor([ops_time], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ops_time = float(t.item())
 
     # parity of this run's results against reference-generated golden rho
     parity = {"max_residual": max(r.residual for r in last)}
@@ -508,6 +707,12 @@ def run_gpu(args):
         if tds:
             parity["max_trace_distance_vs_reference"] = max(tds)
     parity["errors"] = sum(1 for r in last if r.error)
+    if cfg == "c5":  # no reference rho exists at this size: the physical checks
+        rho = last[0].rho
+        parity["trace_minus_one"] = float(abs(np.trace(rho) - 1.0))
+        parity["hermiticity"] = float(np.abs(rho - rho.conj().T).max())
+        parity["note"] = ("residual = ||L vec(rho)||_2 against the plain Liouvillian; the "
+                          "reference itself cannot solve this configuration (SURVEY.md 6.3)")
 
     if rank != 0:
         if dist:
@@ -515,7 +720,8 @@ def run_gpu(args):
         return 0
 
     peak, peak_src = measured_peak()
-    kt = kernel_timings(L, skw, torch, seeds)
+    kt = (kernel_timings_c5(L, skw, torch) if cfg == "c5"
+          else kernel_timings(L, skw, torch, seeds))
     kernels = {}
     for k, v in kt.items():
         gbs = v["bytes"] / v["seconds"] / 1e9
@@ -532,7 +738,15 @@ def run_gpu(args):
             "share_of_step": kt[dom]["seconds"] / step_s}
 
     cpu = None
-    if world == 1 and not args.no_cpu:
+    if cfg == "c5" and world == 1 and not args.no_cpu:
+        dt, cn, cnnz = _c5_spmv_worker(None)
+        cpu = {"value": None, "unit": "solves/s", "cores": 1,
+               "kind": "reference" if _ref_path() else "port",
+               "sample": "the reference cannot solve config 5 (its global ILUTP did not finish "
+                         "in 37 min, SURVEY.md 6.3); its csr_matvec on the N=24 member of the "
+                         f"family (n={cn}, nnz={cnnz}) takes {dt * 1e3:.1f} ms/call = "
+                         f"{(20.0 * cnnz + 36.0 * cn) / dt / 1e9:.2f} GB/s on one core"}
+    elif world == 1 and not args.no_cpu:
         v, kind, count, probe = cpu_solves_per_sec(cfg, 1, args.cpu_seconds)
         cpu = {"value": v, "unit": "solves/s", "cores": 1, "kind": kind,
                "sample": f"{count} sequential solves of the workload's instances on 1 host "
@@ -544,16 +758,18 @@ def run_gpu(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * step_s, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": DESCR[cfg], "n": L.n, "systems_per_gpu": L.nsys,
-                   "nnz_plain_per_gpu": int(L.matrix.nnz),
-                   "parallelism": (f"{world} GPUs, contiguous instance shards" if cfg == "c4"
-                                   else ("replicas" if world > 1 else "single GPU")),
-                   "l2": "flushed before every timed step (256 MiB write)"},
+        "config": config_dict(cfg, L.n, SWEEP if cfg == "c4" else 1,
+                              (int(L.matrix.nnz) // L.nsys) * (SWEEP if cfg == "c4" else 1)),
+        "run": {"gpus": world, "systems_per_gpu": L.nsys,
+                "nnz_plain_per_gpu": int(L.matrix.nnz)},
         "roofline": roof,
         "kernels": kernels,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
+        "e2e_from_operators": {"value": total_solves / ops_time, "unit": "solves/s",
+                               "note": "(H, c_ops) on the host -> device assembly -> solve -> rho "
+                                       "on the host"},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "stages_s": {"build": r0.build_time, "factor": r0.factor_time, "solve": r0.solve_time,

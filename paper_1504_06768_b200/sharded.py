@@ -348,6 +348,7 @@ def inverse_power_sharded(L, sigma=liouville.DEFAULT_SIGMA, tol=1e-10, d=1e-5, p
     comm = Comm(group)
     ops = GpuOps(comm)
     say = (lambda m: log(f"[rank {comm.rank}] {m}")) if log else (lambda m: None)
+    L = liouville.on_device(L)  # a host / pinned matrix is uploaded here
     t0 = time.perf_counter()
     torch.cuda.synchronize()
     shifted = liouville.shift(L, sigma)
