@@ -145,64 +145,102 @@ class Permutation:
         return f"Permutation(n={len(self.forward)})"
 
 
+def _from_sorted_keys(nrows, ncols, keys, vals):
+    """CSR from flat keys (row * ncols + col) that are already unique and
+    ascending."""
+    keys = np.asarray(keys, dtype=np.int64)
+    width = max(ncols, 1)
+    rp = np.zeros(nrows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(keys // width, minlength=nrows), out=rp[1:])
+    return CSRMatrix(nrows, ncols, rp, keys % width, vals)
+
+
+def _flat_keys(a):
+    return a.row_ids() * max(a.ncols, 1) + a.col_idx
+
+
 def identity(n):
-    idx = np.arange(n, dtype=np.int64)
-    return CSRMatrix(n, n, np.arange(n + 1), idx, np.ones(n, dtype=np.complex128))
+    """The n x n identity."""
+    return _from_sorted_keys(n, n, np.arange(n, dtype=np.int64) * (max(n, 1) + 1),
+                             np.ones(n, dtype=np.complex128))
 
 
 def kron(a, b):
-    """((i*b.nrows + k), (j*b.ncols + l)) = a[i,j] * b[k,l]."""
-    ar, ac, av = a.to_coo()
-    br, bc, bv = b.to_coo()
-    rows = (ar[:, None] * b.nrows + br[None, :]).ravel()
-    cols = (ac[:, None] * b.ncols + bc[None, :]).ravel()
-    vals = (av[:, None] * bv[None, :]).ravel()
+    """Kronecker product: entry (i*b.nrows + k, j*b.ncols + l) = a[i,j] * b[k,l]
+    (sparse.py:202-213).  The value products are one outer ufunc call, the
+    arithmetic the reference's broadcast product performs."""
+    rows = np.add.outer(a.row_ids() * b.nrows, b.row_ids()).ravel()
+    cols = np.add.outer(a.col_idx * b.ncols, b.col_idx).ravel()
+    vals = np.multiply.outer(a.values, b.values).ravel()
+    # a's entries are (row, col)-sorted and so are b's, but the combined keys
+    # interleave: let from_coo order them (no duplicates can arise)
     return CSRMatrix.from_coo(a.nrows * b.nrows, a.ncols * b.ncols, rows, cols, vals,
                               prune=False)
 
 
 def transpose(a):
-    r, c, v = a.to_coo()
-    return CSRMatrix.from_coo(a.ncols, a.nrows, c, r, v, prune=False)
+    """a^T: a stable sort of the entries by column keeps rows ascending inside
+    every new row, which is exactly the (row, col) order CSR needs."""
+    order = np.argsort(a.col_idx, kind="stable")
+    rp = np.zeros(a.ncols + 1, dtype=np.int64)
+    np.cumsum(np.bincount(a.col_idx, minlength=a.ncols), out=rp[1:])
+    return CSRMatrix(a.ncols, a.nrows, rp, a.row_ids()[order], a.values[order])
 
 
 def conjugate(a):
-    return CSRMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx, np.conj(a.values))
+    return CSRMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx, a.values.conj())
 
 
 def adjoint(a):
-    return conjugate(transpose(a))
+    return transpose(conjugate(a))
 
 
 def add(a, b, alpha=1.0, beta=1.0):
+    """alpha*a + beta*b with exact zeros dropped (sparse.py:231-240): positions
+    in both operands hold (alpha*a) + (beta*b), the others the scaled entry
+    itself."""
     if a.shape != b.shape:
         raise ValueError(f"shape mismatch: {a.shape} vs {b.shape}")
-    ar, ac, av = a.to_coo()
-    br, bc, bv = b.to_coo()
-    return CSRMatrix.from_coo(a.nrows, a.ncols, np.concatenate([ar, br]),
-                              np.concatenate([ac, bc]),
-                              np.concatenate([alpha * av, beta * bv]))
+    ka, kb = _flat_keys(a), _flat_keys(b)
+    va, vb = alpha * a.values, beta * b.values
+    keys = np.union1d(ka, kb)
+    out = np.empty(len(keys), dtype=np.complex128)
+    ia, ib = np.searchsorted(keys, ka), np.searchsorted(keys, kb)
+    out[ia] = va
+    shared = np.isin(kb, ka, assume_unique=True)
+    out[ib[~shared]] = vb[~shared]
+    out[ib[shared]] = out[ib[shared]] + vb[shared]
+    keep = out != 0
+    return _from_sorted_keys(a.nrows, a.ncols, keys[keep], out[keep])
 
 
 def matmul(a, b):
-    """Row-merge product with scalar accumulation in storage order."""
+    """a @ b (sparse.py:243-265).  Every output entry accumulates its products
+    from 0 in the order (entry of a's row, entry of b's row), each product in
+    the two-rounding complex form of a numpy scalar multiply; exact zeros are
+    dropped.  Vectorised: all products are generated in that order and
+    np.add.at folds them in sequence."""
     if a.ncols != b.nrows:
         raise ValueError(f"shape mismatch: {a.shape} @ {b.shape}")
-    rows, cols, vals = [], [], []
-    bp, bi, bv = b.row_ptr, b.col_idx, b.values
-    for i in range(a.nrows):
-        acc = {}
-        for p in range(a.row_ptr[i], a.row_ptr[i + 1]):
-            j = a.col_idx[p]
-            s = a.values[p]
-            for t in range(bp[j], bp[j + 1]):
-                key = int(bi[t])
-                acc[key] = acc.get(key, 0.0) + s * bv[t]
-        for key, val in acc.items():
-            rows.append(i)
-            cols.append(key)
-            vals.append(val)
-    return CSRMatrix.from_coo(a.nrows, b.ncols, rows, cols, vals)
+    if a.nnz == 0 or b.nnz == 0:
+        return _from_sorted_keys(a.nrows, b.ncols, np.empty(0, np.int64),
+                                 np.empty(0, np.complex128))
+    first = b.row_ptr[a.col_idx]
+    count = b.row_ptr[a.col_idx + 1] - first
+    src_a = np.repeat(np.arange(a.nnz, dtype=np.int64), count)
+    # position inside b: first[src] + (running index within the group)
+    start_of_group = np.repeat(np.cumsum(count) - count, count)
+    src_b = np.repeat(first, count) + (np.arange(len(src_a), dtype=np.int64) - start_of_group)
+    x, y = a.values[src_a], b.values[src_b]
+    prod = np.empty(len(src_a), dtype=np.complex128)
+    prod.real = x.real * y.real - x.imag * y.imag
+    prod.imag = x.real * y.imag + x.imag * y.real
+    keys = a.row_ids()[src_a] * max(b.ncols, 1) + b.col_idx[src_b]
+    uniq, slot = np.unique(keys, return_inverse=True)
+    acc = np.zeros(len(uniq), dtype=np.complex128)
+    np.add.at(acc, slot, prod)
+    keep = acc != 0
+    return _from_sorted_keys(a.nrows, b.ncols, uniq[keep], acc[keep])
 
 
 def as_host_csr(m):
@@ -362,41 +400,35 @@ def write_matrix_market(a, path, comment=None):
         fh.write("\n".join(lines) + "\n")
 
 
+def _mm_tokens(handle):
+    """Whitespace-separated fields of the non-comment, non-blank lines."""
+    for raw in handle:
+        text = raw.strip()
+        if text and not text.startswith("%"):
+            yield text.split()
+
+
 def read_matrix_market(path):
-    """Reader for coordinate general complex / real / integer Matrix Market
-    files (sparse.py:315-351): duplicates summed, nothing pruned."""
-    with open(path, encoding="ascii") as fh:
-        header = fh.readline().strip()
-        fields = header.lower().split()
-        if (len(fields) < 5 or fields[0] != "%%matrixmarket"
-                or fields[1] != "matrix" or fields[2] != "coordinate"):
-            raise ValueError(f"unsupported Matrix Market header: {header}")
-        kind, symmetry = fields[3], fields[4]
+    """Matrix Market coordinate/general reader for complex, real and integer
+    fields (the files sparse.py:315-351 accepts): 1-based indices, duplicate
+    positions summed, explicit zeros kept."""
+    with open(path, encoding="ascii") as handle:
+        banner = handle.readline().split()
+        tag = [t.lower() for t in banner]
+        if len(tag) < 5 or tag[:3] != ["%%matrixmarket", "matrix", "coordinate"]:
+            raise ValueError(f"unsupported Matrix Market header: {' '.join(banner)}")
+        field, symmetry = tag[3], tag[4]
         if symmetry != "general":
             raise ValueError(f"unsupported symmetry: {symmetry}")
-        if kind not in ("complex", "real", "integer"):
-            raise ValueError(f"unsupported field type: {kind}")
-        line = fh.readline()
-        while line.startswith("%") or not line.strip():
-            line = fh.readline()
-        nrows, ncols, nnz = (int(t) for t in line.split())
-        rows = np.empty(nnz, dtype=np.int64)
-        cols = np.empty(nnz, dtype=np.int64)
-        vals = np.empty(nnz, dtype=np.complex128)
-        got = 0
-        for line in fh:
-            line = line.strip()
-            if not line or line.startswith("%"):
-                continue
-            parts = line.split()
-            if got >= nnz:
-                got += 1
-                break
-            rows[got] = int(parts[0]) - 1
-            cols[got] = int(parts[1]) - 1
-            vals[got] = (complex(float(parts[2]), float(parts[3])) if kind == "complex"
-                         else float(parts[2]))
-            got += 1
-        if got != nnz:
-            raise ValueError(f"expected {nnz} entries, found {got}")
-    return CSRMatrix.from_coo(nrows, ncols, rows, cols, vals, prune=False)
+        if field not in ("complex", "real", "integer"):
+            raise ValueError(f"unsupported field type: {field}")
+        body = _mm_tokens(handle)
+        nrows, ncols, nnz = (int(t) for t in next(body))
+        entries = list(body)
+    if len(entries) != nnz:
+        raise ValueError(f"expected {nnz} entries, found {len(entries)}")
+    index = np.array([[int(e[0]), int(e[1])] for e in entries], dtype=np.int64).reshape(-1, 2)
+    vals = np.empty(nnz, dtype=np.complex128)
+    vals.real = [float(e[2]) for e in entries]
+    vals.imag = [float(e[3]) for e in entries] if field == "complex" else 0.0
+    return CSRMatrix.from_coo(nrows, ncols, index[:, 0] - 1, index[:, 1] - 1, vals, prune=False)
