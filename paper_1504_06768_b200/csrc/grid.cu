@@ -36,7 +36,11 @@ namespace rs {
 
 namespace {
 
-constexpr int GT = 512;      // threads per CTA
+constexpr int GT = 256;      // threads per CTA: 255 registers per thread, so the sweeps
+                              // keep a whole chunk in registers (at 512 threads / 128
+                              // registers sweep_slice spilled ~1 KB per call and a
+                              // dependency hop cost 4,460 cycles after the sources
+                              // were loaded)
 constexpr int SP_UNROLL = 4;  // SpMV: chunks of 32 products per warp pass
 constexpr int SP_CH = 32 * SP_UNROLL;
 constexpr int SP_SLOTS = SP_CH + SP_CH / 8;
@@ -760,6 +764,11 @@ int launch_grid_apply(const GridArgs& a, cudaStream_t st) {
 }
 
 }  // namespace rs
+
+extern "C" int rs_debug_slice_clock_mode(int on) {
+  RS_CUDA_TRY(cudaMemcpyToSymbol(rs::tri::g_slice_clock_mode, &on, sizeof(on)));
+  return 0;
+}
 
 extern "C" int rs_debug_slice_times(void* buf) {
   unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);

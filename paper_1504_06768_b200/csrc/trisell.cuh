@@ -43,6 +43,7 @@ namespace tri {
 
 // tuning hook: per-slice (start, first step done, end) global-timer stamps [3 * nslices]
 __device__ unsigned long long* g_slice_times = nullptr;
+__device__ int g_slice_clock_mode = 0;  // 1: slots hold clock64 deltas (key seen->loaded, loaded->published)
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -87,8 +88,8 @@ __device__ __forceinline__ void fold_step(double2& acc, double2 p, int r, unsign
 constexpr int KREG = 8;
 
 template <bool UPPER, int G>
-__device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const double2* rhs,
-                                         double2* out, const double2* rd) {
+__device__ __forceinline__ void sweep_slice(const TriSell& T, int32_t s, const double2* rhs,
+                                            double2* out, const double2* rd) {
   constexpr int H = 32 / G;
   const int lane = threadIdx.x & 31;
   const int r = lane / G;
@@ -112,6 +113,7 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
     }
     __syncwarp();
   }
+  long long ck_seen = 0;
   for (int32_t k0 = 0; k0 < w; k0 += KREG) {
     int32_t c[KREG];
     double2 a[KREG], y[KREG];
@@ -137,6 +139,7 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
         }
       __syncwarp();
     }
+    const long long ck0 = (tt && g_slice_clock_mode) ? clock64() : 0;
     unsigned pend = 0;
 #pragma unroll
     for (int k = 0; k < KREG; ++k)
@@ -152,7 +155,8 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
       for (int k = 0; k < KREG; ++k)
         if (((pend >> k) & 1u) && cta::is_ready(y[k])) pend &= ~(1u << k);
     }
-    if (tt && k0 == 0) tt[3 * (int64_t)s + 1] = gtime();
+    if (tt && k0 == 0) tt[3 * (int64_t)s + 1] = g_slice_clock_mode ? (unsigned long long)(clock64() - ck0) : gtime();
+    ck_seen = (tt && g_slice_clock_mode) ? clock64() : 0;
 #pragma unroll
     for (int k = 0; k < KREG; ++k) {
       if (k0 + k < w) {  // warp-uniform
@@ -165,33 +169,37 @@ __device__ __noinline__ void sweep_slice(const TriSell& T, int32_t s, const doub
     if (UPPER) acc = cmul_plain(acc, rdv);
     cta::vst2(out + row, acc);
   }
-  if (tt) tt[3 * (int64_t)s + 2] = gtime();
-}
-
-template <bool UPPER>
-__device__ __forceinline__ void sweep_slice_g(const TriSell& T, int32_t s, const double2* rhs,
-                                              double2* out, const double2* rd) {
-  switch (T.G) {  // the layouts levels.cu is asked for: 32, 16, 8 or 1 rows per slice
-    case 1: sweep_slice<UPPER, 1>(T, s, rhs, out, rd); break;
-    case 2: sweep_slice<UPPER, 2>(T, s, rhs, out, rd); break;
-    case 4: sweep_slice<UPPER, 4>(T, s, rhs, out, rd); break;
-    default: sweep_slice<UPPER, 32>(T, s, rhs, out, rd); break;
-  }
+  if (tt) tt[3 * (int64_t)s + 2] = g_slice_clock_mode ? (unsigned long long)(clock64() - ck_seen) : gtime();
 }
 
 // The whole sweep from inside a grid-wide kernel: the first apw warps of
 // every CTA take slices in ascending order, consecutive slices going to
 // different CTAs.  All participants are co-resident, so waits cannot deadlock.
+// One out-of-line body per (triangle, lanes per row) with the slice code
+// inlined into its loop: called through the ABI per slice, sweep_slice saved
+// and restored ~0.5-1 KB of registers in local memory on every call and a
+// dependency hop took 4,460 cycles from "sources loaded" to "published".
+template <bool UPPER, int G>
+__device__ __noinline__ void sweep_loop(const TriSell& T, const double2* rhs, double2* out,
+                                        const double2* rd, int32_t first, int32_t stride) {
+  for (int32_t s = first; s < T.nslices; s += stride) sweep_slice<UPPER, G>(T, s, rhs, out, rd);
+}
+
 template <bool UPPER>
-__device__ __noinline__ void sweep_grid(const TriSell& T, const double2* rhs, double2* out,
+__device__ __forceinline__ void sweep_grid(const TriSell& T, const double2* rhs, double2* out,
                                            const double2* rd) {
   const int wpc = blockDim.x >> 5;
   const int apw = (T.apw > 0 && T.apw < wpc) ? T.apw : wpc;
   const int lw = threadIdx.x >> 5;
   if (lw >= apw) return;
   const int32_t stride = apw * (int32_t)gridDim.x;
-  for (int32_t s = lw * (int32_t)gridDim.x + blockIdx.x; s < T.nslices; s += stride)
-    sweep_slice_g<UPPER>(T, s, rhs, out, rd);
+  const int32_t first = lw * (int32_t)gridDim.x + blockIdx.x;
+  switch (T.G) {  // the layouts levels.cu is asked for: 32, 16, 8 or 1 rows per slice
+    case 1: sweep_loop<UPPER, 1>(T, rhs, out, rd, first, stride); break;
+    case 2: sweep_loop<UPPER, 2>(T, rhs, out, rd, first, stride); break;
+    case 4: sweep_loop<UPPER, 4>(T, rhs, out, rd, first, stride); break;
+    default: sweep_loop<UPPER, 32>(T, rhs, out, rd, first, stride); break;
+  }
 }
 
 }  // namespace tri
