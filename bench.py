@@ -45,10 +45,10 @@ WORKLOADS = {
     "c4": ("c4", {}, dict(tol=1e-12, inner="direct", ordering_name="rcm"), 40),
     "c3": ("c3", {}, dict(tol=1e-12, inner="iterative", ordering_name="rcm",
                           solver="bicgstab", d=1e-4, p=300.0, seed=12345), 240),
-    # block-Jacobi ILUTP: 16 blocks, (d, p) = (1e-2, 2), the two documented
+    # block-Jacobi ILUTP: 40 blocks, (d, p) = (1e-2, 2), the two documented
     # opt-ins (zero-pivot floor, early drop); the reference has no
     # block-Jacobi, its global ILUTP of this matrix does not finish in hours
-    "c5": ("c5", {}, dict(tol=1e-10, d=1e-2, p=2.0, seed=3, blocks=16, max_iter=1000,
+    "c5": ("c5", {}, dict(tol=1e-10, d=1e-2, p=2.0, seed=3, blocks=40, max_iter=1000,
                           pivot_floor=1.0, early_drop=True), 1600),
 }
 SWEEP = 512
@@ -62,7 +62,7 @@ DESCR = {
     "c3": "c3: optomechanics Nc=6 x Nm=40 (n=57600), inverse_power inner=BiCGStab, "
           "ILUTP(d=1e-4,p=300) under RCM, tol=1e-12, seed=12345",
     "c5": "c5: two coupled Kerr cavities N=40 x 40 (n=2560000, nnz=37.1M), inverse_power "
-          "inner=BiCGStab, block-Jacobi ILUTP (16 RCM row blocks, d=1e-2, p=2, early drop, "
+          "inner=BiCGStab, block-Jacobi ILUTP (40 RCM row blocks, d=1e-2, p=2, early drop, "
           "pivot floor) under RCM, tol=1e-10, seed=3",
 }
 

@@ -89,6 +89,8 @@ CONFIGS = {
                methods=("power-gmres", "power-bicgstab")),
     "c4": dict(build=jc_sweep, D=40, tol=1e-12, seed=2, d=1e-5, p=10.0,
                methods=("power-direct",)),
-    "c5": dict(build=kerr_kerr, D=1600, tol=1e-10, seed=3, d=1e-5, p=10.0,
-               methods=("power-bicgstab",)),
+    # block-Jacobi ILUTP over 40 RCM row blocks with the two opt-ins of
+    # rs_factorize_opts (config 5): the reference names no (d, p) here
+    "c5": dict(build=kerr_kerr, D=1600, tol=1e-10, seed=3, d=1e-2, p=2.0, blocks=40,
+               pivot_floor=1.0, early_drop=True, methods=("power-bicgstab",)),
 }

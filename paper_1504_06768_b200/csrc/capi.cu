@@ -326,7 +326,12 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
   // hand-off)
   a.cps = 1;
   // (c3: 13.3 s at 1 CTA, 1.70 s at 16, 1.44 s at 32, flat beyond)
-  if (n >= 8192 && nsys < 148) a.cps = std::min(32, std::max(1, 148 / nsys));
+  // ... but only when a column carries enough work to pay for the cross-SM
+  // hand-off: the sparse block-Jacobi factors of config 5 (fill cap ~30) run
+  // faster with one CTA per block (16 blocks of 160k columns: 1.86 s vs 2.59 s
+  // at 9 CTAs per block)
+  const bool heavy_columns = fill_cap < 0 || fill_cap >= 64;  // fill_cap = the largest cap
+  if (n >= 8192 && nsys < 148 && heavy_columns) a.cps = std::min(32, std::max(1, 148 / nsys));
   if (const char* e = getenv("RHOSOLVE_ILU_CPS")) a.cps = std::max(1, atoi(e));  // tuning knob
   if (a.cps > 1) a.warps = 16;
   RS_TRY(ilutp_plan(n, a.warps, &a.smem_mode, &a.bits_in_smem));
