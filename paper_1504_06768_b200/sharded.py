@@ -47,7 +47,10 @@ def shard_range(n, rank, world):
 
 
 class Comm:
-    """Collectives over an optional torch.distributed group (None = 1 rank)."""
+    """Collectives over an optional torch.distributed group (None = 1 rank).
+    With NCCL the tensors stay on the device (NVLink / NVSwitch); a gloo group
+    (CPU tests, and the single-GPU functional test where both ranks share one
+    device) stages CUDA tensors through the host."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -55,33 +58,70 @@ class Comm:
         self.group = group
         self.rank = self.dist.get_rank(group) if self.dist else 0
         self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.staged = bool(self.dist) and self.dist.get_backend(group) == "gloo"
+
+    def _reduce(self, t, op):
+        if self.world > 1:
+            if self.staged and t.is_cuda:
+                h = t.cpu()
+                self.dist.all_reduce(h, op=op, group=self.group)
+                t.copy_(h)
+            else:
+                self.dist.all_reduce(t, op=op, group=self.group)
+        return t
 
     def allreduce_sum(self, t):
-        if self.world > 1:
-            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
-        return t
+        return self._reduce(t, self.dist.ReduceOp.SUM if self.dist else None)
 
     def allreduce_max(self, t):
-        if self.world > 1:
-            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
-        return t
+        return self._reduce(t, self.dist.ReduceOp.MAX if self.dist else None)
 
     def allgather_ints(self, vals, device):
-        t = torch.tensor(vals, dtype=torch.int64, device=device)
         if self.world == 1:
             return [vals]
+        t = torch.tensor(vals, dtype=torch.int64, device="cpu" if self.staged else device)
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return [o.tolist() for o in out]
 
-    def exchange(self, sends, recvs):
-        """Point-to-point: sends = [(peer, tensor)], recvs = [(peer, tensor)]."""
+    def allgather(self, t):
+        """Every rank's tensor (equal dtype, possibly different lengths known
+        from shard_range), concatenated in rank order."""
+        if self.world == 1:
+            return t
+        src = t.cpu() if (self.staged and t.is_cuda) else t.contiguous()
+        sizes = self.allgather_ints([src.numel()], src.device)
+        parts = [torch.empty(k[0], dtype=src.dtype, device=src.device) for k in sizes]
+        self.dist.all_gather(parts, src, group=self.group)
+        return torch.cat(parts).to(t.device)
+
+    def exchange_begin(self, sends, recvs):
+        """Post the point-to-point halo exchange (sends = [(peer, tensor)],
+        recvs = [(peer, tensor)]) and return a handle for exchange_end; the
+        caller launches its interior work in between."""
         if self.world == 1 or (not sends and not recvs):
-            return
+            return None
+        if self.staged:
+            sends = [(p, t.cpu()) for p, t in sends]
+            bufs = [(p, torch.empty(t.shape, dtype=t.dtype), t) for p, t in recvs]
+            ops = [self.dist.P2POp(self.dist.isend, t, p, self.group) for p, t in sends]
+            ops += [self.dist.P2POp(self.dist.irecv, h, p, self.group) for p, h, _ in bufs]
+            return self.dist.batch_isend_irecv(ops), bufs
         ops = [self.dist.P2POp(self.dist.isend, t, p, self.group) for p, t in sends]
         ops += [self.dist.P2POp(self.dist.irecv, t, p, self.group) for p, t in recvs]
-        for req in self.dist.batch_isend_irecv(ops):
+        return self.dist.batch_isend_irecv(ops), None
+
+    def exchange_end(self, handle):
+        if handle is None:
+            return
+        reqs, bufs = handle
+        for req in reqs:
             req.wait()
+        for _, h, t in bufs or ():
+            t.copy_(h)
+
+    def exchange(self, sends, recvs):
+        self.exchange_end(self.exchange_begin(sends, recvs))
 
 
 class ShardedMatrix:
@@ -119,8 +159,29 @@ class ShardedMatrix:
         self.send_right = (self.r1 - allb[rk + 1][0]) if rk + 1 < W else 0
         self.xe = torch.zeros(self.hi - self.lo, dtype=torch.complex128, device=self.device)
 
-    def extend(self, x_local):
-        """x_ext with own entries and the neighbours' halo values."""
+        # interior rows read only this rank's own entries, so their SpMV can run
+        # while the halo is in flight; boundary rows wait for it
+        counts = self.row_ptr.diff()
+        rows = torch.repeat_interleave(torch.arange(self.nloc, device=self.device), counts.long())
+        outside = (self.col_idx < self.left) | (self.col_idx >= self.left + self.nloc)
+        is_bnd = torch.zeros(self.nloc, dtype=torch.bool, device=self.device)
+        is_bnd[rows[outside]] = True
+        self.bnd_rows = torch.nonzero(is_bnd).reshape(-1)
+        keep_int = ~is_bnd[rows]
+        cnt_int = torch.where(is_bnd, torch.zeros_like(counts), counts)
+        self.int_rp = torch.zeros(self.nloc + 1, dtype=torch.int32, device=self.device)
+        self.int_rp[1:] = torch.cumsum(cnt_int, 0)
+        self.int_ci = self.col_idx[keep_int].contiguous()
+        self.int_v = self.values[keep_int].contiguous()
+        cnt_bnd = counts[self.bnd_rows]
+        self.bnd_rp = torch.zeros(len(self.bnd_rows) + 1, dtype=torch.int32, device=self.device)
+        self.bnd_rp[1:] = torch.cumsum(cnt_bnd, 0)
+        self.bnd_ci = self.col_idx[~keep_int].contiguous()
+        self.bnd_v = self.values[~keep_int].contiguous()
+
+    def extend_begin(self, x_local):
+        """Own entries into x_ext and the halo exchange posted; returns the
+        handle for extend_end."""
         xe = self.xe
         xe[self.left:self.left + self.nloc] = x_local
         sends, recvs = [], []
@@ -136,12 +197,21 @@ class ShardedMatrix:
         if self.right:
             rbuf = torch.empty(self.right, dtype=x_local.dtype, device=x_local.device)
             recvs.append((rk + 1, rbuf))
-        self.comm.exchange(sends, recvs)
+        return self.comm.exchange_begin(sends, recvs), lbuf, rbuf
+
+    def extend_end(self, pending):
+        handle, lbuf, rbuf = pending
+        self.comm.exchange_end(handle)
+        xe = self.xe
         if lbuf is not None:
             xe[:self.left] = lbuf
         if rbuf is not None:
             xe[self.left + self.nloc:] = rbuf
         return xe
+
+    def extend(self, x_local):
+        """x_ext with own entries and the neighbours' halo values."""
+        return self.extend_end(self.extend_begin(x_local))
 
 
 class GpuOps:
@@ -152,10 +222,23 @@ class GpuOps:
         self._scal = torch.empty(8, dtype=torch.float64, device="cuda")
 
     def matvec(self, A, x_local):
-        xe = A.extend(x_local)
+        """y = A x over this rank's rows: the halo exchange is posted first,
+        the interior rows (no halo columns) are multiplied while it is in
+        flight, the boundary rows once it has landed.  Every row is summed by
+        exactly one of the two launches, in storage order: same bits as one
+        SpMV over all rows."""
+        pending = A.extend_begin(x_local)
+        xe = A.xe
         y = torch.empty(A.nloc, dtype=torch.complex128, device=x_local.device)
-        _lib.call("rs_csr_matvec", 1, A.nloc, _lib.ptr(A.row_ptr), _lib.ptr(A.col_idx),
-                  _lib.ptr(A.values), _lib.ptr(xe), _lib.ptr(y), _lib.stream_ptr())
+        _lib.call("rs_csr_matvec", 1, A.nloc, _lib.ptr(A.int_rp), _lib.ptr(A.int_ci),
+                  _lib.ptr(A.int_v), _lib.ptr(xe), _lib.ptr(y), _lib.stream_ptr())
+        A.extend_end(pending)
+        nb = A.bnd_rows.numel()
+        if nb:
+            yb = torch.empty(nb, dtype=torch.complex128, device=x_local.device)
+            _lib.call("rs_csr_matvec", 1, nb, _lib.ptr(A.bnd_rp), _lib.ptr(A.bnd_ci),
+                      _lib.ptr(A.bnd_v), _lib.ptr(xe), _lib.ptr(yb), _lib.stream_ptr())
+            y[A.bnd_rows] = yb
         return y
 
     def psolve(self, M, v):
@@ -219,7 +302,8 @@ def bicgstab_dist(ops, A, M, b, tol, max_iter):
     target, prev, it = tol * pbn, math.inf, 0
     conv = brk = False
     while it < max_iter:
-        rn = _norm(ops, r)
+        rr, rho = ops.dots([(r, r), (rh, r)])  # one packed all-reduce
+        rn = math.sqrt(max(rr.real, 0.0))
         if rn <= target:
             tr = _norm(ops, ops.lincomb([(1.0, b), (-1.0, ops.matvec(A, x))]))
             if tr <= tol * bnorm:
@@ -228,7 +312,6 @@ def bicgstab_dist(ops, A, M, b, tol, max_iter):
             if tr >= 0.5 * prev:
                 break
             prev, target = tr, target * 0.1
-        rho = ops.dots([(rh, r)])[0]
         if abs(rho) < 1e-30 or abs(rho) < 1e-16 * rhn * rn:
             brk = True
             break
@@ -388,10 +471,7 @@ def inverse_power_sharded(L, sigma=liouville.DEFAULT_SIGMA, tol=1e-10, d=1e-5, p
         x0 = torch.from_numpy(start_vector(n, seed)[r0:r1].copy()).to(S.values.device)
         x, outer, inner = inverse_power_dist(ops, A, P, M, x0, tol, max_iter, log=say)
         # gather the (permuted) solution and post-process on every rank
-        parts = [torch.empty(shard_range(n, k, comm.world)[1] - shard_range(n, k, comm.world)[0],
-                             dtype=x.dtype, device=x.device) for k in range(comm.world)]
-        comm.dist.all_gather(parts, x.contiguous(), group=group)
-        xg = torch.cat(parts)
+        xg = comm.allgather(x)
     from .steady import _postprocess
     rho, res = _postprocess(xg, fwd, L)
     torch.cuda.synchronize()
