@@ -135,3 +135,20 @@ def test_c3_solve_direct(cuda):
     res = steady.solve_direct(L, ordering_name="rcm")
     assert res.residual <= 1e-10
     assert O.trace_distance(res.rho, g["power_bicgstab_rho"]) <= 1e-6
+
+
+def test_c4_two_shards_equal_one_batch(cuda):
+    """The N-GPU sweep is the 1-GPU sweep cut into contiguous shards: solving
+    two shards separately gives, system by system, the bits of the one batch."""
+    idx = list(range(248, 264))
+    models = [model("c4", i=i) for i in idx]
+    kw = dict(tol=1e-12, inner="direct", ordering_name="rcm")
+    whole = steady.inverse_power_batch(liouville.build_liouvillian_batch(models),
+                                       [2 + i for i in idx], **kw)
+    halves = []
+    for lo in (0, 8):
+        L = liouville.build_liouvillian_batch(models[lo:lo + 8])
+        halves += steady.inverse_power_batch(L, [2 + i for i in idx[lo:lo + 8]], **kw)
+    for a, b in zip(whole, halves):
+        assert a.error is None and b.error is None
+        assert bits_equal(a.rho, b.rho) and a.iterations == b.iterations

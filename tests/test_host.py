@@ -107,3 +107,20 @@ def test_batch_start_vectors_match_reference_draw(m):
     got = steady._start_vectors(1600, seeds, pin=False).numpy()
     ref = np.concatenate([steady.start_vector(1600, s) for s in seeds])
     assert bits_equal(got, ref)
+
+
+def test_bench_c4_shards_cover_the_sweep():
+    """bench.py's instance sharding (config 4): contiguous, disjoint, complete
+    for every world size the driver uses, detunings and seeds kept."""
+    import bench
+    for world in (1, 2, 4, 8):
+        parts = [list(bench.shard(r, world)) for r in range(world)]
+        assert sum(parts, []) == list(range(bench.SWEEP))
+        assert {len(p) for p in parts} == {bench.SWEEP // world}
+    idx, models = bench.build_inputs("c4", rank=1, world=2)
+    assert idx[0] == 256 and len(models) == 256
+    dets = configs.jc_sweep_detunings()
+    H, _ = models[0]
+    H0, _ = configs.jc_sweep(256)
+    assert bits_equal(H.matrix.values, H0.matrix.values)
+    assert dets[256] == np.linspace(-3.0, 3.0, 512)[256]
