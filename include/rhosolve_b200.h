@@ -332,7 +332,8 @@ typedef struct rs_solver_args {
   int32_t n;
   int32_t nsys;
   int32_t mode;    /* rs_solve_mode */
-  int32_t threads; /* CTA size, multiple of 32 (0 = default 512) */
+  int32_t threads; /* CTA size, multiple of 32, <= 512 (0 = 512; the Python layer
+                      passes 128 for batches of more than 148 systems, else 256) */
   /* solver-ready (shifted or modified), ordered system matrix */
   const int32_t* A_rp;
   const int32_t* A_ci;

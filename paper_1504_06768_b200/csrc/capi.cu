@@ -83,15 +83,16 @@ int rs_abi_version(void) { return RS_ABI_VERSION; }
 // returning them to the OS at every synchronisation: the solve path
 // allocates and frees its scratch every call.
 static int keep_pool_memory() {
-  static int done = 0;
-  if (done) return RS_OK;
+  static std::atomic<unsigned long long> done{0};  // one bit per device
   int dev;
   RS_CUDA_TRY(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_relaxed) & bit) return RS_OK;
   cudaMemPool_t pool;
   RS_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
   unsigned long long thr = ~0ull;
   RS_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-  done = 1;
+  done.fetch_or(bit, std::memory_order_relaxed);
   return RS_OK;
 }
 const char* rs_last_error(void) { return g_err; }

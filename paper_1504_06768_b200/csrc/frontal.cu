@@ -45,6 +45,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -984,9 +986,9 @@ __global__ void __launch_bounds__(FT) frontal_finish_kernel(FrontArgs a) {
 
 // tuning: enable the per-phase clock probe of CTA 0; read the last run's
 // cycles per step of phases A, B, C, D
-static bool g_probe_host = false;
+static std::atomic<bool> g_probe_host{false};
 int frontal_probe(int enable, double* out4) {
-  g_probe_host = enable != 0;
+  g_probe_host.store(enable != 0);
   RS_CUDA_TRY(cudaMemcpyToSymbol(g_fprobe_on, &enable, sizeof(int)));
   {
     const char* e = getenv("RHOSOLVE_FRONTAL_DEBUG");
@@ -1004,8 +1006,8 @@ int frontal_probe(int enable, double* out4) {
   return RS_OK;
 }
 
-static int g_frontal_taken = 0;  // systems accepted by the last frontal_factor
-int frontal_last_taken() { return g_frontal_taken; }
+static std::atomic<int> g_frontal_taken{0};  // systems accepted by the last frontal_factor
+int frontal_last_taken() { return g_frontal_taken.load(std::memory_order_relaxed); }
 
 // Selection (RHOSOLVE_FRONTAL: 1 always, 0 never, unset auto).  Auto takes
 // batches of at most three waves (B <= 3 x SMs): measured on the c4 systems
@@ -1014,7 +1016,7 @@ int frontal_last_taken() { return g_frontal_taken; }
 // 8.8 ms); on the 512-system batch (a partial fourth wave) it is level
 // (typically 28.9 vs 29.5 ms, with slower outliers), see DESIGN.md.
 bool frontal_enabled(int nsys) {
-  g_frontal_taken = 0;
+  g_frontal_taken.store(0, std::memory_order_relaxed);
   const char* e = getenv("RHOSOLVE_FRONTAL");
   if (e && e[0] == '1') return true;
   if (e && e[0] == '0') return false;
@@ -1028,7 +1030,7 @@ bool frontal_enabled(int nsys) {
 // keep state 0 for the pipelined kernel.
 int frontal_factor(const FactorArgs& fa, cudaStream_t st) {
   const int n = fa.n, B = fa.B;
-  g_frontal_taken = 0;
+  g_frontal_taken.store(0, std::memory_order_relaxed);
   if (B == 0 || n == 0 || n > MAXN || fa.q) return RS_OK;
   const int64_t N = (int64_t)B * n, N1 = (int64_t)B * (n + 1);
   int32_t nnz_all = 0;
@@ -1048,7 +1050,17 @@ int frontal_factor(const FactorArgs& fa, cudaStream_t st) {
   RS_CUDA_TRY(cudaStreamSynchronize(st));
   const size_t o_eent = take(4 * (size_t)nnz_all), o_eval = take(16 * (size_t)nnz_all);
   unsigned char* ws = nullptr;
+  // released on every exit (error paths included)
+  struct PoolGuard {
+    cudaStream_t st;
+    void* p[2] = {nullptr, nullptr};
+    ~PoolGuard() {
+      for (void* q : p)
+        if (q) cudaFreeAsync(q, st);
+    }
+  } guard{st};
   RS_CUDA_TRY(cudaMallocAsync(&ws, bytes, st));
+  guard.p[0] = ws;
   FrontWs w{};
   w.n = n;
   w.B = B;
@@ -1106,15 +1118,13 @@ int frontal_factor(const FactorArgs& fa, cudaStream_t st) {
     ustride = std::max<int64_t>(ustride, I[I_UB]);
     ++any;
   }
-  g_frontal_taken = any;
-  if (!any) {
-    cudaFreeAsync(ws, st);
-    return RS_OK;
-  }
+  g_frontal_taken.store(any, std::memory_order_relaxed);
+  if (!any) return RS_OK;
   if (changed)
     RS_CUDA_TRY(cudaMemcpyAsync(w.info, info.data(), 4 * info.size(), cudaMemcpyHostToDevice, st));
   unsigned char* us = nullptr;
   RS_CUDA_TRY(cudaMallocAsync(&us, (size_t)B * ustride * 20 + 256, st));
+  guard.p[1] = us;
   FrontArgs a{};
   a.n = n;
   a.B = B;
@@ -1146,15 +1156,13 @@ int frontal_factor(const FactorArgs& fa, cudaStream_t st) {
   a.capU = fa.capU;
   a.pinv = fa.pinv;
   a.state = fa.state;
-  auto kern = g_probe_host ? frontal_lu_kernel<true> : frontal_lu_kernel<false>;
+  auto kern = g_probe_host.load() ? frontal_lu_kernel<true> : frontal_lu_kernel<false>;
   RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<B, FT, smem, st>>>(a);
   ::rs::count_launch();
   frontal_finish_kernel<<<B, FT, 0, st>>>(a);
   ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
-  cudaFreeAsync(us, st);
-  cudaFreeAsync(ws, st);
   return RS_OK;
 }
 
