@@ -165,6 +165,7 @@ __device__ __forceinline__ void sweep_slice(const TriSell& T, int32_t s, const d
       }
     }
   }
+  if (tt && g_slice_clock_mode) tt[3 * (int64_t)s] = (unsigned long long)(clock64() - ck_seen);
   if (row >= 0 && lane % G == 0) {
     if (UPPER) acc = cmul_plain(acc, rdv);
     cta::vst2(out + row, acc);

@@ -81,7 +81,8 @@ def timeline(n="20000"):
     lib.rs_debug_slice_clock_mode(0)
     c = buf.cpu().numpy().reshape(ns, 3).astype(np.float64)
     print(f"clock64: key seen -> sources loaded median {np.median(c[1:, 1]):.0f} cycles; "
-          f"loaded -> published median {np.median(c[1:, 2]):.0f} cycles")
+          f"loaded -> folded median {np.median(c[1:, 0]):.0f}; loaded -> published median "
+          f"{np.median(c[1:, 2]):.0f} cycles")
     for s in (1000, 1001, 1002, 1003):
         print(f"  slice {s}: start {t[s, 0]:.0f} seen {t[s, 1]:.0f} end {t[s, 2]:.0f} (prev end {t[s - 1, 2]:.0f})")
 
