@@ -131,8 +131,8 @@ def kernel_timings_c5(L, skw, torch):
     nLU = int(np.sum(M.lnnz) + np.sum(M.unnz))
     out["factorize"] = {"seconds": fact_s, "bytes": 20 * nnz + 20 * nLU + 8 * (n + blocks),
                         "kernel": "ilutp_pipeline_kernel",
-                        "note": f"{blocks} block-Jacobi blocks of {n // blocks} rows, multi-CTA "
-                                "column pipeline (transpose, row norms, factorization)"}
+                        "note": f"{blocks} block-Jacobi blocks of {n // blocks} rows, one CTA per "
+                                "block (transpose, row norms, column-pipelined ILUTP)"}
     x = torch.randn(n, dtype=torch.complex128, device="cuda")
     y = torch.empty_like(x)
 

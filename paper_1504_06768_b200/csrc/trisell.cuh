@@ -66,6 +66,7 @@ __device__ __forceinline__ void fold_step(double2& acc, double2 p, int r, unsign
     for (int sh = G; sh < 32; sh <<= 1) m |= m >> sh;
     m &= (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
     const int cnt = 32 - __clz(m);  // lane positions 0 .. cnt-1 of a row are in use
+#pragma unroll 1
     for (int j = 0; j < cnt; ++j) {
       const double px = __shfl_sync(FULL, p.x, r * G + j);
       const double py = __shfl_sync(FULL, p.y, r * G + j);
@@ -107,11 +108,11 @@ __device__ __forceinline__ void sweep_slice(const TriSell& T, int32_t s, const d
   if (T.mode == 1) {  // tuning: serialize the whole slice behind its latest dependency
     for (int32_t k0 = 0; k0 < w; k0 += KREG) {
       const int32_t key = __ldg(keys + k0 / KREG);
-      if (key >= 0 && lane == 0)
-        while (!cta::is_ready(cta::vld2(out + key))) {
-        }
+      if (key >= 0) {
+        double2 kv = cta::vld2(out + key);
+        while (!__all_sync(0xffffffffu, cta::is_ready(kv))) kv = cta::vld2(out + key);
+      }
     }
-    __syncwarp();
   }
   long long ck_seen = 0;
   for (int32_t k0 = 0; k0 < w; k0 += KREG) {
@@ -126,18 +127,21 @@ __device__ __forceinline__ void sweep_slice(const TriSell& T, int32_t s, const d
       }
     }
     {
-      // One lane watches this chunk's latest dependency (highest level) while
+      // The warp watches this chunk's latest dependency (highest level) while
       // the entry loads above are in flight; when it is published the chunk's
       // other sources almost always are.  Early chunks hold the oldest
       // sources, so they are folded long before the chain arrives and only
       // the last chunk sits on the critical path.  (Polling every source from
       // every waiting lane -- 1,184 warps x 32 lanes x 8 loads on config 5 --
       // saturates L2 and stretches a dependency hop to ~16 us.)
+      // Every lane loads the same address (one broadcast request per poll) and
+      // the loop is warp-uniform: a lone polling lane with the other 31 parked
+      // at a __syncwarp cost ~2,000 cycles of re-convergence per hop.
       const int32_t key = __ldg(keys + k0 / KREG);
-      if (key >= 0 && lane == 0)
-        while (!cta::is_ready(cta::vld2(out + key))) {
-        }
-      __syncwarp();
+      if (key >= 0) {
+        double2 kv = cta::vld2(out + key);
+        while (!__all_sync(0xffffffffu, cta::is_ready(kv))) kv = cta::vld2(out + key);
+      }
     }
     const long long ck0 = (tt && g_slice_clock_mode) ? clock64() : 0;
     unsigned pend = 0;
@@ -147,7 +151,7 @@ __device__ __forceinline__ void sweep_slice(const TriSell& T, int32_t s, const d
 #pragma unroll
     for (int k = 0; k < KREG; ++k)
       if (c[k] >= 0 && !cta::is_ready(y[k])) pend |= 1u << k;
-    while (pend) {
+    while (__any_sync(0xffffffffu, pend != 0)) {  // warp-uniform: stragglers only
 #pragma unroll
       for (int k = 0; k < KREG; ++k)
         if ((pend >> k) & 1u) y[k] = cta::vld2(out + c[k]);
