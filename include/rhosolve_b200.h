@@ -189,6 +189,17 @@ int rs_lu_solve_cols(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t
                      const int32_t* Us_meta, const rs_complex* Us_rd, const rs_complex* b,
                      rs_complex* x, void* stream);
 
+/* rs_lu_solve_cols with the factors' reach (max |row - column| over the entries
+ * of L and U; see rs_solver_args.col_reach) so that a system too large for
+ * shared memory sweeps through the sliding window.  reach = 0: rs_lu_solve_cols. */
+int rs_lu_solve_cols_reach(int32_t nsys, int32_t n, const int32_t* pinv,
+                           const int32_t* Ls_rowoff, const int32_t* Ls_idx,
+                           const rs_complex* Ls_val, const int32_t* Ls_meta,
+                           const int32_t* Us_rowoff, const int32_t* Us_idx,
+                           const rs_complex* Us_val, const int32_t* Us_meta,
+                           const rs_complex* Us_rd, const rs_complex* b, rs_complex* x,
+                           int32_t reach, void* stream);
+
 /* x = M^{-1} b through the factors: y[pinv] = b; lower_solve; upper_solve;
  * x = y.  Replaces factor.solve_lu (factor.py:137-149) with
  * lower_solve/upper_solve (_ckernels.pyx:53-85); bit-identical. */
@@ -391,6 +402,11 @@ typedef struct rs_solver_args {
   double* trace;
   int32_t* trace_count;
   int32_t trace_cap;
+  /* optional: max |row - column| over the entries of both factors (their
+   * bandwidth in pivotal coordinates; 0 = unknown).  A lone system too large
+   * for shared memory then sweeps through a sliding shared-memory window with
+   * several consumer warps instead of through global memory. */
+  int32_t col_reach;
 } rs_solver_args;
 
 /* One launch runs the whole solve of every system on the device. */

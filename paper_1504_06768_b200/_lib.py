@@ -65,7 +65,8 @@ class SolverArgs(ctypes.Structure):
                 ("Ls_rowoff", _vp), ("Ls_idx", _vp), ("Ls_val", _vp), ("Ls_meta", _vp),
                 ("Us_rowoff", _vp), ("Us_idx", _vp), ("Us_val", _vp), ("Us_meta", _vp),
                 ("Us_rd", _vp), ("colp", _vp), ("skip", _vp),
-                ("trace", _vp), ("trace_count", _vp), ("trace_cap", _i32)]
+                ("trace", _vp), ("trace_count", _vp), ("trace_cap", _i32),
+                ("col_reach", _i32)]
 
 
 class TriFactor(ctypes.Structure):
@@ -102,6 +103,8 @@ _SIGS = {
                             _vp, ctypes.POINTER(_i64), _vp],
     "rs_lu_solve_cols": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp, _vp],
+    "rs_lu_solve_cols_reach": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                               _vp, _i32, _vp],
     "rs_lu_solve": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "rs_tri_levels": [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_i64), _vp],
     "rs_tri_order": [_i32, _i32, _vp, _vp, _i64, _i32, _vp, ctypes.POINTER(_i64), _vp],

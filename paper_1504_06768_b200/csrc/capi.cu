@@ -443,9 +443,21 @@ int rs_lu_solve_cols(int32_t nsys, int32_t n, const int32_t* pinv, const int32_t
                      const int32_t* Us_rowoff, const int32_t* Us_idx, const rs_complex* Us_val,
                      const int32_t* Us_meta, const rs_complex* Us_rd, const rs_complex* b,
                      rs_complex* x, void* stream) {
-  RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
+  return rs_lu_solve_cols_reach(nsys, n, pinv, Ls_rowoff, Ls_idx, Ls_val, Ls_meta, Us_rowoff,
+                                Us_idx, Us_val, Us_meta, Us_rd, b, x, 0, stream);
+}
+
+int rs_lu_solve_cols_reach(int32_t nsys, int32_t n, const int32_t* pinv,
+                           const int32_t* Ls_rowoff, const int32_t* Ls_idx,
+                           const rs_complex* Ls_val, const int32_t* Ls_meta,
+                           const int32_t* Us_rowoff, const int32_t* Us_idx,
+                           const rs_complex* Us_val, const int32_t* Us_meta,
+                           const rs_complex* Us_rd, const rs_complex* b, rs_complex* x,
+                           int32_t reach, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0 && reach >= 0, "negative size");
   if (!nsys || !n) return RS_OK;
   SolverArgs a{};
+  a.col_reach = reach;
   a.n = n;
   a.B = nsys;
   a.Lso = Ls_rowoff;
@@ -638,6 +650,7 @@ int rs_steady_solve(const rs_solver_args* p, void* stream) {
   a.want_condest = p->want_condest;
   a.colp = p->colp;
   a.skip = p->skip;
+  a.col_reach = p->col_reach;
   a.trace = p->trace;
   a.trace_count = p->trace_count;
   a.trace_cap = p->trace_cap;

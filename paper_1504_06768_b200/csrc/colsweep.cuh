@@ -333,24 +333,203 @@ __device__ __forceinline__ void col_consume(int n, int rows, const ColRing& g, d
   }
 }
 
+// Several consumer warps for long columns (config 3: ~175 entries per L / U
+// column = 3 stream rows).  The rows of ONE column update distinct entries of
+// y, so up to W of them are applied by W warps at once; columns stay strictly
+// ordered by a named barrier among the consumers (which also orders their y
+// accesses: same CTA), so every y[i] still receives its subtractions in column
+// order -- bit-identical.  Per group: the consumers read the next W ring
+// slots' sequence words, take g = the leading rows that belong to the current
+// column (the first row plus its continuations, at most W), warp j < g applies
+// row r + j, all meet at the barrier, r += g.
+template <bool UPPER, typename AT>
+__device__ __forceinline__ void col_consume_multi(int n, int rows, const ColRing& g, double2* y,
+                                                  int W, int widx) {
+  using M = YMem<AT>;
+  const int lane = threadIdx.x & 31;
+  const AT yb = M::base(y), dummy = yb + (AT)16 * (AT)n;
+  int c = UPPER ? n : -1;
+  double2 xc = make_double2(0.0, 0.0);
+  int r = 0;
+  while (r < rows) {
+    // the next W rows staged?  lane j watches row r + j
+    int sq;
+    while (true) {
+      const int rr = r + lane;
+      sq = (lane < W && rr < rows) ? ld_acq(g.seq + (rr & (g.S - 1))) : ((rr << 1) | 0);
+      const bool ok = lane >= W || rr >= rows || (sq >> 1) == rr;
+      if (__all_sync(FULL, ok)) break;
+    }
+    // group size: row r, then continuation rows
+    const unsigned contm = __ballot_sync(FULL, lane < W && r + lane < rows && (sq & 1)) & ~1u;
+    const int avail = min(W, rows - r);
+    int gsz = 1;
+    while (gsz < avail && ((contm >> gsz) & 1u)) ++gsz;
+    const int cont0 = __shfl_sync(FULL, sq, 0) & 1;
+    // the column of this group (uniform across the consumers)
+    if (!cont0) {
+      c += UPPER ? -1 : 1;
+      double2 xn = M::ld(yb + (AT)16 * (AT)c);
+      if (UPPER) xn = cmul_plain(xn, g.rd[r & (g.S - 1)]);
+      xc = xn;
+    }
+    if (widx < gsz) {
+      const int slot = (r + widx) & (g.S - 1);
+      const int i0 = g.idx[CW * slot + lane], i1 = g.idx[CW * slot + 32 + lane];
+      const double2 v0 = g.val[CW * slot + lane], v1 = g.val[CW * slot + 32 + lane];
+      const AT a0 = i0 >= 0 ? yb + (AT)16 * (AT)i0 : dummy;
+      const AT a1 = i1 >= 0 ? yb + (AT)16 * (AT)i1 : dummy;
+      const double2 y0 = M::ld(a0), y1 = M::ld(a1);
+      M::st(a0, csub(y0, cmul_plain(v0, xc)));
+      M::st(a1, csub(y1, cmul_plain(v1, xc)));
+    }
+    r += gsz;
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * W) : "memory");
+    // U: the solved entry replaces y[c] once every consumer has read the
+    // unsolved one (no row of this or a later column targets it)
+    if (UPPER && !cont0 && widx == 0 && lane == 0) M::st(yb + (AT)16 * (AT)c, xc);
+    if (widx == 0 && lane == 0) st_rlx(g.head, r);
+  }
+}
+
+// A sliding shared-memory window over a sweep vector that is too large for
+// shared memory (config 3: n = 57,600).  Column c only touches rows within
+// `reach` of it (the factor's bandwidth in pivotal coordinates), so a window
+// of WIN = 2^k >= reach + panel + 1 rows, addressed modulo WIN, holds every
+// row a panel of columns can touch; at a panel boundary the rows that can no
+// longer be touched go back to global memory and the same slots receive the
+// rows that enter.  With several consumer warps the global vector would be
+// re-read from L2 on every step (each warp's stores invalidate the others'
+// L1 lines: 650 ns per column group measured); in the window a step costs
+// shared-memory latency.
+struct YWindow {
+  double2* s;   // [WIN + 1] shared (slot WIN: dummy for padding entries)
+  double2* g;   // the whole vector in global memory
+  int mask;     // WIN - 1
+  int panel;    // columns per panel = WIN - reach - 1
+};
+
+template <bool UPPER>
+__device__ __forceinline__ void col_consume_win(int n, int rows, const ColRing& g,
+                                                const YWindow& w, int W, int widx) {
+  const int lane = threadIdx.x & 31;
+  const int ct = widx * 32 + lane, cn = 32 * W;  // consumer thread index / count
+  const int WIN = w.mask + 1;
+  const unsigned sb = saddr(w.s), dummy = sb + 16u * (unsigned)WIN;
+  auto bar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(32 * W) : "memory"); };
+  // window: L covers rows [edge, edge + WIN), U covers (edge - WIN, edge]
+  int edge = UPPER ? n - 1 : 0;
+  if (!UPPER) {
+    for (int j = ct; j < min(WIN, n); j += cn) w.s[j & w.mask] = w.g[j];
+  } else {
+    for (int j = n - 1 - ct; j >= 0 && j > n - 1 - WIN; j -= cn) w.s[j & w.mask] = w.g[j];
+  }
+  bar();
+  int c = UPPER ? n : -1;
+  double2 xc = make_double2(0.0, 0.0);
+  int r = 0;
+  while (r < rows) {
+    int sq;
+    while (true) {
+      const int rr = r + lane;
+      sq = (lane < W && rr < rows) ? ld_acq(g.seq + (rr & (g.S - 1))) : ((rr << 1) | 0);
+      const bool ok = lane >= W || rr >= rows || (sq >> 1) == rr;
+      if (__all_sync(FULL, ok)) break;
+    }
+    const unsigned contm = __ballot_sync(FULL, lane < W && r + lane < rows && (sq & 1)) & ~1u;
+    const int avail = min(W, rows - r);
+    int gsz = 1;
+    while (gsz < avail && ((contm >> gsz) & 1u)) ++gsz;
+    const int cont0 = __shfl_sync(FULL, sq, 0) & 1;
+    if (!cont0) {
+      c += UPPER ? -1 : 1;
+      // panel boundary: every update of the leaving rows is behind the last
+      // barrier; swap them for the entering rows, slot for slot
+      if (!UPPER && c >= edge + w.panel) {
+        for (int j = edge + ct; j < edge + w.panel; j += cn) {
+          w.g[j] = w.s[j & w.mask];
+          if (j + WIN < n) w.s[j & w.mask] = w.g[j + WIN];
+        }
+        edge += w.panel;
+        bar();
+      } else if (UPPER && c <= edge - w.panel) {
+        for (int j = edge - ct; j > edge - w.panel; j -= cn) {
+          w.g[j] = w.s[j & w.mask];
+          if (j - WIN >= 0) w.s[j & w.mask] = w.g[j - WIN];
+        }
+        edge -= w.panel;
+        bar();
+      }
+      double2 xn = lds2(sb + 16u * (unsigned)(c & w.mask));
+      if (UPPER) xn = cmul_plain(xn, g.rd[r & (g.S - 1)]);
+      xc = xn;
+    }
+    if (widx < gsz) {
+      const int slot = (r + widx) & (g.S - 1);
+      const int i0 = g.idx[CW * slot + lane], i1 = g.idx[CW * slot + 32 + lane];
+      const double2 v0 = g.val[CW * slot + lane], v1 = g.val[CW * slot + 32 + lane];
+      const unsigned a0 = i0 >= 0 ? sb + 16u * (unsigned)(i0 & w.mask) : dummy;
+      const unsigned a1 = i1 >= 0 ? sb + 16u * (unsigned)(i1 & w.mask) : dummy;
+      const double2 y0 = lds2(a0), y1 = lds2(a1);
+      sts2(a0, csub(y0, cmul_plain(v0, xc)));
+      sts2(a1, csub(y1, cmul_plain(v1, xc)));
+    }
+    r += gsz;
+    bar();
+    if (UPPER && !cont0 && widx == 0 && lane == 0) sts2(sb + 16u * (unsigned)(c & w.mask), xc);
+    if (widx == 0 && lane == 0) st_rlx(g.head, r);
+  }
+  bar();
+  // what is still in the window goes back
+  if (!UPPER) {
+    for (int j = edge + ct; j < min(edge + WIN, n); j += cn) w.g[j] = w.s[j & w.mask];
+  } else {
+    for (int j = edge - ct; j >= 0 && j > edge - WIN; j -= cn) w.g[j] = w.s[j & w.mask];
+  }
+}
+
 // CTA-level in-place M^{-1} sweeps on y (shared memory): warp 0 consumes,
 // warps 1..P produce.  Must be called by all threads (contains
-// __syncthreads).
+// __syncthreads).  consumers > 1 (long columns, lone large systems): warps
+// 0..consumers-1 consume together (col_consume_multi), the rest produce.
 template <typename AT>
 __device__ __forceinline__ void col_lu_sweeps(int n, const ColStream& Ls, const ColStream& Us,
-                                              const ColRing& g, double2* y) {
+                                              const ColRing& g, double2* y, int consumers = 1,
+                                              const YWindow* win = nullptr) {
   const int wid = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  const int P = max(1, min(nw - 1, 8));
+  const int W = max(1, min(consumers, nw - 1));
+  const int P = max(1, min(nw - W, 8));
   col_ring_reset(g);
   __syncthreads();
-  if (wid == 0) col_consume<false, AT>(n, Ls.rows, g, y);
-  else if (wid <= P) col_ring_produce(g, Ls, false, wid - 1, P);
+  if (win) {  // y in global memory behind a sliding shared-memory window
+    if (wid < W) col_consume_win<false>(n, Ls.rows, g, *win, W, wid);
+    else if (wid < W + P) col_ring_produce(g, Ls, false, wid - W, P);
+    __syncthreads();
+    col_ring_reset(g);
+    __syncthreads();
+    if (wid < W) col_consume_win<true>(n, Us.rows, g, *win, W, wid);
+    else if (wid < W + P) col_ring_produce(g, Us, true, wid - W, P);
+    __syncthreads();
+    return;
+  }
+  if (W == 1) {
+    if (wid == 0) col_consume<false, AT>(n, Ls.rows, g, y);
+    else if (wid <= P) col_ring_produce(g, Ls, false, wid - 1, P);
+  } else {
+    if (wid < W) col_consume_multi<false, AT>(n, Ls.rows, g, y, W, wid);
+    else if (wid < W + P) col_ring_produce(g, Ls, false, wid - W, P);
+  }
   __syncthreads();
   col_ring_reset(g);
   __syncthreads();
-  if (wid == 0) col_consume<true, AT>(n, Us.rows, g, y);
-  else if (wid <= P) col_ring_produce(g, Us, true, wid - 1, P);
+  if (W == 1) {
+    if (wid == 0) col_consume<true, AT>(n, Us.rows, g, y);
+    else if (wid <= P) col_ring_produce(g, Us, true, wid - 1, P);
+  } else {
+    if (wid < W) col_consume_multi<true, AT>(n, Us.rows, g, y, W, wid);
+    else if (wid < W + P) col_ring_produce(g, Us, true, wid - W, P);
+  }
   __syncthreads();
 }
 

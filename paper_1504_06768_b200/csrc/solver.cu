@@ -13,6 +13,10 @@
 // memory and no scalar crosses to the host until the solve ends, so a solve
 // costs one launch.  A batch of B independent systems (config-4 sweep) is a
 // grid of B CTAs.
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 #include "colsweep.cuh"
 #include "kernels.cuh"
@@ -106,9 +110,21 @@ __device__ __noinline__ void csc_psolve(const SolverArgs* a, const double2* in, 
   Us.meta = a->Usm + u0;
   Us.rd = a->Usr + u0;
   Us.rows = a->Uso[b * n + n] - u0;
-  const cta::ColRing ring = cta::col_ring_at(smem + (yg ? 0 : cta::col_y_bytes(n)), a->ring_R);
-  if (yg) cta::col_lu_sweeps<unsigned long long>(n, Ls, Us, ring, P);
-  else cta::col_lu_sweeps<unsigned>(n, Ls, Us, ring, P);
+  const int win = yg ? a->col_win : 0;
+  const size_t ybytes = win ? 16 * ((size_t)win + 1) : (yg ? 0 : cta::col_y_bytes(n));
+  const cta::ColRing ring = cta::col_ring_at(smem + ybytes, a->ring_R);
+  if (win) {
+    cta::YWindow w;
+    w.s = reinterpret_cast<double2*>(smem);
+    w.g = P;
+    w.mask = win - 1;
+    w.panel = win - a->col_reach - 1;
+    cta::col_lu_sweeps<unsigned long long>(n, Ls, Us, ring, P, a->col_consumers, &w);
+  } else if (yg) {
+    cta::col_lu_sweeps<unsigned long long>(n, Ls, Us, ring, P, a->col_consumers);
+  } else {
+    cta::col_lu_sweeps<unsigned>(n, Ls, Us, ring, P, a->col_consumers);
+  }
   // x[q] = y (factor.py:147-148) when the factors are column pre-ordered
   const int32_t* colp = a->colp ? a->colp + b * n : nullptr;
   if (colp)
@@ -699,13 +715,40 @@ int64_t solver_work_stride(int32_t n, int restart_m) {
   return (int64_t)n * (2 + small_slots + 9 + (m + 1) + 2);
 }
 
+// Consumer warps of the column sweeps: several for a lone large system whose
+// columns span several 64-entry stream rows (config 3: ~175 entries per
+// column), one otherwise (a batch is bound by systems per SM, and short
+// columns have nothing to share).  RHOSOLVE_COL_CONSUMERS overrides.
+// Sliding window for a lone system whose sweep vector lives in global memory:
+// the largest power of two that fits next to the ring, provided it leaves a
+// panel of at least 64 columns beyond the factors' reach.  0 = no window.
+static int col_window_for(const SolverArgs& a, int max_smem) {
+  if (getenv("RHOSOLVE_COL_WINDOW") && atoi(getenv("RHOSOLVE_COL_WINDOW")) == 0) return 0;
+  if (!a.col_y_global || a.col_reach <= 0 || a.B > 148 || a.ring_R <= 0) return 0;
+  for (int win = 16384; win >= 256; win >>= 1) {
+    if (16 * ((size_t)win + 1) + cta::col_ring_bytes(a.ring_R) + 4096 > (size_t)max_smem) continue;
+    return win - a.col_reach - 1 >= 64 ? win : 0;
+  }
+  return 0;
+}
+
+static int col_consumers_for(const SolverArgs& a) {
+  if (const char* e = getenv("RHOSOLVE_COL_CONSUMERS")) return std::max(1, atoi(e));
+  if (a.ring_R <= 0 || a.B > 148 || !a.Lso || !a.Uso) return 1;
+  // measured on config 3 (apply, ms): global y 81 / 75 / 68 for 1 / 4 / 6 consumers,
+  // sliding window 101 / 67 / 51 / 46 for 1 / 2 / 4 / 6
+  return a.col_y_global ? 6 : 1;
+}
+
 int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
   if (a.B == 0) return RS_OK;
   int dev, max_smem;
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int win = col_window_for(a, max_smem);
   size_t smem = a.ring_R > 0
-                    ? (a.col_y_global ? 0 : cta::col_y_bytes(a.n)) + cta::col_ring_bytes(a.ring_R)
+                    ? (win ? 16 * ((size_t)win + 1) : (a.col_y_global ? 0 : cta::col_y_bytes(a.n))) +
+                          cta::col_ring_bytes(a.ring_R)
                     : (a.y_in_smem ? 32 * (size_t)a.n : 0);
   if (smem + 2048 > (size_t)max_smem) {
     set_error("steady solver: n=%d needs %zu B of shared memory", a.n, smem);
@@ -717,6 +760,8 @@ int launch_steady_solver(const SolverArgs& a, cudaStream_t st) {
   SolverArgs la = a;
   la.ywork = a.work;  // slot 0 of each system's workspace (y, then y2 = dummy)
   la.ywork_stride = a.work_stride;
+  la.col_consumers = col_consumers_for(a);
+  la.col_win = win;
   SolverArgs* dev_args = nullptr;
   if (la.ring_R > 0) {  // the out-of-line column sweeps read the arguments from here
     RS_CUDA_TRY(cudaMallocAsync(&dev_args, sizeof(SolverArgs), st));
@@ -900,8 +945,10 @@ int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
   RS_CUDA_TRY(cudaGetDevice(&dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int y_smem = 32 * (size_t)a.n + 2048 <= (size_t)max_smem;
+  const int win = col_window_for(a, max_smem);
   size_t smem = a.ring_R > 0
-                    ? (a.col_y_global ? 0 : cta::col_y_bytes(a.n)) + cta::col_ring_bytes(a.ring_R)
+                    ? (win ? 16 * ((size_t)win + 1) : (a.col_y_global ? 0 : cta::col_y_bytes(a.n))) +
+                          cta::col_ring_bytes(a.ring_R)
                     : (y_smem ? 32 * (size_t)a.n : 0);
   if (a.ring_R <= 0 && !y_smem && !a.work) {
     set_error("lu_solve: n=%d needs global scratch", a.n);
@@ -913,6 +960,8 @@ int launch_lu_solve(const SolverArgs& a, cudaStream_t st) {
   SolverArgs la = a;
   la.ywork = a.work;  // 2 n per system: y, then the dummy slot
   la.ywork_stride = 2 * (int64_t)a.n;
+  la.col_consumers = col_consumers_for(a);
+  la.col_win = win;
   SolverArgs* dev_args = nullptr;
   if (la.ring_R > 0) {
     RS_CUDA_TRY(cudaMallocAsync(&dev_args, sizeof(SolverArgs), st));

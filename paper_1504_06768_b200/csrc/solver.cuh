@@ -80,6 +80,9 @@ struct SolverArgs {
   const int32_t* Usm;
   const double2* Usr;
   int32_t ring_R;  // > 0: column sweeps with a ring of ring_R 64-entry slots
+  int32_t col_reach;       // max |row - column| over both factors (0: unknown)
+  int32_t col_win;         // > 0: sliding shared-memory window of this many rows over a global y
+  int32_t col_consumers;   // consumer warps of the column sweeps (> 1: long columns, lone systems)
   int32_t col_y_global;    // column sweeps with the sweep vector in global memory
   double2* ywork;          // global sweep vectors (set by the launcher)
   int64_t ywork_stride;

@@ -25,6 +25,8 @@
 // x[b*n ...].  A CTA can straddle system boundaries; the element offsets at
 // which a new system starts inside the CTA's slice sit in a small shared
 // table.  A single system is B = 1.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -104,7 +106,16 @@ int launch_spmv(int64_t nrows, int32_t n, const int32_t* rp, const int32_t* ci,
   RS_CHECK_ARG(n > 0, "n must be positive");
   // 8 warps x 32 rows per CTA; 4 chunks of 32 products per warp pass
   const unsigned grid = (unsigned)((nrows + 255) / 256);
-  spmv_warp_kernel<4, 4><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y);
+  static const int variant = getenv("RHOSOLVE_SPMV_VARIANT") ? atoi(getenv("RHOSOLVE_SPMV_VARIANT")) : 0;
+  switch (variant) {  // tuning hook (tools/spmv_c5.py); 0 = the measured best
+    case 1: spmv_warp_kernel<4, 5><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y); break;
+    case 2: spmv_warp_kernel<4, 6><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y); break;
+    case 3: spmv_warp_kernel<2, 6><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y); break;
+    case 4: spmv_warp_kernel<2, 8><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y); break;
+    case 5: spmv_warp_kernel<8, 3><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y); break;
+    case 6: spmv_warp_kernel<8, 4><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y); break;
+    default: spmv_warp_kernel<4, 4><<<grid, 256, 0, st>>>(nrows, n, rp, ci, v, x, y); break;
+  }
   ::rs::count_launch();
   RS_CUDA_TRY(cudaGetLastError());
   return RS_OK;

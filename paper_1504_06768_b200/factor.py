@@ -47,7 +47,7 @@ class LUFactors:
     __slots__ = ("n", "nsys", "raw", "capL", "capU", "pinv", "L_rp", "L_ci", "L_v", "U_rp",
                  "U_ci", "U_v", "rdiag", "fill_factors", "complete", "drop_tol",
                  "fill_limit", "fail", "lnnz", "unnz", "ok", "csc", "Ls", "Us", "colp",
-                 "colp_dev", "fail_dev", "solvable", "Llev", "Ulev", "nfloor")
+                 "colp_dev", "fail_dev", "solvable", "Llev", "Ulev", "nfloor", "reach")
 
     def ensure_cols(self):
         """Column streams of L and U for the one-CTA column sweeps
@@ -57,6 +57,16 @@ class LUFactors:
             dev = self.pinv.device
             self.Ls = _col_stream(self.nsys, self.n, 0, Lp, Li, Lx, self.capL, None, dev)
             self.Us = _col_stream(self.nsys, self.n, 1, Up, Ui, Ux, self.capU, self.rdiag, dev)
+            if self.nsys == 1 and self.ok:
+                # the factors' bandwidth in pivotal coordinates: what a column
+                # can touch (sliding-window sweeps of large lone systems)
+                n = self.n
+                cols = torch.arange(n, device=dev, dtype=torch.int32)
+                lc = torch.repeat_interleave(cols, Lp[:n + 1].diff())
+                uc = torch.repeat_interleave(cols, Up[:n + 1].diff())
+                rl = int((Li[:lc.numel()] - lc).abs().max().item()) if lc.numel() else 0
+                ru = int((Ui[:uc.numel()] - uc).abs().max().item()) if uc.numel() else 0
+                self.reach = max(rl, ru, 1)
         return self
 
     def ensure_rows(self):
@@ -224,6 +234,7 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None, eag
     # larger systems use the row-oriented copy
     f.csc = bool(_lib.load().rs_col_sweep_supported(n))
     f.Ls = f.Us = None
+    f.reach = 0
     f.Llev = f.Ulev = None
     f.colp = f.colp_dev = None
     # a batch with some failed systems can still be solved on the column-sweep
@@ -450,9 +461,10 @@ def _solve_lu_rows(f, b):
     if f.csc:
         f.ensure_cols()
         (lo, li, lv, lm, _), (uo, ui, uv, um, ur) = f.Ls, f.Us
-        _lib.call("rs_lu_solve_cols", f.nsys, f.n, _lib.ptr(f.pinv), _lib.ptr(lo), _lib.ptr(li),
-                  _lib.ptr(lv), _lib.ptr(lm), _lib.ptr(uo), _lib.ptr(ui), _lib.ptr(uv),
-                  _lib.ptr(um), _lib.ptr(ur), _lib.ptr(b), _lib.ptr(x), _lib.stream_ptr())
+        _lib.call("rs_lu_solve_cols_reach", f.nsys, f.n, _lib.ptr(f.pinv), _lib.ptr(lo),
+                  _lib.ptr(li), _lib.ptr(lv), _lib.ptr(lm), _lib.ptr(uo), _lib.ptr(ui),
+                  _lib.ptr(uv), _lib.ptr(um), _lib.ptr(ur), _lib.ptr(b), _lib.ptr(x),
+                  int(f.reach), _lib.stream_ptr())
         return x
     f.ensure_rows()
     _lib.call("rs_lu_solve", f.nsys, f.n, _lib.ptr(f.pinv), _lib.ptr(f.L_rp), _lib.ptr(f.L_ci),

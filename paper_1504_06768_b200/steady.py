@@ -292,6 +292,7 @@ def _solve(mode, A, P, f, rhs, tol, max_iter, restart_m, want_condest, threads=0
                                                           _lib.ptr(lv), _lib.ptr(lm))
             a.Us_rowoff, a.Us_idx, a.Us_val, a.Us_meta, a.Us_rd = (
                 _lib.ptr(uo), _lib.ptr(ui), _lib.ptr(uv), _lib.ptr(um), _lib.ptr(ur))
+            a.col_reach = int(f.reach)
         else:
             f.ensure_rows()
             a.L_rp, a.L_ci, a.L_v = f.L_rp.data_ptr(), f.L_ci.data_ptr(), f.L_v.data_ptr()

@@ -351,3 +351,30 @@ def test_factorize_multi_cta_bit_exact(cuda, monkeypatch, name, kw, d, p, cps, n
         assert bits_equal(li, fo.Li) and bits_equal(ui, fo.Ui)
         assert bits_equal(lx, fo.Lx) and bits_equal(ux, fo.Ux)
         assert bits_equal(x[s * m.n:(s + 1) * m.n], fo.solve(b[s * m.n:(s + 1) * m.n]))
+
+
+def test_apply_sliding_window_multi_consumer_bit_exact(cuda, monkeypatch):
+    """A lone system whose sweep vector does not fit shared memory (n = 14,400)
+    sweeps through the sliding shared-memory window with several consumer
+    warps (colsweep.cuh col_consume_win): same bits as the oracle's column
+    loops, with the window on or off and for 1, 3 and 6 consumers."""
+    from paper_1504_06768_b200 import configs
+    monkeypatch.setenv("RHOSOLVE_GRID_MIN_N", "100000000")
+    H, c = configs.optomech(n_c=4, n_m=30)
+    Lo = oracle_L(H, c)
+    S = O.shift(Lo)
+    fwd, _ = O.rcm(S)
+    pm = O.permute(S, fwd)
+    assert pm.n == 14400
+    fo = O.factorize_raw(pm, 1e-3, 8.0)
+    f = factor.factor_batch(from_host(_host(pm)), 1e-3, 8.0)
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal(pm.n) + 1j * rng.standard_normal(pm.n)
+    ref = fo.solve(b)
+    f.ensure_cols()
+    assert 0 < f.reach < pm.n
+    for win in ("1", "0"):
+        monkeypatch.setenv("RHOSOLVE_COL_WINDOW", win)
+        for w in ("1", "3", "6"):
+            monkeypatch.setenv("RHOSOLVE_COL_CONSUMERS", w)
+            assert bits_equal(factor.solve_lu(f, b), ref), (win, w)
