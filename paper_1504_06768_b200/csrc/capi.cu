@@ -5,6 +5,7 @@
 #include <stdlib.h>
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <stdio.h>
 #include <string.h>
 
@@ -94,6 +95,36 @@ static int keep_pool_memory() {
   RS_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   done.fetch_or(bit, std::memory_order_relaxed);
   return RS_OK;
+}
+// One non-blocking side stream per device (hybrid batch factorization).
+static int side_stream(cudaStream_t* out) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  cudaStream_t& s = streams[dev & 63];
+  if (!s) RS_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = s;
+  return RS_OK;
+}
+// How many leading systems of a complete-LU batch take the frontal kernel
+// while the rest run through pipeline CTAs beside it (0: no hybrid).
+// RHOSOLVE_HYBRID_F overrides (0 disables).
+static int hybrid_frontal_count(int nsys, int n) {
+  if (const char* e = getenv("RHOSOLVE_HYBRID_F")) return std::min(std::max(0, atoi(e)), nsys);
+  (void)n;
+  return 0;
+}
+// Complete-LU batches: the compact shared-memory kernel (ilu_compact.cu).
+// RHOSOLVE_COMPACT=1/0 forces it on/off; auto: batches beyond three waves of
+// the frontal kernel.
+static bool compact_enabled(int nsys) {
+  if (const char* e = getenv("RHOSOLVE_COMPACT")) return e[0] == '1';
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return nsys > 3 * sms;
 }
 const char* rs_last_error(void) { return g_err; }
 long long rs_launch_count(void) { return g_launches.load(); }
@@ -315,6 +346,8 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
   a.pinv = pinv;
   a.state = state;
   a.warps = nsys >= 148 ? 8 : 16;
+  a.hist = 1;
+  a.b0 = 0;
   if (const char* e = getenv("RHOSOLVE_ILU_WARPS")) a.warps = atoi(e);  // tuning knob
   // the critical column's owner polls the frontier hot (naps measured: no
   // gain at 16-128 ns on the 512-system batch)
@@ -347,8 +380,10 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
   };
   const size_t o_x = take(16 * NW);
   const size_t o_flag = take(4 * NW);
-  const size_t o_bits =
-      a.bits_in_smem ? 0 : take(4 * (size_t)nwords * nsys * a.warps * a.cps);
+  const bool maybe_hybrid = hybrid_frontal_count(nsys, n) > 0;  // (its pipeline CTAs keep the bitmaps in global memory)
+  const size_t o_bits = (a.bits_in_smem && !maybe_hybrid)
+                            ? 0
+                            : take(4 * (size_t)nwords * nsys * a.warps * a.cps);
   const size_t o_ctl = take(8 * (size_t)nsys);
   const size_t o_prow = take(4 * N);
   const size_t o_pat = take(4 * NW);
@@ -362,7 +397,7 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
   RS_CUDA_TRY(cudaMallocAsync(&ws, bytes, st));
   a.wx = reinterpret_cast<double2*>(ws + o_x);
   a.wflag = reinterpret_cast<int32_t*>(ws + o_flag);
-  a.wbits = a.bits_in_smem ? nullptr : reinterpret_cast<uint32_t*>(ws + o_bits);
+  a.wbits = (a.bits_in_smem && !maybe_hybrid) ? nullptr : reinterpret_cast<uint32_t*>(ws + o_bits);
   a.prow = reinterpret_cast<int32_t*>(ws + o_prow);
   a.wpat = reinterpret_cast<int32_t*>(ws + o_pat);
   a.wurow = reinterpret_cast<int32_t*>(ws + o_urow);
@@ -373,11 +408,58 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
   a.wkey = reinterpret_cast<uint64_t*>(ws + o_key);
   a.gctl = reinterpret_cast<int32_t*>(ws + o_ctl);
   a.probe = g_factor_probe;
-  // complete LU of small systems (the c4 sweep): right-looking frontal
-  // elimination in shared memory; whatever it does not take (front too large,
-  // zero pivot) runs through the column pipeline below
-  if (frontal_enabled(nsys) && !(drop_tol > 0.0) && fill_cap < 0 && !fill_caps && !q &&
-      !g_factor_probe) {
+  const bool complete_lu = !(drop_tol > 0.0) && fill_cap < 0 && !fill_caps && !q &&
+                           !g_factor_probe && a.cps == 1;
+  // Large batches of complete LUs (the 512-system c4 sweep): hybrid.  The
+  // frontal kernel is bound by shared memory (one system per SM) and latency,
+  // the column pipeline by instruction issue, so they share the SMs: the
+  // first F systems go to the 64-register frontal build on `st`, the others to
+  // pipeline CTAs without shared-memory state (two fit beside a front) on a
+  // side stream, concurrently.  Both produce the reference's factors, so the
+  // split is invisible in the output.
+  const int hybrid_f = complete_lu ? hybrid_frontal_count(nsys, n) : 0;
+  int compact = 0;
+  if (complete_lu && hybrid_f == 0 && compact_enabled(nsys)) {
+    const int crc = launch_lu_compact(a, st, &compact);
+    if (crc) {
+      cudaFreeAsync(ws, st);
+      return crc;
+    }
+  }
+  if (compact) {
+    // (whatever it left in FAC_RUNNING runs through the general kernel below)
+  } else if (hybrid_f > 0) {
+    cudaStream_t side = nullptr;
+    RS_TRY(side_stream(&side));
+    cudaEvent_t fork = nullptr, join = nullptr;
+    RS_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    RS_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    RS_CUDA_TRY(cudaEventRecord(fork, st));
+    RS_CUDA_TRY(cudaStreamWaitEvent(side, fork, 0));
+    FactorArgs fa = a;
+    fa.B = hybrid_f;
+    int rc = frontal_factor(fa, st, true);  // (launched first: the fronts claim their SMs)
+    if (!rc) {
+      FactorArgs pa = a;
+      pa.b0 = hybrid_f;
+      pa.B = nsys - hybrid_f;
+      pa.smem_mode = 0;
+      pa.bits_in_smem = 0;
+      pa.hist = 0;
+      rc = launch_ilutp(pa, side);
+    }
+    cudaEventRecord(join, side);
+    cudaStreamWaitEvent(st, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    if (rc) {
+      cudaFreeAsync(ws, st);
+      return rc;
+    }
+  } else if (frontal_enabled(nsys) && complete_lu) {
+    // complete LU of small systems: right-looking frontal elimination in
+    // shared memory; whatever it does not take (front too large, zero pivot)
+    // runs through the column pipeline below
     const int frc = frontal_factor(a, st);
     if (frc) {
       cudaFreeAsync(ws, st);

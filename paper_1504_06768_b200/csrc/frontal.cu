@@ -500,8 +500,11 @@ __device__ int g_fdebug;  // tuning: 1 skip the update, 2 skip L/U emission
 //       so a fill starts from 0 - l u as in the reference; loaders then write
 //       the rows joining at step k+1 into free slots (never the pivot row,
 //       which the update still reads)
-template <bool PROBE>
-__global__ void __launch_bounds__(FT, 1) frontal_lu_kernel(FrontArgs a) {
+// MINB = 2 caps the kernel at 64 registers (16 bytes of spill): half of the
+// register file stays free for two column-pipeline CTAs on the same SM (the
+// hybrid batch mode of rs_factorize).
+template <bool PROBE, int MINB>
+__global__ void __launch_bounds__(FT, MINB) frontal_lu_kernel(FrontArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int s_jrows;  // rows joining at step k+1 (published in P1)
   const int b = blockIdx.x;
@@ -1028,7 +1031,7 @@ bool frontal_enabled(int nsys) {
 
 // Complete LU of the systems whose front fits (see top of file); the others
 // keep state 0 for the pipelined kernel.
-int frontal_factor(const FactorArgs& fa, cudaStream_t st) {
+int frontal_factor(const FactorArgs& fa, cudaStream_t st, bool share_sm) {
   const int n = fa.n, B = fa.B;
   g_frontal_taken.store(0, std::memory_order_relaxed);
   if (B == 0 || n == 0 || n > MAXN || fa.q) return RS_OK;
@@ -1156,7 +1159,8 @@ int frontal_factor(const FactorArgs& fa, cudaStream_t st) {
   a.capU = fa.capU;
   a.pinv = fa.pinv;
   a.state = fa.state;
-  auto kern = g_probe_host.load() ? frontal_lu_kernel<true> : frontal_lu_kernel<false>;
+  auto kern = g_probe_host.load() ? frontal_lu_kernel<true, 1>
+                                  : (share_sm ? frontal_lu_kernel<false, 2> : frontal_lu_kernel<false, 1>);
   RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<B, FT, smem, st>>>(a);
   ::rs::count_launch();

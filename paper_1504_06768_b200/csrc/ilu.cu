@@ -91,9 +91,9 @@ __device__ __forceinline__ void probe_mark(unsigned long long* pr, int k, int sl
 // shared-memory bytes per CTA: pinv, prow, Lp (when shared_in_smem) + the
 // per-warp pending bitmaps (when bits_in_smem) + control words.
 __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_smem,
-                                            int bits_in_smem) {
+                                            int bits_in_smem, int hist) {
   const size_t nwords = ((size_t)n + 31) / 32;
-  size_t b = 64 + 1024 * (size_t)warps;  // control words + per-warp cap histograms
+  size_t b = 64 + (hist ? 1024 * (size_t)warps : 0);  // control words + per-warp cap histograms
   if (shared_in_smem) b += 4 * ((size_t)n * 2 + (size_t)n + 1);
   if (bits_in_smem) b += 4 * nwords * (size_t)warps;
   return (b + 15) & ~(size_t)15;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
   const int lane = threadIdx.x & 31;
   const int Wl = blockDim.x >> 5;
   const int cps = MULTI ? a.cps : 1;
-  const int b = MULTI ? blockIdx.x / cps : blockIdx.x;
+  const int b = MULTI ? blockIdx.x / cps : blockIdx.x + a.b0;
   const int wid = MULTI ? (blockIdx.x % cps) * Wl + (threadIdx.x >> 5) : (threadIdx.x >> 5);
   const int lw = threadIdx.x >> 5;  // warp index inside this CTA (shared-memory slices)
   const int W = Wl * cps;
@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(MAXT, MINB) ilutp_pipeline_kernel(FactorArgs a
   // control words: ctl[0] = number of finished columns, ctl[1] = abort
   volatile int32_t* ctl = MULTI ? reinterpret_cast<volatile int32_t*>(a.gctl + 2 * (int64_t)b)
                                 : reinterpret_cast<volatile int32_t*>(smem);
-  unsigned char* sp = smem + 64 + 1024 * (size_t)Wl;  // after the per-warp cap histograms
+  // after the per-warp cap histograms (complete LU launched without them: a.hist = 0)
+  unsigned char* sp = smem + 64 + (a.hist ? 1024 * (size_t)Wl : 0);
   int32_t *pinv, *prow, *Lp;
   if (a.smem_mode) {
     pinv = reinterpret_cast<int32_t*>(sp);
@@ -768,7 +769,7 @@ static int launch_ilutp_multi(const FactorArgs& a, size_t smem, cudaStream_t st)
 int launch_ilutp(const FactorArgs& a, cudaStream_t st) {
   if (a.B == 0 || a.n == 0) return RS_OK;
   const int W = a.warps;
-  const size_t smem = ilutp_smem_bytes(a.n, W, a.smem_mode, a.bits_in_smem);
+  const size_t smem = ilutp_smem_bytes(a.n, W, a.smem_mode, a.bits_in_smem, a.hist);
   if (a.cps > 1) return launch_ilutp_multi(a, smem, st);
   // one instantiation per block size so each gets its full register budget
   // (a 1024-thread bound caps registers at 64 and spills the tail loops)
@@ -780,7 +781,9 @@ int launch_ilutp(const FactorArgs& a, cudaStream_t st) {
     return RS_OK;
   };
   // batches: keep 4 systems per SM resident (512 systems ~ one wave)
-  const bool batch = a.B > 148;
+  // (a launch with a system offset shares its SMs with the frontal kernel:
+  // always the 64-register build)
+  const bool batch = a.B > 148 || a.b0 > 0;
   int rc;
   (void)0;
   const bool inc = a.drop_tol > 0.0 || a.fill_cap >= 0 || a.fill_caps != nullptr;
@@ -809,8 +812,8 @@ int ilutp_plan(int32_t n, int warps, int* smem_mode, int* bits_in_smem) {
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   // keep ~96 KB of the carveout as L1 for the per-warp accumulators
   const size_t budget = (size_t)max_smem > 131072 ? (size_t)max_smem - 98304 : 32768;
-  *bits_in_smem = ilutp_smem_bytes(n, warps, 0, 1) <= budget;
-  *smem_mode = ilutp_smem_bytes(n, warps, 1, *bits_in_smem) <= budget;
+  *bits_in_smem = ilutp_smem_bytes(n, warps, 0, 1, 1) <= budget;
+  *smem_mode = ilutp_smem_bytes(n, warps, 1, *bits_in_smem, 1) <= budget;
   return RS_OK;
 }
 

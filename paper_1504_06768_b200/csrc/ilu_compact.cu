@@ -1,0 +1,474 @@
+// Complete LU with partial pivoting, column-pipelined like ilu.cu, with every
+// warp's working column held COMPACTLY in shared memory: the batch kernel of
+// the c4 sweep (512 systems of order 1600, four systems per SM).
+//
+// Same semantics and the same bits as the reference `factorize`
+// (pkg/src/rhosolve/kernels/_ckernels.pyx:144-385) with drop_tol = 0 and no
+// fill cap, and the same pipeline as ilutp_pipeline_kernel (warp w owns
+// columns w, w+W, ...; pending pivotal columns in a per-warp bitmap, popped
+// in ascending order below the finished-column frontier; see ilu.cu for why
+// that reproduces the reference's heap order).  What differs is where the
+// column lives.  ilu.cu keeps a dense n-vector per warp in global memory
+// (x[row], marker[row], pattern list): every access pays a 64-bit address
+// computation and an L1/L2 round trip, and the ncu source view of the batch
+// (profiles/r02_ncu_c4_pipeline_source.txt) shows the kernel issue-bound on
+// exactly that: ~415 warp instructions per applied L column.  Here
+//   * the values of the column's pattern sit in shared memory BY POSITION
+//     (xs[pos], discovery order = the reference's pattern order) next to the
+//     row of every position (pats[pos], u16);
+//   * a per-warp global array holds only pos_of[row], validated as a sparse
+//     set: row i is in the pattern iff p = pos_of[i] < npat and pats[p] == i
+//     -- so it never needs clearing and stale contents are harmless;
+//   * pinv / prow / Lp shadows and the pending bitmaps are shared memory too.
+// One global load per touched row remains; the value traffic, the pattern
+// list, the candidate list and the pivot search run on 32-bit shared-memory
+// addresses.  A column whose pattern outgrows the per-warp capacity stops
+// the system untouched (state stays FAC_RUNNING) and ilu.cu's general kernel
+// factors it afterwards; capacity overflow of the output and zero pivots are
+// reported exactly as ilu.cu does.
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace rs {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ int warp_min_i(int v) {
+  return (int)__reduce_min_sync(FULL, v);
+}
+// another warp of the CTA wrote it: CTA-scope relaxed load
+__device__ __forceinline__ int ld_cta(const int32_t* p) {
+  int v;
+  asm volatile("ld.relaxed.cta.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+}  // namespace
+
+// shared-memory bytes per CTA for `warps` warps and `capx` positions each
+size_t lu_compact_smem_bytes(int32_t n, int warps, int capx) {
+  const size_t nwords = ((size_t)n + 31) / 32;
+  return 16 * (size_t)warps * capx + 4 * (3 * (size_t)n + 1) + 4 * nwords * warps + 16 +
+         2 * (size_t)warps * capx;
+}
+
+// Shared memory is addressed with explicit 32-bit shared-state-space
+// accesses: under the 64-register cap (four systems per SM) the compiler
+// otherwise re-derives every base (CTA window + warp slice + offset) from
+// constants at each use -- a third of the instructions of the first version.
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts2(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1,%2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ int lds32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, int v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return (int)v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, int v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void atoms_or(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void atoms_and(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// keeps a pointer in registers (opaque to rematerialisation from constants)
+template <typename T>
+__device__ __forceinline__ T* pin(T* p) {
+  asm volatile("" : "+l"(p));
+  return p;
+}
+
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, int capx) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int b = blockIdx.x + a.b0;
+  const int32_t n = a.n;
+  const int nwords = (n + 31) >> 5;
+  int32_t* state = a.state + 3 * (int64_t)b;
+  if (state[0] != FAC_RUNNING) return;
+
+  // shared layout: xs[W][capx] | pinv[n] prow[n] Lp[n+1] | bits[W][nwords] | ctl[4] | pats[W][capx]
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
+  uint32_t XS = s0 + 16u * (uint32_t)(wid * capx);      // this warp's values by position
+  uint32_t PINV = s0 + 16u * (uint32_t)(W * capx);      // pinv; prow at +4n; Lp at +8n
+  uint32_t BITS = PINV + 4u * (3u * (uint32_t)n + 1u) + 4u * (uint32_t)(wid * nwords);
+  const uint32_t CTL = PINV + 4u * (3u * (uint32_t)n + 1u) + 4u * (uint32_t)(W * nwords);
+  uint32_t PATS = CTL + 16u + 2u * (uint32_t)(wid * capx);  // this warp's rows by position
+  asm volatile("" : "+r"(XS), "+r"(PINV), "+r"(BITS), "+r"(PATS));
+  const uint32_t n4 = 4u * (uint32_t)n;
+#define PROW (PINV + n4)
+#define LPS (PINV + 2u * n4)
+
+  const int64_t bn = (int64_t)b * n;
+  int32_t* const gLp = a.Lp + (int64_t)b * (n + 1);
+  int32_t* const gUp = a.Up + (int64_t)b * (n + 1);
+  int32_t* const Li = pin(a.Li + (int64_t)b * a.capL);
+  double2* const Lx = pin(a.Lx + (int64_t)b * a.capL);
+  int32_t* const gpinv = a.pinv + bn;
+  const int32_t* const Ap = a.Ap + bn;
+  // per-warp global scratch: position of a row (sparse set), U positions of the column
+  const int64_t ws = ((int64_t)b * W + wid) * n;
+  int32_t* const pos_of = pin(a.wflag + ws);
+  int32_t* const upos = a.wurow + ws;
+
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sts32(PINV + 4u * i, -1);
+    sts32(PROW + 4u * i, -1);
+    gpinv[i] = -1;
+    sts32(LPS + 4u * i, 0);
+  }
+  for (int w = lane; w < nwords; w += 32) sts32(BITS + 4u * w, 0);
+  if (threadIdx.x == 0) {
+    sts32(LPS + n4, 0);
+    sts32(CTL, 0);
+    sts32(CTL + 4, 0);
+    gLp[0] = 0;
+    gUp[0] = 0;
+  }
+  __syncthreads();
+
+  for (int k = wid; k < n; k += W) {
+    int scanned = lds32(CTL);
+    if (lds32(CTL + 4)) break;
+    __threadfence_block();
+    // ---- 1. scatter column k; seed pending with columns already finished ----
+    const int32_t c0 = Ap[k], c1 = Ap[k + 1];
+    int npat = c1 - c0;
+    if (npat > capx) {
+      if (lane == 0) sts32(CTL + 4, 2);
+      break;
+    }
+    int lowc = 0x7fffffff;
+    for (int e = c0 + lane; e < c1; e += 32) {
+      const int i = a.Ai[e];
+      sts2(XS + 16u * (e - c0), a.Ax[e]);
+      sts16(PATS + 2u * (e - c0), i);
+      pos_of[i] = e - c0;
+      const int pv = lds32(PINV + 4u * i);
+      if (pv >= 0 && pv < scanned) {
+        atoms_or(BITS + 4u * (pv >> 5), 1u << (pv & 31));
+        lowc = min(lowc, pv);
+      }
+    }
+    lowc = warp_min_i(lowc);
+    __syncwarp();
+
+    // ---- 2. updates in ascending pivotal order, gated by the frontier -------
+    int unum = 0;
+    int w = (lowc == 0x7fffffff) ? ((scanned + 31) >> 5) : (lowc >> 5);
+    int stop = 0;  // 1: another warp aborted, 2: pattern capacity exceeded
+    while (true) {
+      const int wend = (scanned + 31) >> 5;
+      int c = -1;
+      while (w < wend) {
+        const int ww = w + lane;
+        const uint32_t bv = (ww < wend) ? (uint32_t)lds32(BITS + 4u * ww) : 0u;
+        const unsigned m = __ballot_sync(FULL, bv != 0u);
+        if (m) {
+          const int src = __ffs(m) - 1;
+          const uint32_t word = __shfl_sync(FULL, bv, src);
+          w += src;
+          c = (w << 5) + __ffs(word) - 1;
+          break;
+        }
+        w += 32;
+      }
+      if (c < 0) {
+        if (scanned == k) break;
+        // advance the frontier over newly finished columns; the owner of the
+        // next column to finish polls hot, the others nap with their distance
+        int d;
+        const int dist = k - scanned - 1;
+        const unsigned nap =
+            dist <= 0 ? (unsigned)a.hot_nap : (dist < 4 ? a.nap_step * dist : 8u * a.nap_step);
+        int ab = 0;
+        while ((d = lds32(CTL)) == scanned && !(ab = lds32(CTL + 4))) {
+          if (nap) __nanosleep(nap);
+        }
+        if (ab || lds32(CTL + 4)) {
+          stop = 1;
+          break;
+        }
+        __threadfence_block();
+        int newlow = 0x7fffffff;
+        for (int m = scanned + lane; m < d; m += 32) {
+          const int r = lds32(PROW + 4u * m);
+          const int p = pos_of[r];
+          if ((unsigned)p < (unsigned)npat && lds16(PATS + 2u * p) == r) {
+            atoms_or(BITS + 4u * (m >> 5), 1u << (m & 31));
+            newlow = min(newlow, m);
+          }
+        }
+        newlow = warp_min_i(newlow);
+        __syncwarp();
+        w = (newlow == 0x7fffffff) ? ((d + 31) >> 5) : (newlow >> 5);
+        scanned = d;
+        continue;
+      }
+      // pop column c: U entry = the value of its pivot row, final by now
+      const int pp = pos_of[lds32(PROW + 4u * c)];
+      const int32_t p0 = lds32(LPS + 4u * c) + 1, p1 = lds32(LPS + 4u * c + 4u);
+      const double2 xc = lds2(XS + 16u * pp);
+      if (lane == 0) {
+        atoms_and(BITS + 4u * w, ~(1u << (c & 31)));
+        upos[unum] = pp;
+      }
+      ++unum;
+      // apply L[:,c], 64 entries per pass: every load of a pass is issued
+      // before any is consumed
+      for (int base = p0; base < p1; base += 64) {
+        const int pa = base + lane;
+        const bool acta = pa < p1, actb = pa + 32 < p1;
+        int ia = 0, ib = 0;
+        double2 la = make_double2(0.0, 0.0), lb = la;
+        if (acta) {
+          ia = Li[pa];
+          la = Lx[pa];
+        }
+        if (actb) {
+          ib = Li[pa + 32];
+          lb = Lx[pa + 32];
+        }
+        int fa = acta ? pos_of[ia] : 0x7fffffff, fb = actb ? pos_of[ib] : 0x7fffffff;
+        bool ina = (unsigned)fa < (unsigned)npat, inb = (unsigned)fb < (unsigned)npat;
+        if (ina) ina = lds16(PATS + 2u * fa) == ia;
+        if (inb) inb = lds16(PATS + 2u * fb) == ib;
+        double2 xa = make_double2(0.0, 0.0), xb = xa;
+        if (ina) xa = lds2(XS + 16u * fa);
+        if (inb) xb = lds2(XS + 16u * fb);
+        const bool newa = acta && !ina, newb = actb && !inb;
+        const unsigned ma = __ballot_sync(FULL, newa);
+        const unsigned mb = __ballot_sync(FULL, newb);
+        if (ma | mb) {  // fill rows join the pattern in discovery order
+          const int na = __popc(ma), nb = __popc(mb);
+          if (npat + na + nb > capx) {
+            stop = 2;
+            break;
+          }
+          const unsigned lt = lanemask_lt();
+          if (newa) {
+            fa = npat + __popc(ma & lt);
+            sts16(PATS + 2u * fa, ia);
+            pos_of[ia] = fa;
+            const int v = lds32(PINV + 4u * ia);
+            if (v >= 0 && v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
+          }
+          if (newb) {
+            fb = npat + na + __popc(mb & lt);
+            sts16(PATS + 2u * fb, ib);
+            pos_of[ib] = fb;
+            const int v = lds32(PINV + 4u * ib);
+            if (v >= 0 && v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
+          }
+          npat += na + nb;
+          __syncwarp();
+        }
+        if (acta) sts2(XS + 16u * fa, csub(xa, cmul_plain(la, xc)));
+        if (actb) sts2(XS + 16u * fb, csub(xb, cmul_plain(lb, xc)));
+      }
+      if (stop) break;
+      __syncwarp();
+    }
+    if (stop) {
+      if (stop == 2 && lane == 0) sts32(CTL + 4, 2);
+      break;
+    }
+    __threadfence_block();  // acquire: every column < k is final
+
+    // ---- 3. pivot: max |re|+|im| over non-pivotal rows, ties -> lowest row --
+    double best = -1.0;
+    int ipiv = -1, ipos = -1, lnum = 0;
+    for (int blk = 0; blk < npat; blk += 128) {
+      int iu[4];
+      bool cand[4];
+      double2 xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = blk + 32 * u + lane;
+        iu[u] = t < npat ? lds16(PATS + 2u * t) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = blk + 32 * u + lane;
+        cand[u] = iu[u] >= 0 && lds32(PINV + 4u * iu[u]) < 0;
+        xv[u] = cand[u] ? lds2(XS + 16u * t) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        lnum += __popc(__ballot_sync(FULL, cand[u]));
+        if (cand[u]) {
+          const double mag = cabs1(xv[u]);
+          if (mag > best || (mag == best && iu[u] < ipiv)) {
+            best = mag;
+            ipiv = iu[u];
+            ipos = blk + 32 * u + lane;
+          }
+        }
+      }
+    }
+    double gbest = best;
+    int gipiv = ipiv;
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(FULL, gbest, o);
+      const int oi = __shfl_xor_sync(FULL, gipiv, o);
+      if (ob > gbest || (ob == gbest && oi >= 0 && (gipiv < 0 || oi < gipiv))) {
+        gbest = ob;
+        gipiv = oi;
+      }
+    }
+    if (gipiv < 0 || gbest == 0.0) {
+      if (lane == 0) {
+        state[0] = FAC_ZERO_PIVOT;
+        state[1] = k;
+        sts32(CTL + 4, 1);
+      }
+      break;
+    }
+    const unsigned om = __ballot_sync(FULL, ipiv == gipiv);
+    const int gpos = __shfl_sync(FULL, ipos, __ffs(om) - 1);
+    const double2 piv = lds2(XS + 16u * gpos);
+
+    // ---- 4. emit L (unit diagonal first), publish the column, then U -------
+    const int32_t lnnz = lds32(LPS + 4u * k);
+    const int32_t unnz = ld_cta(gUp + k);
+    if ((int64_t)unnz + unum + 1 > a.capU || (int64_t)lnnz + lnum > a.capL) {
+      if (lane == 0) {
+        state[0] = FAC_OVERFLOW;
+        state[1] = k;
+        sts32(CTL + 4, 1);
+      }
+      break;
+    }
+    const double2 rp = recipc(piv);
+    if (lane == 0) {
+      Li[lnnz] = gipiv;
+      Lx[lnnz] = make_double2(1.0, 0.0);
+    }
+    int off = lnnz + 1;
+    for (int blk = 0; blk < npat; blk += 128) {
+      int iu[4];
+      bool kp[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = blk + 32 * u + lane;
+        iu[u] = t < npat ? lds16(PATS + 2u * t) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        kp[u] = iu[u] >= 0 && iu[u] != gipiv && lds32(PINV + 4u * iu[u]) < 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned m = __ballot_sync(FULL, kp[u]);
+        if (kp[u]) {
+          const int o = off + __popc(m & lanemask_lt());
+          Li[o] = iu[u];
+          Lx[o] = cmul_plain(lds2(XS + 16u * (blk + 32 * u + lane)), rp);
+        }
+        off += __popc(m);
+      }
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) {
+      gUp[k + 1] = unnz + unum + 1;
+      gLp[k + 1] = off;
+      sts32(LPS + 4u * k + 4u, off);
+      sts32(PINV + 4u * gipiv, k);
+      gpinv[gipiv] = k;
+      sts32(PROW + 4u * k, gipiv);
+      __threadfence_block();  // release column k
+      sts32(CTL, k + 1);
+    }
+    // U column k (pops were ascending; pivot last): no later column reads it,
+    // so it is written after the release, off the critical path
+    int32_t* const Ui = a.Ui + (int64_t)b * a.capU;
+    double2* const Ux = a.Ux + (int64_t)b * a.capU;
+    for (int t = lane; t < unum; t += 32) {
+      const int p = upos[t];
+      Ui[unnz + t] = lds32(PINV + 4u * lds16(PATS + 2u * p));
+      Ux[unnz + t] = lds2(XS + 16u * p);
+    }
+    if (lane == 0) {
+      Ui[unnz + unum] = k;
+      Ux[unnz + unum] = piv;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (lds32(CTL + 4)) return;  // zero pivot / overflow recorded; 2: left to the general kernel
+  // ---- finish: remap L rows to pivotal indices --------------------------------
+  const int32_t lnnz = gLp[n];
+  for (int p = threadIdx.x; p < lnnz; p += blockDim.x) Li[p] = lds32(PINV + 4u * Li[p]);
+  if (threadIdx.x == 0) {
+    state[0] = FAC_DONE;
+    state[1] = -1;
+  }
+#undef PROW
+#undef LPS
+}
+
+// Launches the compact kernel when it applies (complete LU, natural column
+// order, shared memory for the shadows plus a useful pattern capacity);
+// *launched = 0 otherwise.  Systems it could not finish keep FAC_RUNNING.
+int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
+  *launched = 0;
+  if (a.B == 0 || a.n == 0 || a.q || a.cps > 1 || a.n > 65535) return RS_OK;
+  if (a.drop_tol > 0.0 || a.fill_cap >= 0 || a.fill_caps || a.pivot_floor > 0.0) return RS_OK;
+  int dev = 0, sms = 0, per_sm = 0, max_block = 0;
+  RS_CUDA_TRY(cudaGetDevice(&dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  RS_CUDA_TRY(cudaDeviceGetAttribute(&max_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int W = a.warps <= 8 ? 8 : 16;
+  if (W != a.warps) return RS_OK;
+  // systems resident per SM: the whole batch in one wave when four fit
+  const int want = W == 8 ? std::min(4, std::max(1, (a.B + sms - 1) / sms)) : 1;
+  const size_t budget = std::min<size_t>((size_t)max_block, (size_t)per_sm / want - 1024);
+  const size_t fixed = lu_compact_smem_bytes(a.n, W, 0);
+  if (fixed + 18 * (size_t)W * 64 > budget) return RS_OK;
+  int capx = (int)((budget - fixed) / (18 * (size_t)W)) & ~7;
+  capx = std::min(capx, (a.n + 7) & ~7);
+  if (const char* e = getenv("RHOSOLVE_COMPACT_CAPX")) capx = std::max(8, atoi(e) & ~7);  // tests
+  const size_t smem = lu_compact_smem_bytes(a.n, W, capx);
+  if (smem > (size_t)max_block) return RS_OK;
+  auto launch = [&](auto kern) -> int {
+    RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<a.B, 32 * W, smem, st>>>(a, capx);
+    ::rs::count_launch();
+    RS_CUDA_TRY(cudaGetLastError());
+    return RS_OK;
+  };
+  RS_TRY(W == 8 ? (want > 1 ? launch(lu_compact_kernel<256, 4>) : launch(lu_compact_kernel<256, 1>))
+                : launch(lu_compact_kernel<512, 1>));
+  *launched = 1;
+  return RS_OK;
+}
+
+}  // namespace rs

@@ -66,6 +66,8 @@ struct FactorArgs {
   int smem_mode;     // 1: pinv / prow / Lp shadow live in shared memory
   int bits_in_smem;  // 1: per-warp pending bitmaps in shared memory
   int warps;         // warps (columns in flight) per system
+  int hist;          // 1: per-warp cap-selection histograms in shared memory (0 only for complete LU)
+  int b0;            // first system of this launch (single-CTA mode; the grid covers b0 .. b0 + grid - 1)
   int hot_nap;       // ns the next column's owner naps between frontier polls
   unsigned nap_step; // ns per column of distance for the other warps' naps
   int cps;           // CTAs per system (> 1: multi-CTA mode for large systems)
@@ -76,8 +78,11 @@ struct FactorArgs {
 enum { FAC_RUNNING = 0, FAC_DONE = 1, FAC_ZERO_PIVOT = 2, FAC_OVERFLOW = 3 };
 int launch_ilutp(const FactorArgs& a, cudaStream_t st);
 __host__ __device__ size_t ilutp_smem_bytes(int32_t n, int warps, int shared_in_smem,
-                                            int bits_in_smem);
+                                            int bits_in_smem, int hist);
 int ilutp_plan(int32_t n, int warps, int* smem_mode, int* bits_in_smem);
+// ilu_compact.cu: complete LU with the working column compact in shared
+// memory (batches); systems it leaves in FAC_RUNNING go to launch_ilutp.
+int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched);
 
 // ---- halfsolve.cu: in-place lower / upper solves on the raw CSC factors ----
 int half_solve(int upper, int B, int32_t n, const int32_t* cp, const int32_t* ci,
@@ -93,7 +98,8 @@ void col_min_degree_host(int64_t n, const int64_t* rp, const int64_t* ci, int64_
 // shared memory and marks it FAC_DONE; the rest keep their state for
 // launch_ilutp.  RHOSOLVE_FRONTAL=1/0 forces it on/off (auto: <= 3 waves).
 bool frontal_enabled(int nsys);
-int frontal_factor(const FactorArgs& a, cudaStream_t st);
+// share_sm: the 64-register build, so column-pipeline CTAs fit beside it.
+int frontal_factor(const FactorArgs& a, cudaStream_t st, bool share_sm = false);
 int frontal_last_taken();
 int frontal_probe(int enable, double* out4);
 
