@@ -57,10 +57,13 @@ __device__ __forceinline__ int ld_cta(const int32_t* p) {
 }  // namespace
 
 // shared-memory bytes per CTA for `warps` warps and `capx` positions each
-size_t lu_compact_smem_bytes(int32_t n, int warps, int capx) {
+// (pos8: the row -> position map lives in shared memory as one byte per row)
+size_t lu_compact_smem_bytes(int32_t n, int warps, int capx, int pos8) {
   const size_t nwords = ((size_t)n + 31) / 32;
-  return 16 * (size_t)warps * capx + 4 * (3 * (size_t)n + 1) + 4 * nwords * warps + 16 +
-         2 * (size_t)warps * capx;
+  size_t b = 16 * (size_t)warps * capx + 4 * ((size_t)n + 1) + 4 * nwords * warps + 16 +
+             2 * 2 * (size_t)n + 2 * (size_t)warps * capx;
+  if (pos8) b += (size_t)warps * n;
+  return b;
 }
 
 // Shared memory is addressed with explicit 32-bit shared-state-space
@@ -91,6 +94,14 @@ __device__ __forceinline__ int lds16(uint32_t a) {
 __device__ __forceinline__ void sts16(uint32_t a, int v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
+__device__ __forceinline__ int lds8(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+  return (int)v;
+}
+__device__ __forceinline__ void sts8(uint32_t a, int v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
 __device__ __forceinline__ void atoms_or(uint32_t a, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -104,7 +115,9 @@ __device__ __forceinline__ T* pin(T* p) {
   return p;
 }
 
-template <int MAXT, int MINB>
+// POS8: row -> position map as one byte per row in shared memory (capx <= 256);
+// otherwise int32 per row in per-warp global scratch.
+template <int MAXT, int MINB, bool POS8>
 __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, int capx) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
@@ -114,17 +127,20 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
   int32_t* state = a.state + 3 * (int64_t)b;
   if (state[0] != FAC_RUNNING) return;
 
-  // shared layout: xs[W][capx] | pinv[n] prow[n] Lp[n+1] | bits[W][nwords] | ctl[4] | pats[W][capx]
+  // shared layout: xs[W][capx] c128 | Lp[n+1] i32 | bits[W][nwords] | ctl[4] |
+  //                pinv[n] prow[n] u16 (0xffff: none) | pats[W][capx] u16 | pos8[W][n] u8
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
-  uint32_t XS = s0 + 16u * (uint32_t)(wid * capx);      // this warp's values by position
-  uint32_t PINV = s0 + 16u * (uint32_t)(W * capx);      // pinv; prow at +4n; Lp at +8n
-  uint32_t BITS = PINV + 4u * (3u * (uint32_t)n + 1u) + 4u * (uint32_t)(wid * nwords);
-  const uint32_t CTL = PINV + 4u * (3u * (uint32_t)n + 1u) + 4u * (uint32_t)(W * nwords);
-  uint32_t PATS = CTL + 16u + 2u * (uint32_t)(wid * capx);  // this warp's rows by position
-  asm volatile("" : "+r"(XS), "+r"(PINV), "+r"(BITS), "+r"(PATS));
-  const uint32_t n4 = 4u * (uint32_t)n;
-#define PROW (PINV + n4)
-#define LPS (PINV + 2u * n4)
+  uint32_t XS = s0 + 16u * (uint32_t)(wid * capx);  // this warp's values by position
+  uint32_t LPS = s0 + 16u * (uint32_t)(W * capx);
+  uint32_t BITS = LPS + 4u * ((uint32_t)n + 1u) + 4u * (uint32_t)(wid * nwords);
+  const uint32_t CTL = LPS + 4u * ((uint32_t)n + 1u) + 4u * (uint32_t)(W * nwords);
+  uint32_t PINV = CTL + 16u;                                    // prow at +2n
+  uint32_t PATS = PINV + 4u * (uint32_t)n + 2u * (uint32_t)(wid * capx);  // rows by position
+  uint32_t POS = PINV + 4u * (uint32_t)n + 2u * (uint32_t)(W * capx) + (uint32_t)(wid * n);
+  asm volatile("" : "+r"(XS), "+r"(LPS), "+r"(PINV), "+r"(BITS), "+r"(PATS), "+r"(POS));
+  const uint32_t n2 = 2u * (uint32_t)n;
+#define PROW (PINV + n2)
+  constexpr int NONE = 0xffff;
 
   const int64_t bn = (int64_t)b * n;
   int32_t* const gLp = a.Lp + (int64_t)b * (n + 1);
@@ -136,17 +152,22 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
   // per-warp global scratch: position of a row (sparse set), U positions of the column
   const int64_t ws = ((int64_t)b * W + wid) * n;
   int32_t* const pos_of = pin(a.wflag + ws);
+  auto pos_get = [&](int i) -> int { return POS8 ? lds8(POS + (uint32_t)i) : pos_of[i]; };
+  auto pos_set = [&](int i, int p) {
+    if (POS8) sts8(POS + (uint32_t)i, p);
+    else pos_of[i] = p;
+  };
   int32_t* const upos = a.wurow + ws;
 
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    sts32(PINV + 4u * i, -1);
-    sts32(PROW + 4u * i, -1);
+    sts16(PINV + 2u * i, NONE);
+    sts16(PROW + 2u * i, NONE);
     gpinv[i] = -1;
     sts32(LPS + 4u * i, 0);
   }
   for (int w = lane; w < nwords; w += 32) sts32(BITS + 4u * w, 0);
   if (threadIdx.x == 0) {
-    sts32(LPS + n4, 0);
+    sts32(LPS + 4u * (uint32_t)n, 0);
     sts32(CTL, 0);
     sts32(CTL + 4, 0);
     gLp[0] = 0;
@@ -170,9 +191,9 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
       const int i = a.Ai[e];
       sts2(XS + 16u * (e - c0), a.Ax[e]);
       sts16(PATS + 2u * (e - c0), i);
-      pos_of[i] = e - c0;
-      const int pv = lds32(PINV + 4u * i);
-      if (pv >= 0 && pv < scanned) {
+      pos_set(i, e - c0);
+      const int pv = lds16(PINV + 2u * i);
+      if (pv < scanned) {  // (NONE = 0xffff is never below the frontier)
         atoms_or(BITS + 4u * (pv >> 5), 1u << (pv & 31));
         lowc = min(lowc, pv);
       }
@@ -219,8 +240,8 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
         __threadfence_block();
         int newlow = 0x7fffffff;
         for (int m = scanned + lane; m < d; m += 32) {
-          const int r = lds32(PROW + 4u * m);
-          const int p = pos_of[r];
+          const int r = lds16(PROW + 2u * m);
+          const int p = pos_get(r);
           if ((unsigned)p < (unsigned)npat && lds16(PATS + 2u * p) == r) {
             atoms_or(BITS + 4u * (m >> 5), 1u << (m & 31));
             newlow = min(newlow, m);
@@ -233,7 +254,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
         continue;
       }
       // pop column c: U entry = the value of its pivot row, final by now
-      const int pp = pos_of[lds32(PROW + 4u * c)];
+      const int pp = pos_get(lds16(PROW + 2u * c));
       const int32_t p0 = lds32(LPS + 4u * c) + 1, p1 = lds32(LPS + 4u * c + 4u);
       const double2 xc = lds2(XS + 16u * pp);
       if (lane == 0) {
@@ -256,7 +277,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
           ib = Li[pa + 32];
           lb = Lx[pa + 32];
         }
-        int fa = acta ? pos_of[ia] : 0x7fffffff, fb = actb ? pos_of[ib] : 0x7fffffff;
+        int fa = acta ? pos_get(ia) : 0x7fffffff, fb = actb ? pos_get(ib) : 0x7fffffff;
         bool ina = (unsigned)fa < (unsigned)npat, inb = (unsigned)fb < (unsigned)npat;
         if (ina) ina = lds16(PATS + 2u * fa) == ia;
         if (inb) inb = lds16(PATS + 2u * fb) == ib;
@@ -276,16 +297,16 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
           if (newa) {
             fa = npat + __popc(ma & lt);
             sts16(PATS + 2u * fa, ia);
-            pos_of[ia] = fa;
-            const int v = lds32(PINV + 4u * ia);
-            if (v >= 0 && v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
+            pos_set(ia, fa);
+            const int v = lds16(PINV + 2u * ia);
+            if (v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
           }
           if (newb) {
             fb = npat + na + __popc(mb & lt);
             sts16(PATS + 2u * fb, ib);
-            pos_of[ib] = fb;
-            const int v = lds32(PINV + 4u * ib);
-            if (v >= 0 && v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
+            pos_set(ib, fb);
+            const int v = lds16(PINV + 2u * ib);
+            if (v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
           }
           npat += na + nb;
           __syncwarp();
@@ -317,7 +338,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int t = blk + 32 * u + lane;
-        cand[u] = iu[u] >= 0 && lds32(PINV + 4u * iu[u]) < 0;
+        cand[u] = iu[u] >= 0 && lds16(PINV + 2u * iu[u]) == NONE;
         xv[u] = cand[u] ? lds2(XS + 16u * t) : make_double2(0.0, 0.0);
       }
 #pragma unroll
@@ -382,7 +403,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        kp[u] = iu[u] >= 0 && iu[u] != gipiv && lds32(PINV + 4u * iu[u]) < 0;
+        kp[u] = iu[u] >= 0 && iu[u] != gipiv && lds16(PINV + 2u * iu[u]) == NONE;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const unsigned m = __ballot_sync(FULL, kp[u]);
@@ -400,9 +421,9 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
       gUp[k + 1] = unnz + unum + 1;
       gLp[k + 1] = off;
       sts32(LPS + 4u * k + 4u, off);
-      sts32(PINV + 4u * gipiv, k);
+      sts16(PINV + 2u * gipiv, k);
       gpinv[gipiv] = k;
-      sts32(PROW + 4u * k, gipiv);
+      sts16(PROW + 2u * k, gipiv);
       __threadfence_block();  // release column k
       sts32(CTL, k + 1);
     }
@@ -412,7 +433,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
     double2* const Ux = a.Ux + (int64_t)b * a.capU;
     for (int t = lane; t < unum; t += 32) {
       const int p = upos[t];
-      Ui[unnz + t] = lds32(PINV + 4u * lds16(PATS + 2u * p));
+      Ui[unnz + t] = lds16(PINV + 2u * lds16(PATS + 2u * p));
       Ux[unnz + t] = lds2(XS + 16u * p);
     }
     if (lane == 0) {
@@ -425,18 +446,39 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
   if (lds32(CTL + 4)) return;  // zero pivot / overflow recorded; 2: left to the general kernel
   // ---- finish: remap L rows to pivotal indices --------------------------------
   const int32_t lnnz = gLp[n];
-  for (int p = threadIdx.x; p < lnnz; p += blockDim.x) Li[p] = lds32(PINV + 4u * Li[p]);
+  for (int p = threadIdx.x; p < lnnz; p += blockDim.x) Li[p] = lds16(PINV + 2u * Li[p]);
   if (threadIdx.x == 0) {
     state[0] = FAC_DONE;
     state[1] = -1;
   }
 #undef PROW
-#undef LPS
+}
+
+// Half-bandwidth of the batch's pattern, max |row - col| (CSC, local rows).
+__global__ void band_kernel(int64_t cols, int32_t n, const int32_t* __restrict__ Ap,
+                            const int32_t* __restrict__ Ai, int32_t* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int d = 0;
+  if (t < cols) {
+    const int j = (int)(t % n);
+    for (int32_t e = Ap[t]; e < Ap[t + 1]; ++e) d = max(d, abs(Ai[e] - j));
+  }
+  d = (int)__reduce_max_sync(FULL, d);
+  if ((threadIdx.x & 31) == 0 && d > 0) atomicMax(out, d);
 }
 
 // Launches the compact kernel when it applies (complete LU, natural column
 // order, shared memory for the shadows plus a useful pattern capacity);
 // *launched = 0 otherwise.  Systems it could not finish keep FAC_RUNNING.
+//
+// Planning.  LU with row interchanges of a matrix of half-bandwidth w keeps
+// at most w + 1 entries in a column of L and 2w + 1 in a column of U, so a
+// column's pattern never exceeds 3w + 1 rows: the capacity to provide.  When
+// that is <= 256 the row -> position map fits one byte per row in shared
+// memory too (POS8), and the planner takes the largest warp count whose
+// capacity reaches the bound (c4: w = 78, bound 235, seven warps per system at
+// four systems per SM).  Otherwise the map stays in global scratch and the
+// capacity is whatever fits; columns beyond it send the system to ilu.cu.
 int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
   *launched = 0;
   if (a.B == 0 || a.n == 0 || a.q || a.cps > 1 || a.n > 65535) return RS_OK;
@@ -446,17 +488,44 @@ int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
   RS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const int W = a.warps <= 8 ? 8 : 16;
-  if (W != a.warps) return RS_OK;
+  if (a.warps != 8 && a.warps != 16) return RS_OK;
   // systems resident per SM: the whole batch in one wave when four fit
-  const int want = W == 8 ? std::min(4, std::max(1, (a.B + sms - 1) / sms)) : 1;
+  const int want = a.warps == 8 ? std::min(4, std::max(1, (a.B + sms - 1) / sms)) : 1;
   const size_t budget = std::min<size_t>((size_t)max_block, (size_t)per_sm / want - 1024);
-  const size_t fixed = lu_compact_smem_bytes(a.n, W, 0);
-  if (fixed + 18 * (size_t)W * 64 > budget) return RS_OK;
-  int capx = (int)((budget - fixed) / (18 * (size_t)W)) & ~7;
-  capx = std::min(capx, (a.n + 7) & ~7);
+  // structural bound on a column's pattern
+  int32_t bw = 0;
+  RS_CUDA_TRY(cudaMemsetAsync(a.gctl, 0, sizeof(int32_t), st));
+  const int64_t cols = (int64_t)a.B * a.n;
+  band_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(cols, a.n, a.Ap, a.Ai, a.gctl);
+  ::rs::count_launch();
+  RS_CUDA_TRY(cudaMemcpyAsync(&bw, a.gctl, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  RS_CUDA_TRY(cudaStreamSynchronize(st));
+  const int need = (int)std::min<int64_t>(a.n, 3 * (int64_t)bw + 1);
+  int W = 0, capx = 0, pos8 = 0;
+  if (need <= 256 && !getenv("RHOSOLVE_COMPACT_NOPOS8")) {
+    const int cand8[] = {8, 7, 6, 5, 4}, cand16[] = {16, 12, 8};
+    const int* cand = a.warps == 8 ? cand8 : cand16;
+    const int nc = a.warps == 8 ? 5 : 3;
+    for (int i = 0; i < nc && !W; ++i) {
+      const size_t fixed = lu_compact_smem_bytes(a.n, cand[i], 0, 1);
+      if (fixed >= budget) continue;
+      const int c = std::min(256, (int)((budget - fixed) / (18 * (size_t)cand[i])) & ~7);
+      if (c >= need) {
+        W = cand[i];
+        capx = std::min(c, (need + 7) & ~7);
+        pos8 = 1;
+      }
+    }
+  }
+  if (!W) {
+    W = a.warps;
+    const size_t fixed = lu_compact_smem_bytes(a.n, W, 0, 0);
+    if (fixed + 18 * (size_t)W * 64 > budget) return RS_OK;
+    capx = (int)((budget - fixed) / (18 * (size_t)W)) & ~7;
+    capx = std::min(capx, (std::max(need, 8) + 7) & ~7);
+  }
   if (const char* e = getenv("RHOSOLVE_COMPACT_CAPX")) capx = std::max(8, atoi(e) & ~7);  // tests
-  const size_t smem = lu_compact_smem_bytes(a.n, W, capx);
+  const size_t smem = lu_compact_smem_bytes(a.n, W, capx, pos8);
   if (smem > (size_t)max_block) return RS_OK;
   auto launch = [&](auto kern) -> int {
     RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -465,8 +534,12 @@ int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
   };
-  RS_TRY(W == 8 ? (want > 1 ? launch(lu_compact_kernel<256, 4>) : launch(lu_compact_kernel<256, 1>))
-                : launch(lu_compact_kernel<512, 1>));
+  if (W <= 8 && want > 1)
+    RS_TRY(pos8 ? launch(lu_compact_kernel<256, 4, true>) : launch(lu_compact_kernel<256, 4, false>));
+  else if (W <= 8)
+    RS_TRY(pos8 ? launch(lu_compact_kernel<256, 1, true>) : launch(lu_compact_kernel<256, 1, false>));
+  else
+    RS_TRY(pos8 ? launch(lu_compact_kernel<512, 1, true>) : launch(lu_compact_kernel<512, 1, false>));
   *launched = 1;
   return RS_OK;
 }
