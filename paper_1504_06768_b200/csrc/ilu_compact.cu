@@ -29,6 +29,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -208,7 +209,12 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
     while (true) {
       const int wend = (scanned + 31) >> 5;
       int c = -1;
-      while (w < wend) {
+      if (w < wend) {  // the current word first: one broadcast load, no vote
+        const uint32_t word = (uint32_t)lds32(BITS + 4u * w);
+        if (word) c = (w << 5) + __ffs(word) - 1;
+        else ++w;
+      }
+      while (c < 0 && w < wend) {
         const int ww = w + lane;
         const uint32_t bv = (ww < wend) ? (uint32_t)lds32(BITS + 4u * ww) : 0u;
         const unsigned m = __ballot_sync(FULL, bv != 0u);
@@ -253,66 +259,99 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
         scanned = d;
         continue;
       }
-      // pop column c: U entry = the value of its pivot row, final by now
-      const int pp = pos_get(lds16(PROW + 2u * c));
+      // pop column c.  The loads of L[:,c] are issued first (64 entries a
+      // pass, 96 when the column is longer: every c4 column in one pass); the
+      // U entry -- the value of c's pivot row, final by now -- and the
+      // bookkeeping overlap their latency.
       const int32_t p0 = lds32(LPS + 4u * c) + 1, p1 = lds32(LPS + 4u * c + 4u);
-      const double2 xc = lds2(XS + 16u * pp);
-      if (lane == 0) {
-        atoms_and(BITS + 4u * w, ~(1u << (c & 31)));
-        upos[unum] = pp;
-      }
-      ++unum;
-      // apply L[:,c], 64 entries per pass: every load of a pass is issued
-      // before any is consumed
-      for (int base = p0; base < p1; base += 64) {
+      double2 xc = make_double2(0.0, 0.0);
+      // one pass over NH x 32 entries from `base`; returns false on capacity overflow
+      auto pass = [&](auto nh, int base) -> bool {
+        constexpr int NH = decltype(nh)::value;
+        const int cnt = p1 - base;  // warp-uniform
         const int pa = base + lane;
-        const bool acta = pa < p1, actb = pa + 32 < p1;
-        int ia = 0, ib = 0;
-        double2 la = make_double2(0.0, 0.0), lb = la;
-        if (acta) {
-          ia = Li[pa];
-          la = Lx[pa];
-        }
-        if (actb) {
-          ib = Li[pa + 32];
-          lb = Lx[pa + 32];
-        }
-        int fa = acta ? pos_get(ia) : 0x7fffffff, fb = actb ? pos_get(ib) : 0x7fffffff;
-        bool ina = (unsigned)fa < (unsigned)npat, inb = (unsigned)fb < (unsigned)npat;
-        if (ina) ina = lds16(PATS + 2u * fa) == ia;
-        if (inb) inb = lds16(PATS + 2u * fb) == ib;
-        double2 xa = make_double2(0.0, 0.0), xb = xa;
-        if (ina) xa = lds2(XS + 16u * fa);
-        if (inb) xb = lds2(XS + 16u * fb);
-        const bool newa = acta && !ina, newb = actb && !inb;
-        const unsigned ma = __ballot_sync(FULL, newa);
-        const unsigned mb = __ballot_sync(FULL, newb);
-        if (ma | mb) {  // fill rows join the pattern in discovery order
-          const int na = __popc(ma), nb = __popc(mb);
-          if (npat + na + nb > capx) {
-            stop = 2;
-            break;
+        bool act[NH];
+        int ii[NH], ff[NH];
+        double2 ll[NH], xx[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          act[h] = lane + 32 * h < cnt;
+          ii[h] = 0;
+          ll[h] = make_double2(0.0, 0.0);
+          if (act[h]) {
+            ii[h] = Li[pa + 32 * h];
+            ll[h] = Lx[pa + 32 * h];
           }
+        }
+        if (base == p0) {
+          const int pp = pos_get(lds16(PROW + 2u * c));
+          xc = lds2(XS + 16u * pp);
+          if (lane == 0) {
+            atoms_and(BITS + 4u * w, ~(1u << (c & 31)));
+            upos[unum] = pp;
+          }
+          ++unum;
+        }
+        bool in[NH];
+        int rr[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          ff[h] = act[h] ? pos_get(ii[h]) : 0x7fffffff;
+          in[h] = (unsigned)ff[h] < (unsigned)npat;
+        }
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {  // row check and value of a candidate position together
+          rr[h] = -1;
+          xx[h] = make_double2(0.0, 0.0);
+          if (in[h]) {
+            rr[h] = lds16(PATS + 2u * ff[h]);
+            xx[h] = lds2(XS + 16u * ff[h]);
+          }
+        }
+        unsigned mm[NH], any = 0;
+        bool nw[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          nw[h] = act[h] && !(in[h] && rr[h] == ii[h]);
+          mm[h] = __ballot_sync(FULL, nw[h]);
+          any |= mm[h];
+        }
+        if (any) {  // fill rows join the pattern in discovery order
+          int tot = 0;
+#pragma unroll
+          for (int h = 0; h < NH; ++h) tot += __popc(mm[h]);
+          if (npat + tot > capx) return false;
           const unsigned lt = lanemask_lt();
-          if (newa) {
-            fa = npat + __popc(ma & lt);
-            sts16(PATS + 2u * fa, ia);
-            pos_set(ia, fa);
-            const int v = lds16(PINV + 2u * ia);
-            if (v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
+          int at = npat;
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            if (nw[h]) {
+              ff[h] = at + __popc(mm[h] & lt);
+              xx[h] = make_double2(0.0, 0.0);
+              sts16(PATS + 2u * ff[h], ii[h]);
+              pos_set(ii[h], ff[h]);
+              const int v = lds16(PINV + 2u * ii[h]);
+              if (v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
+            }
+            at += __popc(mm[h]);
           }
-          if (newb) {
-            fb = npat + na + __popc(mb & lt);
-            sts16(PATS + 2u * fb, ib);
-            pos_set(ib, fb);
-            const int v = lds16(PINV + 2u * ib);
-            if (v < scanned) atoms_or(BITS + 4u * (v >> 5), 1u << (v & 31));
-          }
-          npat += na + nb;
+          npat = at;
           __syncwarp();
         }
-        if (acta) sts2(XS + 16u * fa, csub(xa, cmul_plain(la, xc)));
-        if (actb) sts2(XS + 16u * fb, csub(xb, cmul_plain(lb, xc)));
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          if (act[h]) sts2(XS + 16u * ff[h], csub(xx[h], cmul_plain(ll[h], xc)));
+        return true;
+      };
+      {
+        bool ok = true;
+        int base = p0;
+        do {
+          const int cnt = p1 - base;
+          if (cnt > 64) ok = pass(std::integral_constant<int, 3>(), base), base += 96;
+          else ok = pass(std::integral_constant<int, 2>(), base), base += 64;
+        } while (ok && base < p1);
+        if (!ok) stop = 2;
       }
       if (stop) break;
       __syncwarp();
@@ -534,7 +573,9 @@ int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
   };
-  if (W <= 8 && want > 1)
+  if (W <= 7 && want > 1)  // (224 threads: 72 registers at four systems per SM)
+    RS_TRY(pos8 ? launch(lu_compact_kernel<224, 4, true>) : launch(lu_compact_kernel<224, 4, false>));
+  else if (W <= 8 && want > 1)
     RS_TRY(pos8 ? launch(lu_compact_kernel<256, 4, true>) : launch(lu_compact_kernel<256, 4, false>));
   else if (W <= 8)
     RS_TRY(pos8 ? launch(lu_compact_kernel<256, 1, true>) : launch(lu_compact_kernel<256, 1, false>));
