@@ -499,10 +499,14 @@ def kernel_timings(L, skw, torch, seeds):
     nLU = int(np.sum(f.lnnz) + np.sum(f.unnz))
     fact_s = timed(run_fact, reps=3)
     frontal = _lib.load().rs_debug_frontal_taken() == B  # rs_factorize's own choice
+    compact = bool(_lib.load().rs_debug_compact_taken())
     out["factorize"] = {
         "seconds": fact_s, "bytes": 20 * nnz + 20 * nLU + 8 * B * (n + 1),
-        "kernel": "frontal_lu_kernel" if frontal else "ilutp_pipeline_kernel",
-        "note": (f"{B} system(s), right-looking frontal complete LU (analysis + elimination "
+        "kernel": ("lu_compact_kernel" if compact else
+                   "frontal_lu_kernel" if frontal else "ilutp_pipeline_kernel"),
+        "note": (f"{B} system(s), column-pipelined left-looking complete LU, working column "
+                 "compact in shared memory" if compact else
+                 f"{B} system(s), right-looking frontal complete LU (analysis + elimination "
                  "+ finish)" if frontal else
                  f"{B} system(s), column-pipelined left-looking {'LU' if d == 0 else 'ILUTP'}")}
     x = torch.randn(B * n, dtype=torch.complex128, device="cuda")

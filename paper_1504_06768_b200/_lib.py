@@ -167,6 +167,8 @@ def load():
     lib.rs_tri_sell_keys.restype = _i64
     lib.rs_debug_frontal_taken.argtypes = []
     lib.rs_debug_frontal_taken.restype = _i32
+    lib.rs_debug_compact_taken.argtypes = []
+    lib.rs_debug_compact_taken.restype = _i32
     _lib = lib
     return lib
 

@@ -22,6 +22,7 @@ static std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static unsigned long long* g_factor_probe = nullptr;  // tuning hook
+static std::atomic<int> g_compact_taken{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -116,21 +117,21 @@ static int hybrid_frontal_count(int nsys, int n) {
   (void)n;
   return 0;
 }
-// Complete-LU batches: the compact shared-memory kernel (ilu_compact.cu).
-// RHOSOLVE_COMPACT=1/0 forces it on/off; auto: batches beyond three waves of
-// the frontal kernel.
+// Complete LU: the compact shared-memory kernel (ilu_compact.cu) takes every
+// batch size (measured against the frontal kernel and the general pipeline in
+// tools/lu_policy.py); RHOSOLVE_COMPACT=0 turns it off.
 static bool compact_enabled(int nsys) {
+  (void)nsys;
   if (const char* e = getenv("RHOSOLVE_COMPACT")) return e[0] == '1';
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return nsys > 3 * sms;
+  return true;
 }
 const char* rs_last_error(void) { return g_err; }
 long long rs_launch_count(void) { return g_launches.load(); }
 // Tuning hook (not part of the documented ABI): when set, the next
 // factorizations record per-column phase clocks of system 0 into buf[n*6].
 int rs_debug_frontal_taken(void) { return rs::frontal_last_taken(); }
+// 1 when the last rs_factorize ran the compact complete-LU kernel (ilu_compact.cu)
+int rs_debug_compact_taken(void) { return g_compact_taken.load(std::memory_order_relaxed); }
 
 int rs_weighted_mbm_host(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
                          const rs_complex* values, int64_t* forward) {
@@ -346,6 +347,9 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
   a.pinv = pinv;
   a.state = state;
   a.warps = nsys >= 148 ? 8 : 16;
+  // complete-LU batches of up to two systems per SM run 16 warps per system
+  // in the compact kernel (ilu_compact.cu)
+  if (!(drop_tol > 0.0) && fill_cap < 0 && !fill_caps && !q && nsys <= 2 * 148) a.warps = 16;
   a.hist = 1;
   a.b0 = 0;
   if (const char* e = getenv("RHOSOLVE_ILU_WARPS")) a.warps = atoi(e);  // tuning knob
@@ -419,7 +423,11 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
   // split is invisible in the output.
   const int hybrid_f = complete_lu ? hybrid_frontal_count(nsys, n) : 0;
   int compact = 0;
-  if (complete_lu && hybrid_f == 0 && compact_enabled(nsys)) {
+  g_compact_taken.store(0, std::memory_order_relaxed);
+  const bool frontal_auto = frontal_enabled(nsys);  // (also resets its "taken" counter)
+  const char* fenv = getenv("RHOSOLVE_FRONTAL");
+  const bool frontal_forced = fenv && fenv[0] == '1';
+  if (complete_lu && hybrid_f == 0 && !frontal_forced && compact_enabled(nsys)) {
     const int crc = launch_lu_compact(a, st, &compact);
     if (crc) {
       cudaFreeAsync(ws, st);
@@ -428,6 +436,7 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
   }
   if (compact) {
     // (whatever it left in FAC_RUNNING runs through the general kernel below)
+    g_compact_taken.store(1, std::memory_order_relaxed);
   } else if (hybrid_f > 0) {
     cudaStream_t side = nullptr;
     RS_TRY(side_stream(&side));
@@ -456,7 +465,7 @@ int rs_factorize_opts(int32_t nsys, int32_t n, const int32_t* Ap, const int32_t*
       cudaFreeAsync(ws, st);
       return rc;
     }
-  } else if (frontal_enabled(nsys) && complete_lu) {
+  } else if (frontal_auto && complete_lu) {
     // complete LU of small systems: right-looking frontal elimination in
     // shared memory; whatever it does not take (front too large, zero pivot)
     // runs through the column pipeline below

@@ -59,11 +59,11 @@ __device__ __forceinline__ int ld_cta(const int32_t* p) {
 
 // shared-memory bytes per CTA for `warps` warps and `capx` positions each
 // (pos8: the row -> position map lives in shared memory as one byte per row)
-size_t lu_compact_smem_bytes(int32_t n, int warps, int capx, int pos8) {
+size_t lu_compact_smem_bytes(int32_t n, int warps, int capx, int pos8, int ucap = 0) {
   const size_t nwords = ((size_t)n + 31) / 32;
   size_t b = 16 * (size_t)warps * capx + 4 * ((size_t)n + 1) + 4 * nwords * warps + 16 +
              2 * 2 * (size_t)n + 2 * (size_t)warps * capx;
-  if (pos8) b += (size_t)warps * n;
+  if (pos8) b += (size_t)warps * n + (size_t)warps * ucap;  // + U positions of the column
   return b;
 }
 
@@ -119,7 +119,7 @@ __device__ __forceinline__ T* pin(T* p) {
 // POS8: row -> position map as one byte per row in shared memory (capx <= 256);
 // otherwise int32 per row in per-warp global scratch.
 template <int MAXT, int MINB, bool POS8>
-__global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, int capx) {
+__global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, int capx, int ucap) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int b = blockIdx.x + a.b0;
@@ -138,7 +138,9 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
   uint32_t PINV = CTL + 16u;                                    // prow at +2n
   uint32_t PATS = PINV + 4u * (uint32_t)n + 2u * (uint32_t)(wid * capx);  // rows by position
   uint32_t POS = PINV + 4u * (uint32_t)n + 2u * (uint32_t)(W * capx) + (uint32_t)(wid * n);
-  asm volatile("" : "+r"(XS), "+r"(LPS), "+r"(PINV), "+r"(BITS), "+r"(PATS), "+r"(POS));
+  uint32_t UPOS = PINV + 4u * (uint32_t)n + 2u * (uint32_t)(W * capx) + (uint32_t)(W * n) +
+                  (uint32_t)(wid * ucap);  // POS8: positions of the column's U entries, pop order
+  asm volatile("" : "+r"(XS), "+r"(LPS), "+r"(PINV), "+r"(BITS), "+r"(PATS), "+r"(POS), "+r"(UPOS));
   const uint32_t n2 = 2u * (uint32_t)n;
 #define PROW (PINV + n2)
   constexpr int NONE = 0xffff;
@@ -265,6 +267,10 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
       // bookkeeping overlap their latency.
       const int32_t p0 = lds32(LPS + 4u * c) + 1, p1 = lds32(LPS + 4u * c + 4u);
       double2 xc = make_double2(0.0, 0.0);
+      if (POS8 && unum >= ucap) {  // (cannot happen within the structural bound)
+        stop = 2;
+        break;
+      }
       // one pass over NH x 32 entries from `base`; returns false on capacity overflow
       auto pass = [&](auto nh, int base) -> bool {
         constexpr int NH = decltype(nh)::value;
@@ -288,7 +294,8 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
           xc = lds2(XS + 16u * pp);
           if (lane == 0) {
             atoms_and(BITS + 4u * w, ~(1u << (c & 31)));
-            upos[unum] = pp;
+            if (POS8) sts8(UPOS + (uint32_t)unum, pp);
+            else upos[unum] = pp;
           }
           ++unum;
         }
@@ -471,7 +478,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
     int32_t* const Ui = a.Ui + (int64_t)b * a.capU;
     double2* const Ux = a.Ux + (int64_t)b * a.capU;
     for (int t = lane; t < unum; t += 32) {
-      const int p = upos[t];
+      const int p = POS8 ? lds8(UPOS + (uint32_t)t) : upos[t];
       Ui[unnz + t] = lds16(PINV + 2u * lds16(PATS + 2u * p));
       Ux[unnz + t] = lds2(XS + 16u * p);
     }
@@ -528,8 +535,9 @@ int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
   RS_CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
   RS_CUDA_TRY(cudaDeviceGetAttribute(&max_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   if (a.warps != 8 && a.warps != 16) return RS_OK;
-  // systems resident per SM: the whole batch in one wave when four fit
-  const int want = a.warps == 8 ? std::min(4, std::max(1, (a.B + sms - 1) / sms)) : 1;
+  // systems resident per SM: the whole batch in one wave (up to four per SM
+  // with 8-warp systems, two with 16-warp systems)
+  const int want = std::min(a.warps == 8 ? 4 : 2, std::max(1, (a.B + sms - 1) / sms));
   const size_t budget = std::min<size_t>((size_t)max_block, (size_t)per_sm / want - 1024);
   // structural bound on a column's pattern
   int32_t bw = 0;
@@ -540,13 +548,14 @@ int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
   RS_CUDA_TRY(cudaMemcpyAsync(&bw, a.gctl, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   RS_CUDA_TRY(cudaStreamSynchronize(st));
   const int need = (int)std::min<int64_t>(a.n, 3 * (int64_t)bw + 1);
+  const int ucap = (int)std::min<int64_t>(a.n, 2 * (int64_t)bw + 8);
   int W = 0, capx = 0, pos8 = 0;
   if (need <= 256 && !getenv("RHOSOLVE_COMPACT_NOPOS8")) {
     const int cand8[] = {8, 7, 6, 5, 4}, cand16[] = {16, 12, 8};
     const int* cand = a.warps == 8 ? cand8 : cand16;
     const int nc = a.warps == 8 ? 5 : 3;
     for (int i = 0; i < nc && !W; ++i) {
-      const size_t fixed = lu_compact_smem_bytes(a.n, cand[i], 0, 1);
+      const size_t fixed = lu_compact_smem_bytes(a.n, cand[i], 0, 1, ucap);
       if (fixed >= budget) continue;
       const int c = std::min(256, (int)((budget - fixed) / (18 * (size_t)cand[i])) & ~7);
       if (c >= need) {
@@ -564,23 +573,25 @@ int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
     capx = std::min(capx, (std::max(need, 8) + 7) & ~7);
   }
   if (const char* e = getenv("RHOSOLVE_COMPACT_CAPX")) capx = std::max(8, atoi(e) & ~7);  // tests
-  const size_t smem = lu_compact_smem_bytes(a.n, W, capx, pos8);
+  const size_t smem = lu_compact_smem_bytes(a.n, W, capx, pos8, ucap);
   if (smem > (size_t)max_block) return RS_OK;
   auto launch = [&](auto kern) -> int {
     RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<a.B, 32 * W, smem, st>>>(a, capx);
+    kern<<<a.B, 32 * W, smem, st>>>(a, capx, ucap);
     ::rs::count_launch();
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
   };
-  if (W <= 7 && want > 1)  // (224 threads: 72 registers at four systems per SM)
-    RS_TRY(pos8 ? launch(lu_compact_kernel<224, 4, true>) : launch(lu_compact_kernel<224, 4, false>));
-  else if (W <= 8 && want > 1)
-    RS_TRY(pos8 ? launch(lu_compact_kernel<256, 4, true>) : launch(lu_compact_kernel<256, 4, false>));
-  else if (W <= 8)
-    RS_TRY(pos8 ? launch(lu_compact_kernel<256, 1, true>) : launch(lu_compact_kernel<256, 1, false>));
-  else
+  if (W > 8 && want > 1)  // (two 16-warp systems per SM: 64 registers)
+    RS_TRY(pos8 ? launch(lu_compact_kernel<512, 2, true>) : launch(lu_compact_kernel<512, 2, false>));
+  else if (W > 8)
     RS_TRY(pos8 ? launch(lu_compact_kernel<512, 1, true>) : launch(lu_compact_kernel<512, 1, false>));
+  else if (W <= 7 && want > 1)  // (224 threads: 72 registers at four systems per SM)
+    RS_TRY(pos8 ? launch(lu_compact_kernel<224, 4, true>) : launch(lu_compact_kernel<224, 4, false>));
+  else if (want > 1)
+    RS_TRY(pos8 ? launch(lu_compact_kernel<256, 4, true>) : launch(lu_compact_kernel<256, 4, false>));
+  else
+    RS_TRY(pos8 ? launch(lu_compact_kernel<256, 1, true>) : launch(lu_compact_kernel<256, 1, false>));
   *launched = 1;
   return RS_OK;
 }
