@@ -10,7 +10,7 @@ python bench.py --steps 2 --warmup 3 --no-cpu > $O/p_c4_plain.log 2>&1 &&
 ncu --metrics $M --clock-control none --csv --log-file $O/r02_c4_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > $O/p_c4_ncu.log 2>&1
 # 2. c4: DRAM traffic of the hot kernels (factorization, solver, SpMV, apply)
-ncu --metrics $T --clock-control none -k regex:'ilutp_pipeline|steady_solver|spmv_warp|lu_solve_kernel|frontal_lu' \
+ncu --metrics $T --clock-control none -k regex:'lu_compact|ilutp_pipeline|steady_solver|spmv_warp|lu_solve_kernel|frontal_lu' \
     -c 24 -o $O/r02_c4_traffic python bench.py --steps 1 --warmup 3 --no-cpu > $O/p_c4_traffic.log 2>&1
 # 3. c5: launch list (one step) and traffic of SpMV / apply / solver
 python bench.py --config c5 --steps 1 --warmup 3 --no-cpu > $O/p_c5_plain.log 2>&1 &&
