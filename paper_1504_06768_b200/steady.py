@@ -16,6 +16,7 @@ config-4 parameter sweep) as one block-diagonal batch: one CTA per system.
 
 from __future__ import annotations
 
+import os
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -91,7 +92,8 @@ def start_vector(n, seed):
 _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="rhosolve-rng")
 
 
-_DRAW_POOL = ThreadPoolExecutor(max_workers=2, thread_name_prefix="rhosolve-draw")
+_DRAW_THREADS = max(1, int(os.environ.get("RHOSOLVE_DRAW_THREADS", "2")))
+_DRAW_POOL = ThreadPoolExecutor(max_workers=_DRAW_THREADS, thread_name_prefix="rhosolve-draw")
 
 
 def _start_vectors(n, seeds, pin=True):
@@ -99,8 +101,8 @@ def _start_vectors(n, seeds, pin=True):
     the upload is one asynchronous DMA.  Same bits as start_vector: one
     standard_normal(2n) call continues the PCG64 stream exactly as the
     reference's two calls of n (real part first), and default_rng(seed) is
-    Generator(PCG64(seed)); large batches are split over two threads (the
-    normal draws release the GIL)."""
+    Generator(PCG64(seed)); large batches are split over RHOSOLVE_DRAW_THREADS
+    threads (default 2: measured on the c4 step, 4 or 8 threads slow the launching thread down more than they shorten the draw)."""
     seeds = list(seeds)
     out = torch.empty(len(seeds) * n, dtype=torch.complex128, pin_memory=pin)
     view = out.numpy().reshape(len(seeds), n)
@@ -113,11 +115,12 @@ def _start_vectors(n, seeds, pin=True):
             view[i].imag = tmp[n:]
 
     m = len(seeds)
-    if m >= 64:
-        h = m // 2
-        fut = _DRAW_POOL.submit(part, h, m)
-        part(0, h)
-        fut.result()
+    if m >= 64 and _DRAW_THREADS > 1:
+        cuts = [m * t // _DRAW_THREADS for t in range(_DRAW_THREADS + 1)]
+        futs = [_DRAW_POOL.submit(part, cuts[t], cuts[t + 1]) for t in range(1, _DRAW_THREADS)]
+        part(0, cuts[1])
+        for fut in futs:
+            fut.result()
     else:
         part(0, m)
     return out
