@@ -277,6 +277,15 @@ int rs_trace_modify(int32_t nsys, int32_t n, int32_t D, const int32_t* rp,
 int rs_rcm(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
            int32_t* forward, int32_t* inverse, void* stream);
 
+/* Batch helper (no reference counterpart: the reference orders one matrix at
+ * a time, ordering.py:82-118).  *same (device int32) becomes 1 when every
+ * system of the block-diagonal batch stores exactly system 0's pattern (row
+ * extents and column indices; values may differ), else 0 -- the config-4
+ * sweep, which is then ordered once (`rs_rcm` on system 0) and the
+ * permutation replicated.  nnz = entries of the whole batch. */
+int rs_same_pattern(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, int64_t nnz,
+                    int32_t* same, void* stream);
+
 /* sparse.permute(a, p, p) (sparse.py:276-282): B[f[i], f[j]] = A[i, j]. */
 int rs_permute(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci,
                const rs_complex* v, const int32_t* forward, const int32_t* inverse,

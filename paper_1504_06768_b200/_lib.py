@@ -123,6 +123,7 @@ _SIGS = {
     "rs_trace_modify": [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                         ctypes.POINTER(_i64), _vp],
     "rs_rcm": [_i32, _i32, _vp, _vp, _vp, _vp, _vp],
+    "rs_same_pattern": [_i32, _i32, _vp, _vp, _i64, _vp, _vp],
     "rs_weighted_mbm_host": [_i64, _vp, _vp, _vp, _vp],
     "rs_col_min_degree_host": [_i64, _vp, _vp, _vp],
     "rs_permute": [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -53,6 +53,8 @@ int liouvillian_assemble(int32_t B, int32_t D, const int32_t* Hrp, const int32_t
                          const int32_t* const* Cci, const double2* const* Cv,
                          const int64_t* Cnnz, double* herm_dev, int32_t* out_rp,
                          int32_t* out_ci, double2* out_v, int64_t* nnz_out, cudaStream_t st);
+int same_pattern(int32_t B, int32_t n, const int32_t* rp, const int32_t* ci, int64_t nnz,
+                 int32_t* same, cudaStream_t st);
 int rcm_order(int B, int32_t n, const int32_t* rp, const int32_t* ci, int32_t* fwd,
               int32_t* inv, cudaStream_t st);
 int postprocess(int B, int32_t D, const double2* x, const int32_t* fwd, const int32_t* Lrp,
@@ -662,6 +664,13 @@ int rs_rcm(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, int32_
   RS_CHECK_ARG(nsys >= 0 && n >= 0, "negative size");
   if (!nsys || !n) return RS_OK;
   return rcm_order(nsys, n, rp, ci, forward, inverse, S(stream));
+}
+
+int rs_same_pattern(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, int64_t nnz,
+                    int32_t* same, void* stream) {
+  RS_CHECK_ARG(nsys >= 0 && n >= 0 && nnz >= 0, "negative size");
+  RS_CHECK_ARG(same != nullptr, "same is required");
+  return same_pattern(nsys, n, rp, ci, nnz, same, S(stream));
 }
 
 int rs_permute(int32_t nsys, int32_t n, const int32_t* rp, const int32_t* ci, const rs_complex* v,

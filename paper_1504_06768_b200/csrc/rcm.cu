@@ -244,4 +244,35 @@ int rcm_order(int B, int32_t n, const int32_t* rp, const int32_t* ci, int32_t* f
   return RS_OK;
 }
 
+__global__ void same_pattern_init_kernel(int32_t* same) { *same = 1; }
+
+// Every system of the batch stores system 0's pattern?  (rs_same_pattern)
+__global__ void same_pattern_kernel(int32_t B, int32_t n, int64_t per,
+                                    const int32_t* __restrict__ rp,
+                                    const int32_t* __restrict__ ci, int32_t* same) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nnz = per * B;
+  bool bad = false;
+  if (t < nnz && t >= per) bad = ci[t] != ci[t % per];
+  if (t < (int64_t)B * n) {  // row extents, relative to the system's first entry
+    const int64_t b = t / n;
+    bad = bad || (int64_t)rp[t] - b * per != (int64_t)rp[t - b * n];
+  }
+  if (t == 0) bad = bad || rp[(int64_t)B * n] != nnz;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *same = 0;
+}
+
+int same_pattern(int32_t B, int32_t n, const int32_t* rp, const int32_t* ci, int64_t nnz,
+                 int32_t* same, cudaStream_t st) {
+  const bool candidate = B > 1 && n > 0 && nnz % B == 0;
+  RS_CUDA_TRY(cudaMemsetAsync(same, 0, sizeof(int32_t), st));
+  if (!candidate) return RS_OK;
+  same_pattern_init_kernel<<<1, 1, 0, st>>>(same);
+  const int64_t work = nnz > (int64_t)B * n ? nnz : (int64_t)B * n;
+  same_pattern_kernel<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(B, n, nnz / B, rp, ci, same);
+  ::rs::count_launch();
+  RS_CUDA_TRY(cudaGetLastError());
+  return RS_OK;
+}
+
 }  // namespace rs

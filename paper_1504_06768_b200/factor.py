@@ -161,7 +161,8 @@ def factor_batch(M, drop_tol, fill_limit, raise_on_fail=True, capacity=None, eag
     if n == 0 or M.nnz == 0:
         raise SingularMatrixError("zero pivot at elimination step 0")
     incomplete = drop_tol > 0.0 or not math.isinf(fill_limit)
-    nnz_rows = M.row_ptr.diff().reshape(B, n).sum(1).cpu().numpy()
+    # entries per system: the row pointer at the system boundaries (one strided read)
+    nnz_rows = np.diff(M.row_ptr[::n].cpu().numpy().astype(np.int64))
     if math.isinf(fill_limit):
         cap = -1
     else:

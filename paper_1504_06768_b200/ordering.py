@@ -33,18 +33,11 @@ def shared_structure(M):
     """True when every system of a batch stores exactly system 0's pattern
     (same row extents and column indices; values may differ) -- the config-4
     sweep, whose instances differ only in a detuning."""
-    if M.nsys <= 1:
+    if M.nsys <= 1 or M.nnz % M.nsys:
         return False
-    nnz = M.nnz
-    if nnz % M.nsys:
-        return False
-    per = nnz // M.nsys
-    rp = M.row_ptr[:-1].view(M.nsys, M.n)
-    off = rp - rp[:, :1]
-    same = torch.logical_and(
-        (rp[:, 0] == torch.arange(M.nsys, device=rp.device, dtype=rp.dtype) * per).all(),
-        (off == off[0]).all())
-    same = torch.logical_and(same, (M.col_idx.view(M.nsys, per) == M.col_idx[:per]).all())
+    same = torch.empty(1, dtype=torch.int32, device=M.values.device)
+    _lib.call("rs_same_pattern", M.nsys, M.n, _lib.ptr(M.row_ptr), _lib.ptr(M.col_idx),
+              int(M.nnz), _lib.ptr(same), _lib.stream_ptr())
     return bool(same.item())
 
 

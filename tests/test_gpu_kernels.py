@@ -378,3 +378,36 @@ def test_apply_sliding_window_multi_consumer_bit_exact(cuda, monkeypatch):
         for w in ("1", "3", "6"):
             monkeypatch.setenv("RHOSOLVE_COL_CONSUMERS", w)
             assert bits_equal(factor.solve_lu(f, b), ref), (win, w)
+
+
+def test_shared_structure_detection(cuda):
+    """ordering.shared_structure: one RCM for a batch whose systems store
+    system 0's pattern; any differing row extent or column index disables it
+    (rs_same_pattern: one kernel, one flag)."""
+    import torch
+    from paper_1504_06768_b200 import ordering
+    from paper_1504_06768_b200.sparse import DeviceCSR
+    rp1 = torch.tensor([0, 2, 3, 5], dtype=torch.int32, device="cuda")
+    ci1 = torch.tensor([0, 2, 1, 0, 2], dtype=torch.int32, device="cuda")
+
+    def batch(rps, cis):
+        rp, ci, base = [], [], 0
+        for r, c in zip(rps, cis):
+            rp.append(r[:-1] + base)
+            ci.append(c)
+            base += int(r[-1])
+        rp.append(torch.tensor([base], dtype=torch.int32, device="cuda"))
+        ci = torch.cat(ci)
+        return DeviceCSR(3, len(rps), torch.cat(rp), ci,
+                         torch.zeros(ci.numel(), dtype=torch.complex128, device="cuda"))
+
+    assert ordering.shared_structure(batch([rp1] * 3, [ci1] * 3))
+    assert not ordering.shared_structure(batch([rp1], [ci1]))  # a single system
+    ci2 = torch.tensor([0, 2, 1, 1, 2], dtype=torch.int32, device="cuda")      # same extents, other column
+    assert not ordering.shared_structure(batch([rp1, rp1], [ci1, ci2]))
+    rp3 = torch.tensor([0, 1, 3, 5], dtype=torch.int32, device="cuda")         # same nnz, other extents
+    ci3 = torch.tensor([0, 1, 2, 0, 2], dtype=torch.int32, device="cuda")
+    assert not ordering.shared_structure(batch([rp1, rp3], [ci1, ci3]))
+    rp4 = torch.tensor([0, 1, 2, 3], dtype=torch.int32, device="cuda")         # other nnz
+    ci4 = torch.tensor([0, 1, 2], dtype=torch.int32, device="cuda")
+    assert not ordering.shared_structure(batch([rp1, rp4], [ci1, ci4]))

@@ -66,39 +66,6 @@ def test_jc_sweep_detunings():
     assert len(d) == 512 and d[0] == -3.0 and d[-1] == 3.0 and not np.any(d == 0.0)
 
 
-def test_shared_structure_detection():
-    """ordering.shared_structure: one RCM for a batch whose systems store
-    system 0's pattern; any differing row extent or column index disables it
-    (torch logic only, runs on CPU tensors)."""
-    import torch
-    from paper_1504_06768_b200 import ordering
-    from paper_1504_06768_b200.sparse import DeviceCSR
-    rp1 = torch.tensor([0, 2, 3, 5], dtype=torch.int32)
-    ci1 = torch.tensor([0, 2, 1, 0, 2], dtype=torch.int32)
-
-    def batch(rps, cis):
-        rp, ci, base = [], [], 0
-        for r, c in zip(rps, cis):
-            rp.append(r[:-1] + base)
-            ci.append(c)
-            base += int(r[-1])
-        rp.append(torch.tensor([base], dtype=torch.int32))
-        ci = torch.cat(ci)
-        return DeviceCSR(3, len(rps), torch.cat(rp), ci,
-                         torch.zeros(ci.numel(), dtype=torch.complex128))
-
-    assert ordering.shared_structure(batch([rp1] * 3, [ci1] * 3))
-    assert not ordering.shared_structure(batch([rp1], [ci1]))  # a single system
-    ci2 = torch.tensor([0, 2, 1, 1, 2], dtype=torch.int32)      # same extents, other column
-    assert not ordering.shared_structure(batch([rp1, rp1], [ci1, ci2]))
-    rp3 = torch.tensor([0, 1, 3, 5], dtype=torch.int32)         # same nnz, other extents
-    ci3 = torch.tensor([0, 1, 2, 0, 2], dtype=torch.int32)
-    assert not ordering.shared_structure(batch([rp1, rp3], [ci1, ci3]))
-    rp4 = torch.tensor([0, 1, 2, 3], dtype=torch.int32)         # other nnz
-    ci4 = torch.tensor([0, 1, 2], dtype=torch.int32)
-    assert not ordering.shared_structure(batch([rp1, rp4], [ci1, ci4]))
-
-
 @pytest.mark.parametrize("m", [1, 5, 100])
 def test_batch_start_vectors_match_reference_draw(m):
     """The batched draw (one standard_normal(2n) per seed, two threads for
