@@ -61,7 +61,7 @@ __device__ __forceinline__ int ld_cta(const int32_t* p) {
 // (pos8: the row -> position map lives in shared memory as one byte per row)
 size_t lu_compact_smem_bytes(int32_t n, int warps, int capx, int pos8, int ucap = 0) {
   const size_t nwords = ((size_t)n + 31) / 32;
-  size_t b = 16 * (size_t)warps * capx + 4 * ((size_t)n + 1) + 4 * nwords * warps + 16 +
+  size_t b = 16 * (size_t)warps * capx + 4 * ((size_t)n + 1) + 4 * nwords * warps + 16 + 128 +
              2 * 2 * (size_t)n + 2 * (size_t)warps * capx;
   if (pos8) b += (size_t)warps * n + (size_t)warps * ucap;  // + U positions of the column
   return b;
@@ -128,14 +128,15 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
   int32_t* state = a.state + 3 * (int64_t)b;
   if (state[0] != FAC_RUNNING) return;
 
-  // shared layout: xs[W][capx] c128 | Lp[n+1] i32 | bits[W][nwords] | ctl[4] |
+  // shared layout: xs[W][capx] c128 | Lp[n+1] i32 | bits[W][nwords] | ctl[4] | Up ring[32] |
   //                pinv[n] prow[n] u16 (0xffff: none) | pats[W][capx] u16 | pos8[W][n] u8
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
   uint32_t XS = s0 + 16u * (uint32_t)(wid * capx);  // this warp's values by position
   uint32_t LPS = s0 + 16u * (uint32_t)(W * capx);
   uint32_t BITS = LPS + 4u * ((uint32_t)n + 1u) + 4u * (uint32_t)(wid * nwords);
   const uint32_t CTL = LPS + 4u * ((uint32_t)n + 1u) + 4u * (uint32_t)(W * nwords);
-  uint32_t PINV = CTL + 16u;                                    // prow at +2n
+  const uint32_t UPR = CTL + 16u;  // Up[k], handed from column k-1's owner to column k's (k mod 32)
+  uint32_t PINV = UPR + 128u;                                   // prow at +2n
   uint32_t PATS = PINV + 4u * (uint32_t)n + 2u * (uint32_t)(wid * capx);  // rows by position
   uint32_t POS = PINV + 4u * (uint32_t)n + 2u * (uint32_t)(W * capx) + (uint32_t)(wid * n);
   uint32_t UPOS = PINV + 4u * (uint32_t)n + 2u * (uint32_t)(W * capx) + (uint32_t)(W * n) +
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
     sts32(LPS + 4u * (uint32_t)n, 0);
     sts32(CTL, 0);
     sts32(CTL + 4, 0);
+    sts32(UPR, 0);
     gLp[0] = 0;
     gUp[0] = 0;
   }
@@ -400,16 +402,20 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
         }
       }
     }
-    double gbest = best;
-    int gipiv = ipiv;
-    for (int o = 16; o; o >>= 1) {
-      const double ob = __shfl_xor_sync(FULL, gbest, o);
-      const int oi = __shfl_xor_sync(FULL, gipiv, o);
-      if (ob > gbest || (ob == gbest && oi >= 0 && (gipiv < 0 || oi < gipiv))) {
-        gbest = ob;
-        gipiv = oi;
-      }
-    }
+    // warp argmax of (magnitude, lowest row) with three redux.sync: non-negative
+    // doubles order like their bit patterns; a lane without a candidate (best
+    // = -1) contributes key 0 like a zero magnitude, and a best of 0 fails the
+    // pivot test below either way.  (A NaN never becomes a lane's best: the
+    // reference's comparisons fail on it too.)
+    const unsigned long long km =
+        best >= 0.0 ? (unsigned long long)__double_as_longlong(best) : 0ull;
+    const unsigned khi = (unsigned)(km >> 32), klo = (unsigned)km;
+    const unsigned mh = __reduce_max_sync(FULL, khi);
+    const unsigned ml = __reduce_max_sync(FULL, khi == mh ? klo : 0u);
+    const bool top = ipiv >= 0 && khi == mh && klo == ml;
+    const unsigned br = __reduce_min_sync(FULL, top ? (unsigned)ipiv : 0xffffffffu);
+    const int gipiv = br == 0xffffffffu ? -1 : (int)br;
+    const double gbest = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
     if (gipiv < 0 || gbest == 0.0) {
       if (lane == 0) {
         state[0] = FAC_ZERO_PIVOT;
@@ -424,7 +430,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
 
     // ---- 4. emit L (unit diagonal first), publish the column, then U -------
     const int32_t lnnz = lds32(LPS + 4u * k);
-    const int32_t unnz = ld_cta(gUp + k);
+    const int32_t unnz = lds32(UPR + 4u * (k & 31));
     if ((int64_t)unnz + unum + 1 > a.capU || (int64_t)lnnz + lnum > a.capL) {
       if (lane == 0) {
         state[0] = FAC_OVERFLOW;
@@ -464,14 +470,18 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
     __threadfence_block();
     __syncwarp();
     if (lane == 0) {
-      gUp[k + 1] = unnz + unum + 1;
-      gLp[k + 1] = off;
+      // only shared-memory state is published on the critical path (the fence
+      // has no global store of this lane to wait for); the global copies the
+      // kernel itself never reads follow the release
       sts32(LPS + 4u * k + 4u, off);
       sts16(PINV + 2u * gipiv, k);
-      gpinv[gipiv] = k;
       sts16(PROW + 2u * k, gipiv);
+      sts32(UPR + 4u * ((k + 1) & 31), unnz + unum + 1);
       __threadfence_block();  // release column k
       sts32(CTL, k + 1);
+      gUp[k + 1] = unnz + unum + 1;
+      gLp[k + 1] = off;
+      gpinv[gipiv] = k;
     }
     // U column k (pops were ascending; pivot last): no later column reads it,
     // so it is written after the release, off the critical path
