@@ -143,3 +143,16 @@ def test_compact_output_overflow_resumes(cuda):
     m = _c4(40)
     f = factor.factor_batch(from_host(_host(m)), 0.0, math.inf, capacity=20000)
     _check(f, 0, m)
+
+
+def test_hybrid_frontal_pipeline_split_same_factors(cuda, monkeypatch):
+    """The measured-and-disabled experiment of DESIGN.md (RHOSOLVE_HYBRID_F: the
+    first F systems in the 64-register frontal build, the rest in pipeline CTAs
+    without shared-memory state on a side stream) still produces the factors
+    of the default path."""
+    A = _c4_batch_device(12)
+    a = factor.factor_batch(A, 0.0, math.inf)
+    monkeypatch.setenv("RHOSOLVE_HYBRID_F", "5")
+    b = factor.factor_batch(A, 0.0, math.inf)
+    assert _compact_taken() == 0 and int(_lib.load().rs_debug_frontal_taken()) == 5
+    _same_factors(a, b)
