@@ -41,7 +41,7 @@ constexpr int GT = 256;      // threads per CTA: 255 registers per thread, so th
                               // registers sweep_slice spilled ~1 KB per call and a
                               // dependency hop cost 4,460 cycles after the sources
                               // were loaded)
-constexpr int SP_UNROLL = 4;  // SpMV: chunks of 32 products per warp pass
+constexpr int SP_UNROLL = 12;  // SpMV: 12 x 32 products in flight per warp (8 warps per SM have to cover the HBM latency)
 constexpr int SP_CH = 32 * SP_UNROLL;
 constexpr int SP_SLOTS = SP_CH + SP_CH / 8;
 

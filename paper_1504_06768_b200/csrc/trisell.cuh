@@ -190,6 +190,20 @@ __device__ __noinline__ void sweep_loop(const TriSell& T, const double2* rhs, do
   for (int32_t s = first; s < T.nslices; s += stride) sweep_slice<UPPER, G>(T, s, rhs, out, rd);
 }
 
+// The sweep bodies are reached through a table of function pointers, i.e. by
+// an INDIRECT call: that forces the standard ABI on them (compiled on their
+// own with the full register budget; the caller saves what it needs around
+// the call, once per sweep).  Called directly from the solver kernel, ptxas'
+// interprocedural register allocation confined them to the registers the
+// Krylov code leaves free (R144 and up) and the polling loop spilled on every
+// step: the same sweeps ran 1.9x slower inside grid_solver_kernel than in
+// grid_apply_kernel (2.70 + 1.57 ms vs 1.38 + 0.85 ms per apply on config 5).
+typedef void (*sweep_fn_t)(const TriSell&, const double2*, double2*, const double2*, int32_t,
+                           int32_t);
+__device__ sweep_fn_t g_sweep_table[2][4] = {
+    {sweep_loop<false, 1>, sweep_loop<false, 2>, sweep_loop<false, 4>, sweep_loop<false, 32>},
+    {sweep_loop<true, 1>, sweep_loop<true, 2>, sweep_loop<true, 4>, sweep_loop<true, 32>}};
+
 template <bool UPPER>
 __device__ __forceinline__ void sweep_grid(const TriSell& T, const double2* rhs, double2* out,
                                            const double2* rd) {
@@ -199,12 +213,10 @@ __device__ __forceinline__ void sweep_grid(const TriSell& T, const double2* rhs,
   if (lw >= apw) return;
   const int32_t stride = apw * (int32_t)gridDim.x;
   const int32_t first = lw * (int32_t)gridDim.x + blockIdx.x;
-  switch (T.G) {  // the layouts levels.cu is asked for: 32, 16, 8 or 1 rows per slice
-    case 1: sweep_loop<UPPER, 1>(T, rhs, out, rd, first, stride); break;
-    case 2: sweep_loop<UPPER, 2>(T, rhs, out, rd, first, stride); break;
-    case 4: sweep_loop<UPPER, 4>(T, rhs, out, rd, first, stride); break;
-    default: sweep_loop<UPPER, 32>(T, rhs, out, rd, first, stride); break;
-  }
+  // the layouts levels.cu is asked for: 32, 16, 8 or 1 rows per slice
+  const int idx = T.G == 1 ? 0 : T.G == 2 ? 1 : T.G == 4 ? 2 : 3;
+  sweep_fn_t fn = *(volatile sweep_fn_t*)&g_sweep_table[UPPER ? 1 : 0][idx];
+  fn(T, rhs, out, rd, first, stride);
 }
 
 }  // namespace tri
