@@ -41,7 +41,7 @@ constexpr int GT = 256;      // threads per CTA: 255 registers per thread, so th
                               // registers sweep_slice spilled ~1 KB per call and a
                               // dependency hop cost 4,460 cycles after the sources
                               // were loaded)
-constexpr int SP_UNROLL = 12;  // SpMV: 12 x 32 products in flight per warp (8 warps per SM have to cover the HBM latency)
+constexpr int SP_UNROLL = 8;  // SpMV: chunks of 8 x 32 products per warp pass (two chunks in flight)
 constexpr int SP_CH = 32 * SP_UNROLL;
 constexpr int SP_SLOTS = SP_CH + SP_CH / 8;
 
@@ -135,9 +135,15 @@ __device__ __forceinline__ double2 gvdot(Q& q, int n, const double2* a, const do
   return make_double2(o[0], o[1]);
 }
 
-// y = A x, bit-exact with csr_matvec (_ckernels.pyx:34-50); the body of
+// y = A x, bit-exact with csr_matvec (_ckernels.pyx:34-50); the arithmetic of
 // spmv_warp_kernel (spmv.cu) for one system, warps striding over 32-row
-// groups.  Barriers: x complete before, y complete after.
+// groups.  Only 8 warps per SM run here (the sweeps need the registers), so
+// every warp keeps the NEXT chunk's CSR entries in flight -- of this group or
+// of its next group, whose row pointers were fetched a group earlier -- while
+// it gathers x, stages the products and folds the current chunk (in-solver
+// SpMV on config 5: 0.96 ms with 4 chunks of 32 in flight per warp, 0.73 ms
+// with 12, then this software pipeline).  Barriers: x complete before, y
+// complete after.
 __device__ __noinline__ void g_spmv(Q& q, int n, const int32_t* __restrict__ rp,
                        const int32_t* __restrict__ ci, const double2* __restrict__ v,
                        const double2* x, double2* y) {
@@ -145,24 +151,46 @@ __device__ __noinline__ void g_spmv(Q& q, int n, const int32_t* __restrict__ rp,
   const int lane = threadIdx.x & 31;
   double2* s_p = q.stage;
   const int ngroups = (n + 31) >> 5;
-  for (int grp = q.gw; grp < ngroups; grp += q.ngw) {
-    const int r0 = grp << 5;
-    const int r1 = min(r0 + 32, n);
-    const int row = r0 + lane;
-    const bool have = row < r1;
-    const int32_t base = __ldg(rp + r0), end = __ldg(rp + r1);
-    const int32_t p0 = have ? __ldg(rp + row) : 0, p1 = have ? __ldg(rp + row + 1) : 0;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int32_t cb = base; cb < end; cb += SP_CH) {
-      const int32_t ce = min(cb + SP_CH, end);
-      int c[SP_UNROLL];
-      double2 a[SP_UNROLL];
+  int grp = q.gw;
+  if (grp < ngroups) {
+    // header of a group: entry range of its 32 rows and of this lane's row
+    auto header = [&](int g, int32_t& b, int32_t& e, int32_t& a0, int32_t& a1) {
+      const int r0 = g << 5, r1 = min(r0 + 32, n), row = r0 + lane;
+      b = __ldg(rp + r0);
+      e = __ldg(rp + r1);
+      a0 = row < r1 ? __ldg(rp + row) : 0;
+      a1 = row < r1 ? __ldg(rp + row + 1) : 0;
+    };
+    int32_t base, end, p0, p1, nb = 0, ne = 0, np0 = 0, np1 = 0;
+    header(grp, base, end, p0, p1);
+    if (grp + q.ngw < ngroups) header(grp + q.ngw, nb, ne, np0, np1);
+    int c[SP_UNROLL], nc[SP_UNROLL];
+    double2 a[SP_UNROLL], na[SP_UNROLL];
+    int32_t cb = base;
 #pragma unroll
-      for (int u = 0; u < SP_UNROLL; ++u) {
-        const int32_t e = cb + 32 * u + lane;
-        if (e < ce) {
-          c[u] = __ldg(ci + e);
-          a[u] = ldg2(v + e);
+    for (int u = 0; u < SP_UNROLL; ++u) {
+      const int32_t e = cb + 32 * u + lane;
+      if (e < min(cb + SP_CH, end)) {
+        c[u] = __ldg(ci + e);
+        a[u] = ldg2(v + e);
+      }
+    }
+    double2 acc = make_double2(0.0, 0.0);
+    while (true) {
+      const int32_t ce = min(cb + SP_CH, end);
+      // the chunk after this one: same group, or the first of the next group
+      const bool same = cb + SP_CH < end;
+      const bool more = same || grp + q.ngw < ngroups;
+      const int32_t ncb = same ? cb + SP_CH : nb;
+      const int32_t nce = min(ncb + SP_CH, same ? end : ne);
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < SP_UNROLL; ++u) {
+          const int32_t e = ncb + 32 * u + lane;
+          if (e < nce) {
+            nc[u] = __ldg(ci + e);
+            na[u] = ldg2(v + e);
+          }
         }
       }
 #pragma unroll
@@ -181,8 +209,25 @@ __device__ __noinline__ void g_spmv(Q& q, int n, const int32_t* __restrict__ rp,
         acc = (t == p0) ? pq : cadd(acc, pq);
       }
       __syncwarp();
+      if (!same) {  // last chunk of the group: its rows are complete
+        const int row = (grp << 5) + lane;
+        if (row < n) y[row] = acc;
+        if (!more) break;
+        grp += q.ngw;
+        base = nb;
+        end = ne;
+        p0 = np0;
+        p1 = np1;
+        acc = make_double2(0.0, 0.0);
+        if (grp + q.ngw < ngroups) header(grp + q.ngw, nb, ne, np0, np1);
+      }
+      cb = ncb;
+#pragma unroll
+      for (int u = 0; u < SP_UNROLL; ++u) {
+        c[u] = nc[u];
+        a[u] = na[u];
+      }
     }
-    if (have) y[row] = acc;
   }
   q.g.sync();
 }
