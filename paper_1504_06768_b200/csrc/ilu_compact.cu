@@ -15,17 +15,22 @@
 // exactly that: ~415 warp instructions per applied L column.  Here
 //   * the values of the column's pattern sit in shared memory BY POSITION
 //     (xs[pos], discovery order = the reference's pattern order) next to the
-//     row of every position (pats[pos], u16);
-//   * a per-warp global array holds only pos_of[row], validated as a sparse
-//     set: row i is in the pattern iff p = pos_of[i] < npat and pats[p] == i
-//     -- so it never needs clearing and stale contents are harmless;
-//   * pinv / prow / Lp shadows and the pending bitmaps are shared memory too.
-// One global load per touched row remains; the value traffic, the pattern
-// list, the candidate list and the pivot search run on 32-bit shared-memory
-// addresses.  A column whose pattern outgrows the per-warp capacity stops
-// the system untouched (state stays FAC_RUNNING) and ilu.cu's general kernel
-// factors it afterwards; capacity overflow of the output and zero pivots are
-// reported exactly as ilu.cu does.
+//     row of every position (pats[pos], u16), so the pivot search and both
+//     emissions are plain scans over positions;
+//   * the row -> position map is validated as a sparse set: row i is in the
+//     pattern iff p = pos[i] < npat and pats[p] == i -- it never needs
+//     clearing and stale contents are harmless.  When the structural bound on
+//     a column's pattern (3w+1 for half-bandwidth w, see launch_lu_compact)
+//     is <= 256 the map is one byte per row in shared memory (POS8), else an
+//     int32 per row in per-warp global scratch;
+//   * pinv / prow (u16 shadows), Lp, the pending bitmaps, the U positions of
+//     the column and Up[k] (a ring handed from column to column) are shared
+//     memory too, all addressed with explicit 32-bit ld/st.shared.
+// With POS8 the only global traffic of a pop is the L column itself.  A
+// column whose pattern outgrows the per-warp capacity (int32 variant only)
+// stops the system untouched (state stays FAC_RUNNING) and ilu.cu's general
+// kernel factors it afterwards; capacity overflow of the output and zero
+// pivots are reported exactly as ilu.cu does.
 #include <stdlib.h>
 
 #include <algorithm>
@@ -47,12 +52,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 __device__ __forceinline__ int warp_min_i(int v) {
   return (int)__reduce_min_sync(FULL, v);
-}
-// another warp of the CTA wrote it: CTA-scope relaxed load
-__device__ __forceinline__ int ld_cta(const int32_t* p) {
-  int v;
-  asm volatile("ld.relaxed.cta.s32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
 }
 
 }  // namespace
