@@ -579,6 +579,10 @@ int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
     const size_t fixed = lu_compact_smem_bytes(a.n, W, 0, 0);
     if (fixed + 18 * (size_t)W * 64 > budget) return RS_OK;
     capx = (int)((budget - fixed) / (18 * (size_t)W)) & ~7;
+    // complete LU fills its band, so the bound is nearly reached (c4: 228 of
+    // 235): a capacity below it would abandon the system half-way and leave
+    // the whole factorization to ilu.cu anyway
+    if (capx < need) return RS_OK;
     capx = std::min(capx, (std::max(need, 8) + 7) & ~7);
   }
   if (const char* e = getenv("RHOSOLVE_COMPACT_CAPX")) capx = std::max(8, atoi(e) & ~7);  // tests
