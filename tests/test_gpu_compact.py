@@ -156,3 +156,23 @@ def test_hybrid_frontal_pipeline_split_same_factors(cuda, monkeypatch):
     b = factor.factor_batch(A, 0.0, math.inf)
     assert _compact_taken() == 0 and int(_lib.load().rs_debug_frontal_taken()) == 5
     _same_factors(a, b)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 64])
+def test_compact_tiny_systems(cuda, n):
+    """Orders around and below a warp: n = 1 (a lone pivot), a full 2 x 2, ragged
+    bands -- the planner's capacities clamp to n and the factors stay the oracle's."""
+    rng = np.random.default_rng(100 + n)
+    mats = [_random_system(rng, n, band=max(1, min(n - 1, int(rng.integers(1, 6)))), density=0.7,
+                           ints=bool(k % 2)) for k in range(6)]
+    f = factor.factor_batch(from_host([_host(m) for m in mats]), 0.0, math.inf,
+                            raise_on_fail=False)
+    assert _compact_taken() == 1
+    for b, m in enumerate(mats):
+        try:
+            O.factorize_raw(m, 0.0, math.inf)
+        except O.Breakdown as e:
+            assert f.fail[b] == e.step
+            continue
+        assert f.fail[b] < 0
+        _check(f, b, m)
