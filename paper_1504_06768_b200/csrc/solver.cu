@@ -148,6 +148,9 @@ __device__ void psolve(const Ctx& C, const double2* in, double2* out) {
   }
 }
 
+typedef void (*psolve_fn_t)(const SolverArgs*, const double2*, double2*);
+__device__ psolve_fn_t g_csc_psolve = csc_psolve;
+
 __device__ void psolve_body(const Ctx& C, const double2* in, double2* out) {
   const int n = C.n;
   if (!C.have_M) {
@@ -159,7 +162,11 @@ __device__ void psolve_body(const Ctx& C, const double2* in, double2* out) {
   double2* P = C.y;
   double2* Q = C.y2;
   if (C.csc) {  // reference column loops on shared memory (colsweep.cuh)
-    csc_psolve(C.sa, in, out);
+    // reached by an indirect call: the standard ABI gives the sweeps their
+    // own register allocation instead of what the Krylov code leaves free
+    // (see trisell.cuh: the same direct call cost the grid solver 1.9x)
+    psolve_fn_t fn = *(volatile psolve_fn_t*)&g_csc_psolve;
+    fn(C.sa, in, out);
     return;
   }
   const double2 s = cta::sentinel2();
