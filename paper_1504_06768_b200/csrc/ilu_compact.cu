@@ -169,6 +169,8 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
     sts32(LPS + 4u * i, 0);
   }
   for (int w = lane; w < nwords; w += 32) sts32(BITS + 4u * w, 0);
+  if (POS8)  // the byte map is kept exact: 0xff = not in the working column
+    for (int i = lane; i < n; i += 32) sts8(POS + (uint32_t)i, 0xff);
   if (threadIdx.x == 0) {
     sts32(LPS + 4u * (uint32_t)n, 0);
     sts32(CTL, 0);
@@ -251,7 +253,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
         for (int m = scanned + lane; m < d; m += 32) {
           const int r = lds16(PROW + 2u * m);
           const int p = pos_get(r);
-          if ((unsigned)p < (unsigned)npat && lds16(PATS + 2u * p) == r) {
+          if (POS8 ? p != 0xff : ((unsigned)p < (unsigned)npat && lds16(PATS + 2u * p) == r)) {
             atoms_or(BITS + 4u * (m >> 5), 1u << (m & 31));
             newlow = min(newlow, m);
           }
@@ -305,14 +307,14 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           ff[h] = act[h] ? pos_get(ii[h]) : 0x7fffffff;
-          in[h] = (unsigned)ff[h] < (unsigned)npat;
+          in[h] = POS8 ? (act[h] && ff[h] != 0xff) : (unsigned)ff[h] < (unsigned)npat;
         }
 #pragma unroll
         for (int h = 0; h < NH; ++h) {  // row check and value of a candidate position together
           rr[h] = -1;
           xx[h] = make_double2(0.0, 0.0);
           if (in[h]) {
-            rr[h] = lds16(PATS + 2u * ff[h]);
+            if (!POS8) rr[h] = lds16(PATS + 2u * ff[h]);  // sparse-set check (int32 map only)
             xx[h] = lds2(XS + 16u * ff[h]);
           }
         }
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
         bool nw[NH];
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          nw[h] = act[h] && !(in[h] && rr[h] == ii[h]);
+          nw[h] = act[h] && !(in[h] && (POS8 || rr[h] == ii[h]));
           mm[h] = __ballot_sync(FULL, nw[h]);
           any |= mm[h];
         }
@@ -495,6 +497,8 @@ __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, in
       Ui[unnz + unum] = k;
       Ux[unnz + unum] = piv;
     }
+    if (POS8)  // the column leaves the byte map
+      for (int t = lane; t < npat; t += 32) sts8(POS + (uint32_t)lds16(PATS + 2u * t), 0xff);
     __syncwarp();
   }
   __syncthreads();
@@ -559,14 +563,14 @@ int launch_lu_compact(const FactorArgs& a, cudaStream_t st, int* launched) {
   const int need = (int)std::min<int64_t>(a.n, 3 * (int64_t)bw + 1);
   const int ucap = (int)std::min<int64_t>(a.n, 2 * (int64_t)bw + 8);
   int W = 0, capx = 0, pos8 = 0;
-  if (need <= 256 && !getenv("RHOSOLVE_COMPACT_NOPOS8")) {
+  if (need <= 248 && !getenv("RHOSOLVE_COMPACT_NOPOS8")) {  // (position 0xff = absent)
     const int cand8[] = {8, 7, 6, 5, 4}, cand16[] = {16, 12, 8};
     const int* cand = a.warps == 8 ? cand8 : cand16;
     const int nc = a.warps == 8 ? 5 : 3;
     for (int i = 0; i < nc && !W; ++i) {
       const size_t fixed = lu_compact_smem_bytes(a.n, cand[i], 0, 1, ucap);
       if (fixed >= budget) continue;
-      const int c = std::min(256, (int)((budget - fixed) / (18 * (size_t)cand[i])) & ~7);
+      const int c = std::min(248, (int)((budget - fixed) / (18 * (size_t)cand[i])) & ~7);
       if (c >= need) {
         W = cand[i];
         capx = std::min(c, (need + 7) & ~7);
