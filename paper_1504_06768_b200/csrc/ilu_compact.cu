@@ -17,12 +17,14 @@
 //     (xs[pos], discovery order = the reference's pattern order) next to the
 //     row of every position (pats[pos], u16), so the pivot search and both
 //     emissions are plain scans over positions;
-//   * the row -> position map is validated as a sparse set: row i is in the
-//     pattern iff p = pos[i] < npat and pats[p] == i -- it never needs
-//     clearing and stale contents are harmless.  When the structural bound on
-//     a column's pattern (3w+1 for half-bandwidth w, see launch_lu_compact)
-//     is <= 256 the map is one byte per row in shared memory (POS8), else an
-//     int32 per row in per-warp global scratch;
+//   * the row -> position map: when the structural bound on a column's
+//     pattern (3w+1 for half-bandwidth w, see launch_lu_compact) is <= 248 it
+//     is one byte per row in shared memory (POS8), kept exact -- 0xff =
+//     absent, and a column clears its own rows when it leaves -- so membership
+//     and position are one load; else an int32 per row in per-warp global
+//     scratch validated as a sparse set (row i is in the pattern iff
+//     p = pos[i] < npat and pats[p] == i: never cleared, stale contents are
+//     harmless);
 //   * pinv / prow (u16 shadows), Lp, the pending bitmaps, the U positions of
 //     the column and Up[k] (a ring handed from column to column) are shared
 //     memory too, all addressed with explicit 32-bit ld/st.shared.
@@ -115,7 +117,7 @@ __device__ __forceinline__ T* pin(T* p) {
   return p;
 }
 
-// POS8: row -> position map as one byte per row in shared memory (capx <= 256);
+// POS8: row -> position map as one byte per row in shared memory (capx <= 248, 0xff = absent);
 // otherwise int32 per row in per-warp global scratch.
 template <int MAXT, int MINB, bool POS8>
 __global__ void __launch_bounds__(MAXT, MINB) lu_compact_kernel(FactorArgs a, int capx, int ucap) {
@@ -533,7 +535,7 @@ __global__ void band_kernel(int64_t cols, int32_t n, const int32_t* __restrict__
 // Planning.  LU with row interchanges of a matrix of half-bandwidth w keeps
 // at most w + 1 entries in a column of L and 2w + 1 in a column of U, so a
 // column's pattern never exceeds 3w + 1 rows: the capacity to provide.  When
-// that is <= 256 the row -> position map fits one byte per row in shared
+// that is <= 248 the row -> position map fits one byte per row in shared
 // memory too (POS8), and the planner takes the largest warp count whose
 // capacity reaches the bound (c4: w = 78, bound 235, seven warps per system at
 // four systems per SM).  Otherwise the map stays in global scratch and the
